@@ -1,0 +1,114 @@
+/* ds_blstm.h — C ABI of libds: the B200 (sm_100a) hot path of arXiv
+ * 1904.04956 behind the reference `distsgd` plug-in points.
+ *
+ * Conventions
+ *   - every function returns 0 on success or a negative DS_ERR_* code and never
+ *     throws; ds_last_error() returns a thread-local message for the last
+ *     failure of the calling thread;
+ *   - all tensor pointers are DEVICE pointers owned by the caller (PyTorch);
+ *     all work is asynchronous on the given cudaStream_t; nothing allocates
+ *     after ds_blstm_create;
+ *   - weights/gradients are flat float32 vectors in the canonical BLSTM
+ *     packing documented in paper_1904_04956_b200/csrc/layout.h (the
+ *     reference's flat-float64 convention, objectives.py:3-5, at 4 B/param).
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/distsgd/...).
+ */
+#ifndef DS_BLSTM_H
+#define DS_BLSTM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DS_OK 0
+#define DS_ERR_ARG (-1)       /* shape / config error  -> ValueError   */
+#define DS_ERR_CUDA (-2)      /* CUDA failure          -> RuntimeError */
+#define DS_ERR_NONFINITE (-3) /* non-finite loss/grad  -> ValueError   */
+
+typedef struct ds_blstm ds_blstm;
+typedef void* ds_stream_t; /* cudaStream_t */
+
+typedef struct {
+  int32_t layers;     /* bidirectional LSTM layers (paper: 6)             */
+  int32_t input_dim;  /* feature dim (paper: 260), <= 272                 */
+  int32_t bottleneck; /* linear bottleneck units (paper: 256), %64 == 0   */
+  int32_t classes;    /* soft-max outputs (paper: 32000), %16 == 0        */
+  int32_t frames;     /* unrolled frames T (paper: 21)                    */
+  int32_t max_batch;  /* workspace is sized for this many sequences       */
+} ds_blstm_cfg;       /* hidden size is fixed at 512 cells per direction  */
+
+/* Number of parameters of the packed model (objective.param_dim,
+ * objectives.py:93-95 for the reference's tiny-mlp analogue). */
+int64_t ds_blstm_param_dim(const ds_blstm_cfg* cfg);
+
+/* Objective construction (objectives.py:111-131 make_objective). */
+int ds_blstm_create(const ds_blstm_cfg* cfg, int device, ds_blstm** out);
+int ds_blstm_destroy(ds_blstm* h);
+
+/* Bind the device-resident dataset (objectives.py:23-43 Dataset):
+ * feats bf16 [n_seq, frames, 272] (columns >= input_dim zero), labels int32
+ * [n_seq, frames].  Pointers are borrowed. */
+int ds_blstm_set_dataset(ds_blstm* h, const void* feats_bf16, const int32_t* labels, int64_t n_seq);
+
+/* K2: operand snapshot of theta (the copy `snap = st.weights.copy()` of
+ * engines/adpsgd.py:132-134 that the gradient is computed on). */
+int ds_blstm_cast_snapshot(ds_blstm* h, const float* theta, ds_stream_t stream);
+
+/* K1,K3-K8: gradient(objective, snapshot, batch, dataset)
+ * (objectives.py:236-263): grad <- d/dtheta mean-over-frames CE of the
+ * minibatch `idx` (int64 [B], device).  *loss_sum <- sum of per-frame CE
+ * (device float); *nonfinite |= 1 when the loss is not finite.  Uses the
+ * snapshot set by the last ds_blstm_cast_snapshot / ds_sgd_momentum. */
+int ds_blstm_fwd_bwd(ds_blstm* h, const int64_t* idx, int32_t B, float* grad, float* loss_sum, int32_t* nonfinite,
+                     ds_stream_t stream);
+
+/* K13: evaluate/heldout_loss forward only (objectives.py:223-233, 286-291). */
+int ds_blstm_loss(ds_blstm* h, const int64_t* idx, int32_t B, float* loss_sum, int32_t* nonfinite,
+                  ds_stream_t stream);
+
+/* K9 (+K2 fused): sgd_step (optim.py:109-121): v <- mu*v + g;
+ * theta <- theta - lr*v; if snap_owner != NULL also refresh its operand
+ * snapshot from the new theta.  *nonfinite |= 1 on a non-finite gradient. */
+int ds_sgd_momentum(float* theta, float* v, const float* g, float lr, float mu, int64_t n, ds_blstm* snap_owner,
+                    int32_t* nonfinite, ds_stream_t stream);
+
+/* K10: adpsgd_mix (engines/adpsgd.py:36-43) + the receiver's atomic
+ * reply-and-mix (:280-286): a <- b <- (a + b) / 2, the identical fp32 value
+ * stored to both sides (peer pointer allowed: NVLink P2P). */
+int ds_adpsgd_mix(float* theta_a, float* theta_b, int64_t n, ds_stream_t stream);
+
+/* K11/K12: RingAllreduceGroup.allreduce (collective.py:122-163) fused with
+ * the SSGD update of engines/ssgd.py:85-87, executed for the chunks owned by
+ * `rank` of make_chunk_plan(n, world, nchunks) (collective.py:79-95):
+ *   mode 0: g_mean = (sum in canonical owner-first ring order) / world, then
+ *           per-member sgd_step; results stored into every member's buffers;
+ *   mode 1: theta <- (canonical sum of theta) / world for every member
+ *           (epoch consensus, engines/adpsgd.py:293-295; Hybrid pull).
+ * Arrays hold one device pointer per member (peer pointers allowed).
+ * snap_owners may be NULL or hold per-member handles to refresh. */
+int ds_group_reduce(int32_t world, int32_t rank, float* const* grads, float* const* thetas, float* const* vels,
+                    ds_blstm* const* snap_owners, int64_t n, int32_t nchunks, float lr, float mu, int32_t mode,
+                    ds_stream_t stream);
+
+/* GEMM self-test hook (tests only): C[M,N] f32 = A . B^T with bf16 operands,
+ * a_mn/b_mn select MN-major storage ([K][M] / [K][N]). */
+int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C,
+                       int64_t ldc, int32_t M, int32_t N, int32_t K, ds_stream_t stream);
+
+/* Recurrent-kernel self-test hooks (tests only): run one bidirectional layer's
+ * forward / backward recurrence on caller buffers (layouts of lstm_rec.cu). */
+int ds_debug_lstm_fwd(int32_t B, int32_t T, void* gates, float* cstate, void* y_full, const void* whh,
+                      uint32_t* counters, ds_stream_t stream);
+int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* cstate, const void* whhT, const void* dy,
+                      void* dg, uint32_t* counters, ds_stream_t stream);
+
+const char* ds_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DS_BLSTM_H */

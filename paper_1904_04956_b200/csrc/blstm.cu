@@ -1,0 +1,493 @@
+// blstm.cu — the ds_blstm handle: workspace, operand snapshot and the full
+// training-step schedule of the paper BLSTM issued as one CUDA
+// graph per (batch, buffer) binding.  Implements the C ABI of
+// include/ds_blstm.h.
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../include/ds_blstm.h"
+#include "ds_internal.h"
+#include "layout.h"
+#include "lstm_rec.h"
+#include "ops.h"
+
+using namespace ds;
+
+struct ds_blstm {
+  ds_blstm_cfg cfg;
+  ModelLayout L;
+  int device = 0;
+  int T = 0, Bmax = 0;
+  int64_t Nmax = 0;
+  int ntiles_c = 0;
+  // dataset (borrowed)
+  const __nv_bfloat16* feats = nullptr;
+  const int32_t* labels = nullptr;
+  int64_t n_seq = 0;
+  // one device allocation holding everything below
+  void* arena = nullptr;
+  // operand snapshot
+  __nv_bfloat16* snap = nullptr;
+  __nv_bfloat16* whhT = nullptr;
+  __nv_bfloat16* wih0pad = nullptr;
+  float* bias_snap = nullptr;
+  int64_t* d_whh_offs = nullptr;
+  // activations
+  __nv_bfloat16* x0 = nullptr;
+  int32_t* lab = nullptr;
+  std::vector<__nv_bfloat16*> gates, yfull;
+  std::vector<float*> cstate;
+  __nv_bfloat16* z = nullptr;
+  float2* stats = nullptr;
+  float* tgt = nullptr;
+  float* lse = nullptr;
+  __nv_bfloat16* dlogits = nullptr;
+  __nv_bfloat16* dz = nullptr;
+  __nv_bfloat16* dy = nullptr;
+  __nv_bfloat16* dg = nullptr;
+  float* colpart = nullptr;
+  uint32_t* counters = nullptr;
+  // graph cache
+  struct Key {
+    int B;
+    const int64_t* idx;
+    float* grad;
+    float* loss;
+    int* flag;
+    int bwd;
+    bool operator==(const Key& o) const {
+      return B == o.B && idx == o.idx && grad == o.grad && loss == o.loss && flag == o.flag && bwd == o.bwd;
+    }
+  };
+  struct Entry {
+    Key key;
+    cudaGraphExec_t exec;
+  };
+  std::vector<Entry> graphs;
+};
+
+namespace {
+
+struct Arena {
+  size_t off = 0;
+  template <class T>
+  T* take(char* base, size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+int carve(ds_blstm* h, char* base, size_t* total) {
+  Arena a;
+  const ModelLayout& L = h->L;
+  const int64_t N = h->Nmax;
+  h->snap = a.take<__nv_bfloat16>(base, L.total);
+  h->whhT = a.take<__nv_bfloat16>(base, (size_t)L.layers * kGates2 * kHidden);
+  h->wih0pad = a.take<__nv_bfloat16>(base, (size_t)kGates2 * kInPad);
+  h->bias_snap = a.take<float>(base, (size_t)L.layers * kGates2 + L.bottleneck + L.classes);
+  h->d_whh_offs = a.take<int64_t>(base, L.layers);
+  h->x0 = a.take<__nv_bfloat16>(base, (size_t)N * kInPad);
+  h->lab = a.take<int32_t>(base, N);
+  h->gates.resize(L.layers);
+  h->cstate.resize(L.layers);
+  h->yfull.resize(L.layers);
+  for (int l = 0; l < L.layers; ++l) {
+    h->gates[l] = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
+    h->cstate[l] = a.take<float>(base, (size_t)N * kLayerOut);
+    h->yfull[l] = a.take<__nv_bfloat16>(base, (size_t)(h->T + 2) * h->Bmax * kLayerOut);
+  }
+  h->z = a.take<__nv_bfloat16>(base, (size_t)N * L.bottleneck);
+  h->stats = a.take<float2>(base, (size_t)h->ntiles_c * N);
+  h->tgt = a.take<float>(base, N);
+  h->lse = a.take<float>(base, N);
+  h->dlogits = a.take<__nv_bfloat16>(base, (size_t)N * L.classes);
+  h->dz = a.take<__nv_bfloat16>(base, (size_t)N * L.bottleneck);
+  h->dy = a.take<__nv_bfloat16>(base, (size_t)N * kLayerOut);
+  h->dg = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
+  int64_t cp = op_colsum_scratch(L.classes > kGates2 ? L.classes : kGates2);
+  h->colpart = a.take<float>(base, cp);
+  h->counters = a.take<uint32_t>(base, 2 * ((h->Bmax + 127) / 128) + 64);
+  *total = a.off + 256;
+  return DS_OK;
+}
+
+int validate_cfg(const ds_blstm_cfg* c) {
+  if (!c) return fail_arg("null config");
+  if (c->layers < 1 || c->layers > kMaxLayers) return fail_arg("layers must be in 1..16");
+  if (c->input_dim < 1 || c->input_dim > kInPad) return fail_arg("input_dim must be in 1..272");
+  if (c->bottleneck < 64 || c->bottleneck % 64) return fail_arg("bottleneck must be a positive multiple of 64");
+  if (c->classes < 16 || c->classes % 16) return fail_arg("classes must be a positive multiple of 16");
+  if (c->frames < 1 || c->frames > 1024) return fail_arg("frames must be in 1..1024");
+  if (c->max_batch < 1 || c->max_batch > 65536) return fail_arg("max_batch must be in 1..65536");
+  return DS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// The step schedule.  Forward always runs; backward when `grad` != nullptr.
+int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, int* flag, cudaStream_t s) {
+  const ModelLayout& L = h->L;
+  const int T = h->T;
+  const int N = T * B;
+  const int Lh = L.layers;
+  const int bott = L.bottleneck, C = L.classes;
+  const float* bias_l = h->bias_snap;
+  const float* bias_b = h->bias_snap + (size_t)Lh * kGates2;
+  const float* bias_o = bias_b + bott;
+  int rc;
+#define TRY(x)            \
+  do {                    \
+    if ((rc = (x))) return rc; \
+  } while (0)
+
+  TRY(op_gather(idx, B, T, h->feats, h->labels, h->n_seq, h->x0, h->lab, flag, s));
+  for (int l = 0; l < Lh; ++l) {
+    DS_CUDA_TRY(cudaMemsetAsync(h->yfull[l], 0, (size_t)B * kLayerOut * 2, s));
+    DS_CUDA_TRY(cudaMemsetAsync(h->yfull[l] + (size_t)(T + 1) * B * kLayerOut, 0, (size_t)B * kLayerOut * 2, s));
+  }
+  auto Y = [&](int l) { return h->yfull[l] + (size_t)B * kLayerOut; };
+
+  // ---- forward ----
+  for (int l = 0; l < Lh; ++l) {
+    GemmBatch gb;
+    memset(&gb, 0, sizeof(gb));
+    gb.nprob = 1;
+    GemmProblem& p = gb.p[0];
+    if (l == 0)
+      TRY(gemm_problem(&p, h->x0, kInPad, 0, h->wih0pad, kInPad, 0, N, kGates2, kInPad));
+    else
+      TRY(gemm_problem(&p, Y(l - 1), kLayerOut, 0, h->snap + L.off_wih[l], kLayerOut, 0, N, kGates2, kLayerOut));
+    p.epi = EPI_BF16;
+    p.out = h->gates[l];
+    p.ldo = kGates2;
+    p.bias = bias_l + (size_t)l * kGates2;
+    TRY(gemm_launch(&gb, s));
+    LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], nullptr, nullptr,
+                     h->counters};
+    TRY(lstm_forward(la, s));
+  }
+  {
+    GemmBatch gb;
+    memset(&gb, 0, sizeof(gb));
+    gb.nprob = 1;
+    GemmProblem& p = gb.p[0];
+    TRY(gemm_problem(&p, Y(Lh - 1), kLayerOut, 0, h->snap + L.off_wb, kLayerOut, 0, N, bott, kLayerOut));
+    p.epi = EPI_BF16;
+    p.out = h->z;
+    p.ldo = bott;
+    p.bias = bias_b;
+    TRY(gemm_launch(&gb, s));
+  }
+  {
+    GemmBatch gb;
+    memset(&gb, 0, sizeof(gb));
+    gb.nprob = 1;
+    GemmProblem& p = gb.p[0];
+    TRY(gemm_problem(&p, h->z, bott, 0, h->snap + L.off_wo, bott, 0, N, C, bott));
+    p.epi = EPI_CE_STATS;
+    p.bias = bias_o;
+    p.labels = h->lab;
+    p.stats = h->stats;
+    p.stats_ld = (int)h->Nmax;
+    p.tgt = h->tgt;
+    TRY(gemm_launch(&gb, s));
+    TRY(op_ce_combine(h->stats, p.tiles_n, h->Nmax, h->tgt, N, h->lse, loss, flag, s));
+  }
+  if (!grad) return DS_OK;
+
+  // ---- backward ----
+  {
+    GemmBatch gb;
+    memset(&gb, 0, sizeof(gb));
+    gb.nprob = 1;
+    GemmProblem& p = gb.p[0];
+    TRY(gemm_problem(&p, h->z, bott, 0, h->snap + L.off_wo, bott, 0, N, C, bott));
+    p.epi = EPI_CE_GRAD;
+    p.bias = bias_o;
+    p.labels = h->lab;
+    p.lse = h->lse;
+    p.out = h->dlogits;
+    p.ldo = C;
+    p.scale = 1.0f / (float)N;
+    TRY(gemm_launch(&gb, s));
+  }
+  {
+    GemmBatch gb;
+    memset(&gb, 0, sizeof(gb));
+    gb.nprob = 2;
+    GemmProblem& p0 = gb.p[0];  // dW_o = dlogits^T Z
+    TRY(gemm_problem(&p0, h->dlogits, C, 1, h->z, bott, 1, C, bott, N));
+    p0.epi = EPI_F32;
+    p0.out = grad + L.off_wo;
+    p0.ldo = bott;
+    GemmProblem& p1 = gb.p[1];  // dZ = dlogits W_o
+    TRY(gemm_problem(&p1, h->dlogits, C, 0, h->snap + L.off_wo, bott, 1, N, bott, C));
+    p1.epi = EPI_BF16;
+    p1.out = h->dz;
+    p1.ldo = bott;
+    TRY(gemm_launch(&gb, s));
+    TRY(op_colsum(h->dlogits, N, C, C, h->colpart, grad + L.off_bo, s));
+  }
+  {
+    GemmBatch gb;
+    memset(&gb, 0, sizeof(gb));
+    gb.nprob = 2;
+    GemmProblem& p0 = gb.p[0];  // dW_b = dZ^T Y
+    TRY(gemm_problem(&p0, h->dz, bott, 1, Y(Lh - 1), kLayerOut, 1, bott, kLayerOut, N));
+    p0.epi = EPI_F32;
+    p0.out = grad + L.off_wb;
+    p0.ldo = kLayerOut;
+    GemmProblem& p1 = gb.p[1];  // dY = dZ W_b
+    TRY(gemm_problem(&p1, h->dz, bott, 0, h->snap + L.off_wb, kLayerOut, 1, N, kLayerOut, bott));
+    p1.epi = EPI_BF16;
+    p1.out = h->dy;
+    p1.ldo = kLayerOut;
+    TRY(gemm_launch(&gb, s));
+    TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, s));
+  }
+  for (int l = Lh - 1; l >= 0; --l) {
+    LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->whhT + (size_t)l * kGates2 * kHidden, h->dy,
+                     h->dg, h->counters};
+    TRY(lstm_backward(la, s));
+    GemmBatch gb;
+    memset(&gb, 0, sizeof(gb));
+    GemmProblem& p0 = gb.p[0];  // dW_ih = dG^T X
+    if (l == 0) {
+      TRY(gemm_problem(&p0, h->dg, kGates2, 1, h->x0, kInPad, 1, kGates2, kInPad, N));
+      p0.n_valid = L.input_dim;
+      p0.ldo = L.input_dim;
+    } else {
+      TRY(gemm_problem(&p0, h->dg, kGates2, 1, Y(l - 1), kLayerOut, 1, kGates2, kLayerOut, N));
+      p0.ldo = kLayerOut;
+    }
+    p0.epi = EPI_F32;
+    p0.out = grad + L.off_wih[l];
+    for (int d = 0; d < 2; ++d) {  // dW_hh[dir] = dG_dir^T H_prev_dir
+      GemmProblem& p = gb.p[1 + d];
+      const __nv_bfloat16* hp = d == 0 ? h->yfull[l] : h->yfull[l] + (size_t)2 * B * kLayerOut + kHidden;
+      TRY(gemm_problem(&p, h->dg + d * kGates, kGates2, 1, hp, kLayerOut, 1, kGates, kHidden, N));
+      p.epi = EPI_F32;
+      p.out = grad + L.off_whh[l] + (size_t)d * kGates * kHidden;
+      p.ldo = kHidden;
+    }
+    gb.nprob = 3;
+    if (l > 0) {  // dY_{l-1} = dG W_ih
+      GemmProblem& p3 = gb.p[3];
+      TRY(gemm_problem(&p3, h->dg, kGates2, 0, h->snap + L.off_wih[l], kLayerOut, 1, N, kLayerOut, kGates2));
+      p3.epi = EPI_BF16;
+      p3.out = h->dy;
+      p3.ldo = kLayerOut;
+      gb.nprob = 4;
+    }
+    TRY(gemm_launch(&gb, s));
+    TRY(op_colsum(h->dg, N, kGates2, kGates2, h->colpart, grad + L.off_b[l], s));
+  }
+#undef TRY
+  return DS_OK;
+}
+
+bool use_graphs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_NO_GRAPH");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, int* flag, cudaStream_t s) {
+  if (B < 1 || B > h->Bmax) return fail_arg("batch size out of range 1..max_batch");
+  if (!h->feats) return fail_arg("dataset not bound (ds_blstm_set_dataset)");
+  if (!loss) return fail_arg("loss_sum pointer is required");
+  DS_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStreamCaptureStatus cs;
+  DS_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+  if (!use_graphs() || cs != cudaStreamCaptureStatusNone) return issue_step(h, idx, B, grad, loss, flag, s);
+  ds_blstm::Key key{B, idx, grad, loss, flag, grad != nullptr};
+  for (auto& e : h->graphs)
+    if (e.key == key) {
+      DS_CUDA_TRY(cudaGraphLaunch(e.exec, s));
+      return DS_OK;
+    }
+  cudaStream_t cap;
+  DS_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  DS_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  int rc = issue_step(h, idx, B, grad, loss, flag, cap);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(cap, &g);
+  cudaStreamDestroy(cap);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ce != cudaSuccess) return fail_cuda(ce, "cudaStreamEndCapture");
+  cudaGraphExec_t ex;
+  ce = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return fail_cuda(ce, "cudaGraphInstantiate");
+  if (h->graphs.size() >= 16) {
+    cudaGraphExecDestroy(h->graphs.front().exec);
+    h->graphs.erase(h->graphs.begin());
+  }
+  h->graphs.push_back({key, ex});
+  DS_CUDA_TRY(cudaGraphLaunch(ex, s));
+  return DS_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int64_t ds_blstm_param_dim(const ds_blstm_cfg* c) {
+  if (validate_cfg(c)) return -1;
+  return make_layout(c->layers, c->input_dim, c->bottleneck, c->classes).total;
+}
+
+int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
+  int rc = validate_cfg(c);
+  if (rc) return rc;
+  if (!out) return fail_arg("null output handle");
+  DS_CUDA_TRY(cudaSetDevice(device));
+  ds_blstm* h = new ds_blstm();
+  h->cfg = *c;
+  h->L = make_layout(c->layers, c->input_dim, c->bottleneck, c->classes);
+  h->device = device;
+  h->T = c->frames;
+  h->Bmax = c->max_batch;
+  h->Nmax = (int64_t)c->frames * c->max_batch;
+  h->ntiles_c = (c->classes + kGemmBN - 1) / kGemmBN;
+  size_t total = 0;
+  carve(h, nullptr, &total);
+  cudaError_t e = cudaMalloc(&h->arena, total);
+  if (e != cudaSuccess) {
+    delete h;
+    return fail_cuda(e, "cudaMalloc(workspace)");
+  }
+  carve(h, reinterpret_cast<char*>(h->arena), &total);
+  std::vector<int64_t> offs(h->L.layers);
+  for (int l = 0; l < h->L.layers; ++l) offs[l] = h->L.off_whh[l];
+  e = cudaMemcpy(h->d_whh_offs, offs.data(), sizeof(int64_t) * offs.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(h->counters, 0, sizeof(uint32_t) * 64);
+  if (e != cudaSuccess) {
+    cudaFree(h->arena);
+    delete h;
+    return fail_cuda(e, "workspace init");
+  }
+  *out = h;
+  return DS_OK;
+}
+
+int ds_blstm_destroy(ds_blstm* h) {
+  if (!h) return DS_OK;
+  cudaSetDevice(h->device);
+  for (auto& e : h->graphs) cudaGraphExecDestroy(e.exec);
+  if (h->arena) cudaFree(h->arena);
+  delete h;
+  return DS_OK;
+}
+
+int ds_blstm_set_dataset(ds_blstm* h, const void* feats, const int32_t* labels, int64_t n_seq) {
+  if (!h || !feats || !labels || n_seq < 1) return fail_arg("bad dataset binding");
+  h->feats = reinterpret_cast<const __nv_bfloat16*>(feats);
+  h->labels = labels;
+  h->n_seq = n_seq;
+  for (auto& e : h->graphs) cudaGraphExecDestroy(e.exec);
+  h->graphs.clear();
+  return DS_OK;
+}
+
+int ds_blstm_cast_snapshot(ds_blstm* h, const float* theta, ds_stream_t stream) {
+  if (!h || !theta) return fail_arg("null argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DS_CUDA_TRY(cudaSetDevice(h->device));
+  int rc = op_cast(theta, h->L.total, h->snap, s);
+  if (rc) return rc;
+  return op_snapshot_aux(theta, h->L, h->d_whh_offs, h->whhT, h->wih0pad, h->bias_snap, s);
+}
+
+int ds_blstm_fwd_bwd(ds_blstm* h, const int64_t* idx, int32_t B, float* grad, float* loss_sum, int32_t* nonfinite,
+                     ds_stream_t stream) {
+  if (!h || !idx || !grad) return fail_arg("null argument");
+  return run_step(h, idx, B, grad, loss_sum, nonfinite, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_blstm_loss(ds_blstm* h, const int64_t* idx, int32_t B, float* loss_sum, int32_t* nonfinite,
+                  ds_stream_t stream) {
+  if (!h || !idx) return fail_arg("null argument");
+  return run_step(h, idx, B, nullptr, loss_sum, nonfinite, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_sgd_momentum(float* theta, float* v, const float* g, float lr, float mu, int64_t n, ds_blstm* snap_owner,
+                    int32_t* nonfinite, ds_stream_t stream) {
+  if (!theta || !v || !g || n < 0) return fail_arg("null argument");
+  if (!(lr > 0.f)) return fail_arg("learning rate must be > 0");
+  if (snap_owner && snap_owner->L.total != n) return fail_arg("snapshot owner has a different param_dim");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int rc = op_sgd(theta, v, g, lr, mu, n, snap_owner ? snap_owner->snap : nullptr, nonfinite, s);
+  if (rc || !snap_owner) return rc;
+  return op_snapshot_aux(theta, snap_owner->L, snap_owner->d_whh_offs, snap_owner->whhT, snap_owner->wih0pad,
+                         snap_owner->bias_snap, s);
+}
+
+int ds_adpsgd_mix(float* a, float* b, int64_t n, ds_stream_t stream) {
+  if (!a || !b || n < 0) return fail_arg("null argument");
+  return op_mix(a, b, n, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_group_reduce(int32_t world, int32_t rank, float* const* grads, float* const* thetas, float* const* vels,
+                    ds_blstm* const* snap_owners, int64_t n, int32_t nchunks, float lr, float mu, int32_t mode,
+                    ds_stream_t stream) {
+  if (!thetas || n < 1) return fail_arg("null argument");
+  if (rank < 0 || rank >= world) return fail_arg("rank out of range");
+  if (mode != 0 && mode != 1) return fail_arg("mode must be 0 (sgd) or 1 (average)");
+  if (mode == 0 && !(lr > 0.f)) return fail_arg("learning rate must be > 0");
+  __nv_bfloat16* snaps[kMaxGroup] = {};
+  bool any = false;
+  if (snap_owners)
+    for (int r = 0; r < world && r < kMaxGroup; ++r)
+      if (snap_owners[r]) {
+        snaps[r] = snap_owners[r]->snap;
+        any = true;
+      }
+  return op_group_reduce(world, rank, grads, thetas, vels, any ? snaps : nullptr, n, nchunks, lr, mu, mode,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C,
+                       int64_t ldc, int32_t M, int32_t N, int32_t K, ds_stream_t stream) {
+  GemmBatch gb;
+  memset(&gb, 0, sizeof(gb));
+  gb.nprob = 1;
+  int rc = gemm_problem(&gb.p[0], A, lda, a_mn, B, ldb, b_mn, M, N, K);
+  if (rc) return rc;
+  gb.p[0].epi = EPI_F32;
+  gb.p[0].out = C;
+  gb.p[0].ldo = ldc;
+  return gemm_launch(&gb, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_debug_lstm_fwd(int32_t B, int32_t T, void* gates, float* cstate, void* y_full, const void* whh,
+                      uint32_t* counters, ds_stream_t stream) {
+  LstmLayerArgs a{B, T, reinterpret_cast<__nv_bfloat16*>(gates), cstate, reinterpret_cast<__nv_bfloat16*>(y_full),
+                  reinterpret_cast<const __nv_bfloat16*>(whh), nullptr, nullptr, counters};
+  return lstm_forward(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* cstate, const void* whhT, const void* dy,
+                      void* dg, uint32_t* counters, ds_stream_t stream) {
+  LstmLayerArgs a{B,
+                  T,
+                  const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(gates)),
+                  const_cast<float*>(cstate),
+                  nullptr,
+                  reinterpret_cast<const __nv_bfloat16*>(whhT),
+                  reinterpret_cast<const __nv_bfloat16*>(dy),
+                  reinterpret_cast<__nv_bfloat16*>(dg),
+                  counters};
+  return lstm_backward(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

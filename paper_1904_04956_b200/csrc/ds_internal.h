@@ -1,0 +1,94 @@
+// ds_internal.h — host-side interfaces shared by the .cu translation units of
+// libds (not part of the public C ABI in include/ds_blstm.h).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <string>
+
+namespace ds {
+
+// ---------------------------------------------------------------------------
+// error plumbing: every C-ABI entry returns 0 or a negative code and records a
+// thread-local message (ds_last_error()).
+#ifndef DS_OK
+#define DS_OK 0
+#define DS_ERR_ARG (-1)       /* bad shape / config (maps to ValueError) */
+#define DS_ERR_CUDA (-2)      /* CUDA runtime/driver failure (RuntimeError) */
+#define DS_ERR_NONFINITE (-3) /* non-finite loss/gradient (ValueError) */
+#endif
+void set_error(const std::string& msg);
+int fail_arg(const std::string& msg);
+int fail_cuda(cudaError_t e, const char* where);
+
+#define DS_CUDA_TRY(expr)                                  \
+  do {                                                     \
+    cudaError_t _e = (expr);                               \
+    if (_e != cudaSuccess) return ::ds::fail_cuda(_e, #expr); \
+  } while (0)
+
+int num_sms();
+
+// ---------------------------------------------------------------------------
+// TMA descriptors
+// 2D row-major tensor [outer][inner] of `elem_bytes` elements, row pitch in
+// bytes; box = box_inner x box_outer elements; SWIZZLE_128B (box_inner *
+// elem_bytes must be 128).
+int make_tmap_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t outer,
+                 uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer);
+
+// ---------------------------------------------------------------------------
+// GEMM: C[m, n] = sum_k A[m, k] * B[n, k], bf16 operands, fp32 accumulate in
+// TMEM (tcgen05), persistent tile loop, up to kMaxProblems per launch.
+//
+// Operand storage:
+//   a_mn = 0: A stored [M][K] (K contiguous)   a_mn = 1: A stored [K][M]
+//   b_mn = 0: B stored [N][K] (K contiguous)   b_mn = 1: B stored [K][N]
+enum Epilogue : int {
+  EPI_BF16 = 0,      // out bf16 [M, ldo] = acc (+ bias[n])
+  EPI_F32 = 1,       // out f32  [M, ldo] = acc*scale (+ out if accumulate)
+  EPI_CE_STATS = 2,  // per-row partial (max, sumexp) of acc+bias[n] over n < n_valid, target logit
+  EPI_CE_GRAD = 3,   // out bf16 = (exp(acc+bias-lse[m]) - [n==label[m]]) * scale
+};
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBN = 256;
+constexpr int kGemmBK = 64;
+constexpr int kMaxProblems = 4;
+
+struct GemmProblem {
+  CUtensorMap tmA;  // 64-byte aligned (first member)
+  CUtensorMap tmB;
+  int M, N, K;
+  int a_mn, b_mn;
+  int epi;
+  int tiles_m, tiles_n, tile_begin;
+  int n_valid;      // columns >= n_valid are not stored (and masked in CE)
+  int m_valid;      // rows >= m_valid are not stored
+  long long ldo;    // output row pitch in elements
+  void* out;
+  const float* bias;
+  float scale;
+  int accumulate;
+  // CE
+  const int* labels;      // [m_valid]
+  const float* lse;       // [m_valid]
+  float2* stats;          // [tiles_n][stats_ld]
+  float* tgt;             // [m_valid]
+  int stats_ld;
+};
+
+struct GemmBatch {
+  GemmProblem p[kMaxProblems];
+  int nprob;
+  int total_tiles;
+};
+
+// Host helpers -------------------------------------------------------------
+// Describe one problem. A/B are device pointers with the given row pitches
+// (elements).  Returns DS_OK or an error.
+int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const void* B, long long ldb, int b_mn,
+                 int M, int N, int K);
+int gemm_launch(GemmBatch* batch, cudaStream_t stream);
+
+}  // namespace ds

@@ -1,0 +1,36 @@
+// lstm_rec.h — launch interface of the persistent recurrent kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "ds_internal.h"
+
+namespace ds {
+
+struct LstmParams {
+  CUtensorMap tmA;  // forward: Y_full; backward: dG
+  CUtensorMap tmW;  // forward: W_hh [4096, 512]; backward: W_hh^T [1024, 2048]
+  __nv_bfloat16* gates;
+  float* cstate;
+  __nv_bfloat16* y;
+  const __nv_bfloat16* dy;
+  __nv_bfloat16* dg;
+  uint32_t* counters;
+  int B, T, b0, nb, n_btile;
+};
+
+struct LstmLayerArgs {
+  int B, T;
+  __nv_bfloat16* gates;     // [T*B, 4096]
+  float* cstate;            // [T*B, 1024]
+  __nv_bfloat16* y_full;    // [(T+2)*B, 1024]
+  const __nv_bfloat16* w;   // forward: W_hh bf16 [4096, 512]; backward: W_hh^T bf16 [1024, 2048]
+  const __nv_bfloat16* dy;  // backward: [T*B, 1024]
+  __nv_bfloat16* dg;        // backward: [T*B, 4096]
+  uint32_t* counters;       // >= 2 * ceil(B / 128)
+};
+
+int lstm_forward(const LstmLayerArgs& a, cudaStream_t stream);
+int lstm_backward(const LstmLayerArgs& a, cudaStream_t stream);
+
+}  // namespace ds
