@@ -1,0 +1,242 @@
+"""GPU-backed BLSTM objective: the `kind="blstm"` plug-in for the reference's
+objective interface (/root/reference/pkg/src/distsgd/objectives.py:223-311).
+
+`BlstmObjective` is the frozen config object the engines carry around
+(param_dim / kind / regularization, like TinyMlpObjective at :79-103);
+`Learner` owns one learner's device state (fp32 master theta, momentum
+velocity, gradient, operand snapshot, libds workspace) and issues the hot
+path through the C ABI of include/ds_blstm.h.  There is no CPU fallback: all
+compute runs in libds.so on the GPU and any failure raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+HIDDEN = 512  # cells per direction (fixed by the recurrent kernels)
+IN_PAD = 272  # layer-0 feature pitch on the device (16-byte TMA rows)
+
+
+@dataclass(frozen=True)
+class BlstmObjective:
+    """Paper acoustic model as an objective.  Defaults are the
+    paper sizes; smaller configs keep the 512-cell layers (kernel shape)."""
+
+    layers: int = 6
+    input_dim: int = 260
+    bottleneck: int = 256
+    classes: int = 32000
+    frames: int = 21
+    regularization: float = 0.0
+
+    kind = "blstm"
+
+    def __post_init__(self):
+        if self.regularization != 0.0:
+            raise ValueError("blstm objective has no L2 term (regularization must be 0)")
+        if not 1 <= self.input_dim <= IN_PAD:
+            raise ValueError(f"input_dim must be in 1..{IN_PAD}, got {self.input_dim}")
+        if self.bottleneck < 64 or self.bottleneck % 64:
+            raise ValueError("bottleneck must be a positive multiple of 64")
+        if self.classes < 16 or self.classes % 16:
+            raise ValueError("classes must be a positive multiple of 16")
+
+    @property
+    def param_dim(self) -> int:
+        return offsets(self)["total"]
+
+    def cfg(self, max_batch: int) -> _lib.DsCfg:
+        return _lib.DsCfg(self.layers, self.input_dim, self.bottleneck, self.classes, self.frames, max_batch)
+
+
+def offsets(obj: BlstmObjective) -> dict:
+    """Flat packing of csrc/layout.h (== oracle/blstm_ref.py BlstmSpec.offsets)."""
+    g2 = 8 * HIDDEN
+    o = 0
+    out = {}
+    for l in range(obj.layers):
+        d = obj.input_dim if l == 0 else 2 * HIDDEN
+        out[("wih", l)] = (o, (g2, d))
+        o += g2 * d
+        out[("whh", l)] = (o, (g2, HIDDEN))
+        o += g2 * HIDDEN
+        out[("b", l)] = (o, (g2,))
+        o += g2
+    out["wb"] = (o, (obj.bottleneck, 2 * HIDDEN))
+    o += obj.bottleneck * 2 * HIDDEN
+    out["bb"] = (o, (obj.bottleneck,))
+    o += obj.bottleneck
+    out["wo"] = (o, (obj.classes, obj.bottleneck))
+    o += obj.classes * obj.bottleneck
+    out["bo"] = (o, (obj.classes,))
+    o += obj.classes
+    out["total"] = o
+    return out
+
+
+def training_flops_per_frame(obj: BlstmObjective) -> float:
+    """Algorithmic training FLOPs per frame: 2*P_w forward, 2*P_w
+    weight gradients, 2*(P_w - layer-0 W_ih) input gradients."""
+    offs = offsets(obj)
+    p_w = 0
+    for k, (o, shape) in offs.items():
+        if k == "total":
+            continue
+        if len(shape) == 2:
+            p_w += shape[0] * shape[1]
+    w_ih0 = 8 * HIDDEN * obj.input_dim
+    return 2.0 * p_w + 2.0 * p_w + 2.0 * (p_w - w_ih0)
+
+
+class DeviceDataset:
+    """Device-resident copy of a `Dataset` whose inputs are [n_seq, T, D]
+    21-frame feature sequences and targets [n_seq, T] class ids
+    (objectives.py:23-43 layout, rows = sequences)."""
+
+    def __init__(self, inputs: np.ndarray, targets: np.ndarray, device: int = 0):
+        import torch
+
+        if inputs.ndim != 3:
+            raise ValueError(f"blstm inputs must be [n_seq, frames, dim], got shape {inputs.shape}")
+        n, T, D = inputs.shape
+        if targets.shape != (n, T):
+            raise ValueError(f"blstm targets must be [n_seq, frames] = {(n, T)}, got {targets.shape}")
+        self.n_seq, self.frames, self.input_dim = n, T, D
+        self.device = device
+        dev = torch.device("cuda", device)
+        feats = torch.zeros((n, T, IN_PAD), dtype=torch.bfloat16, device=dev)
+        chunk = max(1, (1 << 26) // max(1, T * D))
+        for s in range(0, n, chunk):
+            part = torch.from_numpy(np.ascontiguousarray(inputs[s:s + chunk], dtype=np.float32))
+            feats[s:s + chunk, :, :D] = part.to(dev).to(torch.bfloat16)
+        self.feats = feats
+        self.labels = torch.from_numpy(np.ascontiguousarray(targets).astype(np.int32)).to(dev)
+
+
+class Learner:
+    """One learner's device state + libds handle (one per GPU, or several
+    simulated learners sharing a GPU)."""
+
+    def __init__(self, obj: BlstmObjective, data: DeviceDataset, max_batch: int, device: int = 0,
+                 theta0: np.ndarray | None = None, momentum: float = 0.9):
+        import torch
+
+        if data.frames != obj.frames or data.input_dim != obj.input_dim:
+            raise ValueError("dataset shape does not match the objective (frames / input_dim)")
+        self.obj = obj
+        self.data = data
+        self.device = device
+        self.max_batch = max_batch
+        self.mu = float(momentum)
+        lib = _lib.load()
+        torch.cuda.set_device(device)
+        dev = torch.device("cuda", device)
+        h = ctypes.c_void_p()
+        cfg = obj.cfg(max_batch)
+        _lib.check(lib.ds_blstm_create(ctypes.byref(cfg), device, ctypes.byref(h)), "ds_blstm_create")
+        self.handle = h
+        _lib.check(lib.ds_blstm_set_dataset(h, data.feats.data_ptr(), data.labels.data_ptr(), data.n_seq),
+                   "ds_blstm_set_dataset")
+        P = obj.param_dim
+        self.theta = torch.zeros(P, dtype=torch.float32, device=dev)
+        self.vel = torch.zeros(P, dtype=torch.float32, device=dev)
+        self.grad = torch.zeros(P, dtype=torch.float32, device=dev)
+        self.loss_sum = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.idx = torch.zeros(max_batch, dtype=torch.int64, device=dev)
+        self.idx_host = torch.zeros(max_batch, dtype=torch.int64).pin_memory()
+        self.stream = torch.cuda.Stream(device=dev)
+        self.batch = 0
+        if theta0 is not None:
+            self.set_weights(theta0)
+
+    # -- state ----------------------------------------------------------------
+    def set_weights(self, w: np.ndarray) -> None:
+        import torch
+
+        if w.shape != (self.obj.param_dim,):
+            raise ValueError(
+                f"parameter dim mismatch for blstm: expected {self.obj.param_dim}, got shape {w.shape}")
+        with torch.cuda.stream(self.stream):
+            self.theta.copy_(torch.from_numpy(np.asarray(w, dtype=np.float32)).to(self.theta.device))
+        self.snapshot()
+
+    def weights(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.theta.double().cpu().numpy()
+
+    def snapshot(self) -> None:
+        """K2: operand snapshot of the current theta (engines/adpsgd.py:132-134)."""
+        lib = _lib.load()
+        _lib.check(lib.ds_blstm_cast_snapshot(self.handle, self.theta.data_ptr(), self.stream.cuda_stream),
+                   "ds_blstm_cast_snapshot")
+
+    # -- hot path -------------------------------------------------------------
+    def _upload_batch(self, batch: np.ndarray) -> int:
+        import torch
+
+        B = len(batch)
+        if not 1 <= B <= self.max_batch:
+            raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
+        self.stream.synchronize()  # pinned staging buffer reuse
+        self.idx_host[:B] = torch.from_numpy(np.asarray(batch, dtype=np.int64))
+        with torch.cuda.stream(self.stream):
+            self.idx[:B].copy_(self.idx_host[:B], non_blocking=True)
+        return B
+
+    def gradient(self, batch: np.ndarray) -> None:
+        """gradient(objective, snapshot, batch, dataset) into self.grad
+        (objectives.py:236-263); asynchronous on self.stream."""
+        B = self._upload_batch(batch)
+        self.batch = B
+        lib = _lib.load()
+        _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self.idx.data_ptr(), B, self.grad.data_ptr(),
+                                        self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
+                   "ds_blstm_fwd_bwd")
+
+    def loss(self, batch: np.ndarray) -> None:
+        B = self._upload_batch(batch)
+        self.batch = B
+        lib = _lib.load()
+        _lib.check(lib.ds_blstm_loss(self.handle, self.idx.data_ptr(), B, self.loss_sum.data_ptr(),
+                                     self.flag.data_ptr(), self.stream.cuda_stream), "ds_blstm_loss")
+
+    def sgd_step(self, lr: float) -> None:
+        """sgd_step (optim.py:109-121) fused with the operand snapshot (K9+K2)."""
+        if lr <= 0:
+            raise ValueError(f"learning rate must be > 0, got {lr}")
+        lib = _lib.load()
+        _lib.check(lib.ds_sgd_momentum(self.theta.data_ptr(), self.vel.data_ptr(), self.grad.data_ptr(), lr,
+                                       self.mu, self.obj.param_dim, self.handle, self.flag.data_ptr(),
+                                       self.stream.cuda_stream), "ds_sgd_momentum")
+
+    def check_finite(self, what: str = "gradient") -> None:
+        """Raise the reference's ValueError (objectives.py:261-262) when the
+        device flagged a non-finite loss / gradient."""
+        self.stream.synchronize()
+        if int(self.flag.item()) & 1:
+            self.flag.zero_()
+            raise ValueError(f"blstm {what} is non-finite (weights diverged?)")
+        if int(self.flag.item()) & 2:
+            self.flag.zero_()
+            raise ValueError("minibatch index outside the dataset")
+
+    def mean_loss(self) -> float:
+        self.stream.synchronize()
+        return float(self.loss_sum.item()) / (self.batch * self.obj.frames)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.load().ds_blstm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

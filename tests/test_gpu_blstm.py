@@ -1,0 +1,144 @@
+"""End-to-end parity of the GPU BLSTM training step against the float64 CPU
+oracle (oracle/blstm_ref.py) on identical inputs, plus the sync kernels
+against float32 restatements of the reference arithmetic.
+
+Stated tolerances (BF16 tensor-core operands, FP32 accumulation/state):
+  loss                      : |rel| <= 5e-3
+  gradient, per tensor block: ||g - g_ref|| / ||g_ref|| <= 2.5e-2 and cosine >= 0.9995
+  sgd_step / adpsgd_mix / canonical allreduce : bit-exact vs float32 numpy
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle import blstm_ref as O  # noqa: E402
+from paper_1904_04956_b200 import _lib  # noqa: E402
+from paper_1904_04956_b200.blstm import BlstmObjective, DeviceDataset, Learner, offsets  # noqa: E402
+
+
+def _spec(obj):
+    return O.BlstmSpec(layers=obj.layers, input_dim=obj.input_dim, hidden=512, bottleneck=obj.bottleneck,
+                       classes=obj.classes, frames=obj.frames)
+
+
+@pytest.mark.parametrize("layers,B,T,classes", [(2, 24, 6, 512), (1, 136, 5, 256)])
+def test_fwd_bwd_matches_oracle(layers, B, T, classes):
+    obj = BlstmObjective(layers=layers, classes=classes, frames=T)
+    spec = _spec(obj)
+    assert spec.param_dim == obj.param_dim
+    x, y, _, _ = O.make_dataset(spec, 2 * B + 3, seed=5)
+    w = O.initial_weights(spec, 5)
+    rng = np.random.default_rng(0)
+    batch = rng.permutation(len(x))[:B]
+    # the GPU consumes bf16 features: give the oracle the same rounded inputs
+    xb = torch.from_numpy(x).bfloat16().double().numpy()
+    loss_ref, g_ref = O.loss_and_grad(spec, w, xb[batch], y[batch])
+
+    L = Learner(obj, DeviceDataset(x, y), max_batch=2 * B, theta0=w)
+    L.gradient(batch)
+    L.check_finite()
+    loss = L.mean_loss()
+    g = L.grad.double().cpu().numpy()
+    assert abs(loss - loss_ref) <= 5e-3 * abs(loss_ref), (loss, loss_ref)
+    report = {}
+    for k, v in offsets(obj).items():
+        if k == "total":
+            continue
+        o, shape = v
+        n = int(np.prod(shape))
+        a, r = g[o:o + n], g_ref[o:o + n]
+        rel = np.linalg.norm(a - r) / max(np.linalg.norm(r), 1e-30)
+        cos = float(a @ r / max(np.linalg.norm(a) * np.linalg.norm(r), 1e-30))
+        report[k] = (rel, cos)
+    print(report)
+    for k, (rel, cos) in report.items():
+        assert rel <= 2.5e-2 and cos >= 0.9995, (k, rel, cos)
+    # second call reuses the cached CUDA graph and must give the same result
+    L.gradient(batch)
+    L.stream.synchronize()
+    assert torch.equal(L.grad.double().cpu(), torch.from_numpy(g))
+    L.close()
+
+
+def test_sgd_kernel_bitexact():
+    lib = _lib.load()
+    n = 1_000_003
+    rng = np.random.default_rng(1)
+    th = rng.standard_normal(n).astype(np.float32)
+    v = rng.standard_normal(n).astype(np.float32)
+    g = rng.standard_normal(n).astype(np.float32)
+    lr, mu = np.float32(0.1), np.float32(0.9)
+    T = [torch.from_numpy(a.copy()).cuda() for a in (th, v, g)]
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(lib.ds_sgd_momentum(T[0].data_ptr(), T[1].data_ptr(), T[2].data_ptr(), float(lr), float(mu), n, None,
+                                   flag.data_ptr(), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    v_ref = (v * mu).astype(np.float32) + g
+    th_ref = th - (lr * v_ref).astype(np.float32)
+    assert np.array_equal(T[1].cpu().numpy(), v_ref)
+    assert np.array_equal(T[0].cpu().numpy(), th_ref)
+    assert flag.item() == 0
+    T[2][5] = float("nan")
+    _lib.check(lib.ds_sgd_momentum(T[0].data_ptr(), T[1].data_ptr(), T[2].data_ptr(), float(lr), float(mu), n, None,
+                                   flag.data_ptr(), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert flag.item() == 1
+
+
+def test_mix_kernel_pair_sum_exact():
+    lib = _lib.load()
+    n = 777_777
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal(n).astype(np.float32)
+    b = (rng.standard_normal(n) * 1e3).astype(np.float32)
+    A, Bt = torch.from_numpy(a.copy()).cuda(), torch.from_numpy(b.copy()).cuda()
+    _lib.check(lib.ds_adpsgd_mix(A.data_ptr(), Bt.data_ptr(), n, _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    m = ((a + b) / np.float32(2)).astype(np.float32)
+    assert np.array_equal(A.cpu().numpy(), m) and np.array_equal(Bt.cpu().numpy(), m)
+    # identical value on both sides => pair sum preserved bit-exactly (test_adpsgd.py:34-41)
+    assert np.array_equal(A.cpu().numpy() + Bt.cpu().numpy(), (a + b).astype(np.float32))
+
+
+@pytest.mark.parametrize("world,chunks", [(2, None), (3, 7), (4, None), (8, 16)])
+def test_group_reduce_canonical_order(world, chunks):
+    lib = _lib.load()
+    n = 100_003
+    chunks = chunks or world
+    rng = np.random.default_rng(world)
+    gs = [rng.standard_normal(n).astype(np.float32) * (10.0 ** k) for k in range(world)]
+    th = rng.standard_normal(n).astype(np.float32)
+    v = rng.standard_normal(n).astype(np.float32)
+    G = [torch.from_numpy(x).cuda() for x in gs]
+    TH = [torch.from_numpy(th.copy()).cuda() for _ in range(world)]
+    V = [torch.from_numpy(v.copy()).cuda() for _ in range(world)]
+    ptrs = ctypes_arr
+    for r in range(world):
+        _lib.check(lib.ds_group_reduce(world, r, ptrs(G), ptrs(TH), ptrs(V), None, n, chunks, 0.1, 0.9, 0,
+                                       _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    size = -(-n // chunks)
+    mean = np.empty(n, np.float32)
+    for j in range(chunks):
+        lo, hi = min(j * size, n), min((j + 1) * size, n)
+        o = j % world
+        s = gs[o][lo:hi].copy()
+        for k in range(1, world):
+            s = (s + gs[(o + k) % world][lo:hi]).astype(np.float32)
+        mean[lo:hi] = s / np.float32(world)
+    v_ref = (v * np.float32(0.9)).astype(np.float32) + mean
+    th_ref = th - (np.float32(0.1) * v_ref).astype(np.float32)
+    for r in range(world):
+        assert np.array_equal(TH[r].cpu().numpy(), th_ref)
+        assert np.array_equal(V[r].cpu().numpy(), v_ref)
+
+
+def ctypes_arr(ts):
+    import ctypes
+
+    return (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
