@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""bench.py — training frames/s of the paper BLSTM on B200 (BASELINE.json).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+N = 1 : config "paper BLSTM ... SSGD batch 256 on 1 B200" — the reference's
+        single-learner path run_single (engines/single.py:49-55): gather ->
+        fwd/bwd -> learning_rate -> sgd_step, per minibatch of 256 21-frame
+        sequences drawn from epoch_minibatches.
+N > 1 : one rank per GPU (torchrun), SSGD with per-learner batch B (weak
+        scaling): each rank computes its gradient, the gradient is
+        allreduced (torch.distributed / NCCL — the comparison baseline
+        transport) and every rank applies the fused SGD+snapshot kernel.
+
+`value` is device-timed (CUDA events on the learner stream, inputs resident
+in HBM, max over ranks); `e2e` goes through the public Learner API with the
+minibatch indices copied host->device and the loss read back every step.
+`--impl reference` times the CPU oracle port (oracle/blstm_ref.py, float64
+numpy, all host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training frames/sec at 1/2/4/8 B200 per strategy (SSGD/ADPSGD/H-ADPSGD)"
+UNIT = "frames/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), float(
+            d["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 8:
+                    self.rows.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_data(obj, n_seq: int, seed: int = 0):
+    """Synthetic SWB-shaped data: x ~ N(0,1), y ~ U{0..C-1}."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n_seq, obj.frames, obj.input_dim), dtype=np.float32)
+    y = rng.integers(0, obj.classes, size=(n_seq, obj.frames), dtype=np.int64)
+    n_held = n_seq // 10
+    return x, y, np.arange(n_seq - n_held)
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference(obj, batch: int, steps: int, warmup: int, seed: int = 0):
+    """The CPU oracle port timed on the host cores (float64 numpy, BLAS uses
+    every host thread).  Returns (frames/s, seconds per step)."""
+    from oracle import blstm_ref as O
+
+    spec = O.BlstmSpec(layers=obj.layers, input_dim=obj.input_dim, hidden=512, bottleneck=obj.bottleneck,
+                       classes=obj.classes, frames=obj.frames)
+    rng = np.random.default_rng(seed)
+    w = O.initial_weights(spec, seed)
+    v = np.zeros_like(w)
+    times = []
+    for i in range(warmup + steps):
+        x = rng.standard_normal((batch, spec.frames, spec.input_dim))
+        y = rng.integers(0, spec.classes, size=(batch, spec.frames))
+        t0 = time.perf_counter()
+        _, g = O.loss_and_grad(spec, w, x, y)
+        v *= 0.9
+        v += g
+        w = w - 0.1 * v
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    sec = sum(times) / len(times)
+    return batch * spec.frames / sec, sec
+
+
+def run_reference_arm(args, rank: int):
+    from paper_1904_04956_b200.blstm import BlstmObjective
+
+    if rank != 0:
+        return
+    obj = BlstmObjective()
+    cb = args.cpu_batch
+    steps = max(1, min(args.steps, args.ref_max_steps))
+    warm = max(0, min(args.warmup, 1))
+    fps, sec = cpu_reference(obj, cb, steps, warm)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(fps, 2), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": round(sec * 1e3, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "paper BLSTM training step (run_single), CPU oracle port", "model": "paper-blstm",
+                   "batch_per_step_sample": cb, "seq_len": obj.frames},
+        "cpu_baseline": {"value": round(fps, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{steps} step(s) of B={cb} sequences x 21 frames, paper-size model, float64"},
+        "e2e": {"value": round(fps, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+
+    from paper_1904_04956_b200.blstm import (BlstmObjective, DeviceDataset, Learner, initial_weights,
+                                             training_flops_per_frame)
+    from paper_1904_04956_b200.schedule import baseline_schedule, epoch_minibatches, learning_rate
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    obj = BlstmObjective()
+    B = args.batch
+    T = obj.frames
+    x, y, train = make_data(obj, args.n_seq, seed=0)
+    data = DeviceDataset(x, y, device=local_rank)
+    del x
+    L = Learner(obj, data, max_batch=B, device=local_rank, theta0=initial_weights(obj, 0))
+    sched = baseline_schedule(0.1)
+    # the run_single draw order; rank r of an SSGD group takes every world-th batch (static_partition)
+    pool = epoch_minibatches(train, B, seed=0, epoch=1)
+    pool = [b for b in pool if len(b) == B]
+    mine = pool[rank::world] if world > 1 else pool
+    q = len(mine)
+    idx_dev = torch.from_numpy(np.stack(mine)).to(torch.device("cuda", local_rank))
+    stream = L.stream
+    P = obj.param_dim
+
+    def step(k: int):
+        j = k % q
+        L.gradient_device(idx_dev[j], B)
+        if dist is not None:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(L.grad)
+                L.grad.div_(world)
+        L.sgd_step(learning_rate(sched, 1, j, q))
+
+    for k in range(args.warmup):
+        step(k)
+    L.check_finite()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        ev0.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    L.check_finite()
+    frames = args.steps * B * T * world
+    value = frames / (ms / 1e3)
+    launches_per_step = L.kernel_count() + 4 + obj.layers  # + sgd, W_hh^T, W_ih0 pad, bias copies
+
+    # ---- end to end through the public Learner API (host indices in, loss out)
+    e2e_steps = max(3, min(args.steps, 20))
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        j = k % q
+        L.gradient(mine[j])
+        if dist is not None:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(L.grad)
+                L.grad.div_(world)
+        L.sgd_step(learning_rate(sched, 1, j, q))
+        _ = L.mean_loss()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": round(e2e_steps * B * T * world / e2e_s, 1), "unit": UNIT, "h2d_bytes_per_step": B * 8,
+           "d2h_bytes_per_step": 4}
+
+    # ---- per-phase device times (profiling pass, events around each phase)
+    L.set_profile(True)
+    L.profile_read()
+    nprof = 3
+    for k in range(nprof):
+        L.gradient_device(idx_dev[k % q], B)
+    torch.cuda.synchronize()
+    ph = {k: v / nprof for k, v in L.profile_read().items()}
+    L.set_profile(False)
+
+    burst, sustained, hbm, peak_kind = _peaks()
+    flops_frame = training_flops_per_frame(obj)
+    N = B * T
+    rec_flops = 2 * obj.layers * 2.0 * N * (8 * 512) * 512  # forward h W_hh^T + backward dh = dG W_hh
+    gemm_flops = flops_frame * N - rec_flops
+    gemm_tfs = gemm_flops / (ph["gemm"] * 1e-3) / 1e12 if ph["gemm"] > 0 else 0.0
+    roof = {"bound": "tensor", "kernel": "gemm_kernel (tcgen05 bf16, all GEMM launches of one step)",
+            "achieved": round(gemm_tfs, 1), "peak": burst, "unit": "TFLOP/s", "frac": round(gemm_tfs / burst, 4),
+            "peak_kind": f"{peak_kind} burst bf16", "traffic": None,
+            "step_tensor_frac": round(value / world * flops_frame / 1e12 / sustained, 4),
+            "phase_ms": {k: round(v, 3) for k, v in ph.items()}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        fps, sec = cpu_reference(obj, args.cpu_batch, 1, 0)
+        cpu = {"value": round(fps, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"1 step of B={args.cpu_batch} x 21 frames, paper-size model, float64 numpy oracle"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": ("paper BLSTM run_single step, batch 256 (config 2)" if world == 1 else
+                                f"paper BLSTM SSGD, {B}/learner, allreduce=nccl-baseline"),
+                   "layers": obj.layers, "cells": 1024, "bottleneck": obj.bottleneck, "classes": obj.classes,
+                   "input_dim": obj.input_dim, "frames": T, "batch_per_learner": B, "global_batch": B * world,
+                   "strategy": "single" if world == 1 else "ssgd",
+                   "l2_policy": "per-step working set ~1.2 GB (activations, 344 MB dlogits) >> 126 MB L2; no flush",
+                   "parallelism": f"dp{world}"},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    L.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--n-seq", type=int, default=16384)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-batch", type=int, default=32)
+    ap.add_argument("--ref-max-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+    if args.warmup < 3:
+        args.warmup = 3
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

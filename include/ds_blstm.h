@@ -94,6 +94,16 @@ int ds_group_reduce(int32_t world, int32_t rank, float* const* grads, float* con
                     ds_blstm* const* snap_owners, int64_t n, int32_t nchunks, float lr, float mu, int32_t mode,
                     ds_stream_t stream);
 
+/* Phase profiling (bench/tests): when enabled the step is issued without the
+ * CUDA graph and CUDA events bracket every phase; ds_blstm_profile_read sums
+ * the per-kind milliseconds since the last read into ms_by_kind[0..nkinds):
+ * 0 = tcgen05 GEMMs, 1 = recurrent forward, 2 = recurrent backward,
+ * 3 = gather / soft-max combine / bias column sums. */
+int ds_blstm_set_profile(ds_blstm* h, int32_t enable);
+int ds_blstm_profile_read(ds_blstm* h, float* ms_by_kind, int32_t nkinds);
+/* Kernel launches issued by the last ds_blstm_fwd_bwd / ds_blstm_loss. */
+int32_t ds_blstm_kernel_count(ds_blstm* h);
+
 /* GEMM self-test hook (tests only): C[M,N] f32 = A . B^T with bf16 operands,
  * a_mn/b_mn select MN-major storage ([K][M] / [K][N]). */
 int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C,

@@ -182,12 +182,12 @@ def loss_and_grad(spec: BlstmSpec, w: np.ndarray, x: np.ndarray, y: np.ndarray):
     np.put_along_axis(dlog, cache["yt"][..., None], np.take_along_axis(dlog, cache["yt"][..., None], -1) - 1.0, -1)
     dlog /= Nf
     z = cache["z"]
-    put("wo", np.einsum("tbc,tbk->ck", dlog, z))
+    put("wo", dlog.reshape(Nf, -1).T @ z.reshape(Nf, -1))
     put("bo", dlog.sum((0, 1)))
     dz = dlog @ P["wo"]
     if spec.bottleneck:
         top = cache["top_in"]
-        put("wb", np.einsum("tbk,tbj->kj", dz, top))
+        put("wb", dz.reshape(Nf, -1).T @ top.reshape(Nf, -1))
         put("bb", dz.sum((0, 1)))
         dy = dz @ P["wb"]
     else:

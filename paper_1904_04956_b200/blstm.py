@@ -84,13 +84,19 @@ def training_flops_per_frame(obj: BlstmObjective) -> float:
     weight gradients, 2*(P_w - layer-0 W_ih) input gradients."""
     offs = offsets(obj)
     p_w = 0
-    for k, (o, shape) in offs.items():
+    for k, v in offs.items():
         if k == "total":
             continue
+        shape = v[1]
         if len(shape) == 2:
             p_w += shape[0] * shape[1]
     w_ih0 = 8 * HIDDEN * obj.input_dim
     return 2.0 * p_w + 2.0 * p_w + 2.0 * (p_w - w_ih0)
+
+
+def initial_weights(obj: BlstmObjective, seed: int) -> np.ndarray:
+    """objectives.py:307-311: 0.1 * N(0, 1) from default_rng((seed, 0))."""
+    return 0.1 * np.random.default_rng((seed, 0)).standard_normal(obj.param_dim)
 
 
 class DeviceDataset:
@@ -198,6 +204,33 @@ class Learner:
         _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self.idx.data_ptr(), B, self.grad.data_ptr(),
                                         self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
                    "ds_blstm_fwd_bwd")
+
+    def gradient_device(self, idx_dev, B: int) -> None:
+        """Same as `gradient` for indices already resident on the device: a
+        device-to-device copy into the bound index buffer keeps the cached
+        CUDA graph and never synchronises the host."""
+        if not 1 <= B <= self.max_batch:
+            raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            self.idx[:B].copy_(idx_dev[:B], non_blocking=True)
+        self.batch = B
+        lib = _lib.load()
+        _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self.idx.data_ptr(), B, self.grad.data_ptr(),
+                                        self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
+                   "ds_blstm_fwd_bwd")
+
+    def set_profile(self, on: bool) -> None:
+        _lib.check(_lib.load().ds_blstm_set_profile(self.handle, 1 if on else 0), "ds_blstm_set_profile")
+
+    def profile_read(self) -> dict:
+        buf = (ctypes.c_float * 4)()
+        _lib.check(_lib.load().ds_blstm_profile_read(self.handle, buf, 4), "ds_blstm_profile_read")
+        return {"gemm": buf[0], "lstm_fwd": buf[1], "lstm_bwd": buf[2], "other": buf[3]}
+
+    def kernel_count(self) -> int:
+        return int(_lib.load().ds_blstm_kernel_count(self.handle))
 
     def loss(self, batch: np.ndarray) -> None:
         B = self._upload_batch(batch)

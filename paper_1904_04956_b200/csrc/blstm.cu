@@ -65,6 +65,11 @@ struct ds_blstm {
     cudaGraphExec_t exec;
   };
   std::vector<Entry> graphs;
+  // phase profiling (tests / bench only; bypasses the graph)
+  int profile = 0;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_kind;
+  int launches = 0;  // kernel launches issued by the last step
 };
 
 namespace {
@@ -125,6 +130,19 @@ int validate_cfg(const ds_blstm_cfg* c) {
   return DS_OK;
 }
 
+// phase kinds for profiling
+enum { PH_GEMM = 0, PH_LSTM_FWD = 1, PH_LSTM_BWD = 2, PH_OTHER = 3, PH_END = 4 };
+
+int mark(ds_blstm* h, int kind, cudaStream_t s) {
+  if (!h->profile) return DS_OK;
+  cudaEvent_t e;
+  DS_CUDA_TRY(cudaEventCreate(&e));
+  DS_CUDA_TRY(cudaEventRecord(e, s));
+  h->ev.push_back(e);
+  h->ev_kind.push_back(kind);
+  return DS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // The step schedule.  Forward always runs; backward when `grad` != nullptr.
 int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, int* flag, cudaStream_t s) {
@@ -141,7 +159,11 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   do {                    \
     if ((rc = (x))) return rc; \
   } while (0)
+#define MARK(k) TRY(mark(h, k, s))
+  int& nl = h->launches;
+  nl = 0;
 
+  MARK(PH_OTHER);
   TRY(op_gather(idx, B, T, h->feats, h->labels, h->n_seq, h->x0, h->lab, flag, s));
   for (int l = 0; l < Lh; ++l) {
     DS_CUDA_TRY(cudaMemsetAsync(h->yfull[l], 0, (size_t)B * kLayerOut * 2, s));
@@ -163,10 +185,13 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.out = h->gates[l];
     p.ldo = kGates2;
     p.bias = bias_l + (size_t)l * kGates2;
+    MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], nullptr, nullptr,
                      h->counters};
+    MARK(PH_LSTM_FWD);
     TRY(lstm_forward(la, s));
+    nl += 2 + (B - 1) / (128 * (num_sms() / 32));
   }
   {
     GemmBatch gb;
@@ -178,7 +203,9 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.out = h->z;
     p.ldo = bott;
     p.bias = bias_b;
+    MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
+    nl += 1;
   }
   {
     GemmBatch gb;
@@ -193,9 +220,14 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.stats_ld = (int)h->Nmax;
     p.tgt = h->tgt;
     TRY(gemm_launch(&gb, s));
+    MARK(PH_OTHER);
     TRY(op_ce_combine(h->stats, p.tiles_n, h->Nmax, h->tgt, N, h->lse, loss, flag, s));
+    nl += 3;  // gather, ce stats gemm, combine
   }
-  if (!grad) return DS_OK;
+  if (!grad) {
+    MARK(PH_END);
+    return DS_OK;
+  }
 
   // ---- backward ----
   {
@@ -211,7 +243,9 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.out = h->dlogits;
     p.ldo = C;
     p.scale = 1.0f / (float)N;
+    MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
+    nl += 1;
   }
   {
     GemmBatch gb;
@@ -228,7 +262,9 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p1.out = h->dz;
     p1.ldo = bott;
     TRY(gemm_launch(&gb, s));
+    MARK(PH_OTHER);
     TRY(op_colsum(h->dlogits, N, C, C, h->colpart, grad + L.off_bo, s));
+    nl += 3;
   }
   {
     GemmBatch gb;
@@ -244,13 +280,18 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p1.epi = EPI_BF16;
     p1.out = h->dy;
     p1.ldo = kLayerOut;
+    MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
+    MARK(PH_OTHER);
     TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, s));
+    nl += 3;
   }
   for (int l = Lh - 1; l >= 0; --l) {
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->whhT + (size_t)l * kGates2 * kHidden, h->dy,
                      h->dg, h->counters};
+    MARK(PH_LSTM_BWD);
     TRY(lstm_backward(la, s));
+    nl += 1 + (B - 1) / (128 * (num_sms() / 32));
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
     GemmProblem& p0 = gb.p[0];  // dW_ih = dG^T X
@@ -281,9 +322,14 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       p3.ldo = kLayerOut;
       gb.nprob = 4;
     }
+    MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
+    MARK(PH_OTHER);
     TRY(op_colsum(h->dg, N, kGates2, kGates2, h->colpart, grad + L.off_b[l], s));
+    nl += 3;
   }
+  MARK(PH_END);
+#undef MARK
 #undef TRY
   return DS_OK;
 }
@@ -304,7 +350,8 @@ int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, i
   DS_CUDA_TRY(cudaSetDevice(h->device));
   cudaStreamCaptureStatus cs;
   DS_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
-  if (!use_graphs() || cs != cudaStreamCaptureStatusNone) return issue_step(h, idx, B, grad, loss, flag, s);
+  if (!use_graphs() || h->profile || cs != cudaStreamCaptureStatusNone)
+    return issue_step(h, idx, B, grad, loss, flag, s);
   ds_blstm::Key key{B, idx, grad, loss, flag, grad != nullptr};
   for (auto& e : h->graphs)
     if (e.key == key) {
@@ -455,6 +502,31 @@ int ds_group_reduce(int32_t world, int32_t rank, float* const* grads, float* con
   return op_group_reduce(world, rank, grads, thetas, vels, any ? snaps : nullptr, n, nchunks, lr, mu, mode,
                          reinterpret_cast<cudaStream_t>(stream));
 }
+
+int ds_blstm_set_profile(ds_blstm* h, int32_t enable) {
+  if (!h) return fail_arg("null handle");
+  h->profile = enable ? 1 : 0;
+  return DS_OK;
+}
+
+int ds_blstm_profile_read(ds_blstm* h, float* ms_by_kind, int32_t nkinds) {
+  if (!h || !ms_by_kind) return fail_arg("null argument");
+  for (int k = 0; k < nkinds; ++k) ms_by_kind[k] = 0.f;
+  DS_CUDA_TRY(cudaSetDevice(h->device));
+  if (!h->ev.empty()) DS_CUDA_TRY(cudaEventSynchronize(h->ev.back()));
+  for (size_t i = 0; i + 1 < h->ev.size(); ++i) {
+    float ms = 0.f;
+    DS_CUDA_TRY(cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
+    int k = h->ev_kind[i];
+    if (k >= 0 && k < nkinds) ms_by_kind[k] += ms;
+  }
+  for (auto e : h->ev) cudaEventDestroy(e);
+  h->ev.clear();
+  h->ev_kind.clear();
+  return DS_OK;
+}
+
+int32_t ds_blstm_kernel_count(ds_blstm* h) { return h ? h->launches : -1; }
 
 int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C,
                        int64_t ldc, int32_t M, int32_t N, int32_t K, ds_stream_t stream) {
