@@ -105,7 +105,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
     h->yfull[l] = a.take<__nv_bfloat16>(base, (size_t)(h->T + 2) * h->Bmax * kLayerOut);
   }
   h->z = a.take<__nv_bfloat16>(base, (size_t)N * L.bottleneck);
-  h->stats = a.take<float2>(base, (size_t)h->ntiles_c * N);
+  h->stats = a.take<float2>(base, (size_t)2 * h->ntiles_c * N);  // two column halves per tile
   h->tgt = a.take<float>(base, N);
   h->lse = a.take<float>(base, N);
   h->dlogits = a.take<__nv_bfloat16>(base, (size_t)N * L.classes);
@@ -114,7 +114,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   h->dg = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
   int64_t cp = op_colsum_scratch(L.classes > kGates2 ? L.classes : kGates2);
   h->colpart = a.take<float>(base, cp);
-  h->counters = a.take<uint32_t>(base, 2 * ((h->Bmax + 127) / 128) + 64);
+  h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64);
   *total = a.off + 256;
   return DS_OK;
 }
@@ -191,7 +191,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
                      h->counters};
     MARK(PH_LSTM_FWD);
     TRY(lstm_forward(la, s));
-    nl += 2 + (B - 1) / (128 * (num_sms() / 32));
+    nl += 2 + (B - 1) / (128 * lstm_max_tiles());
   }
   {
     GemmBatch gb;
@@ -221,8 +221,8 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.tgt = h->tgt;
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
-    TRY(op_ce_combine(h->stats, p.tiles_n, h->Nmax, h->tgt, N, h->lse, loss, flag, s));
-    nl += 3;  // gather, ce stats gemm, combine
+    TRY(op_ce_combine(h->stats, 2 * p.tiles_n, h->Nmax, h->tgt, N, h->lse, h->colpart, loss, flag, s));
+    nl += 4;  // gather, ce stats gemm, combine (2 kernels)
   }
   if (!grad) {
     MARK(PH_END);
@@ -291,7 +291,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
                      h->dg, h->counters};
     MARK(PH_LSTM_BWD);
     TRY(lstm_backward(la, s));
-    nl += 1 + (B - 1) / (128 * (num_sms() / 32));
+    nl += 1 + (B - 1) / (128 * lstm_max_tiles());
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
     GemmProblem& p0 = gb.p[0];  // dW_ih = dG^T X
@@ -542,14 +542,14 @@ int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, 
 }
 
 int ds_debug_lstm_fwd(int32_t B, int32_t T, void* gates, float* cstate, void* y_full, const void* whh,
-                      uint32_t* counters, ds_stream_t stream) {
+                      uint32_t* counters, uint64_t* trace, ds_stream_t stream) {
   LstmLayerArgs a{B, T, reinterpret_cast<__nv_bfloat16*>(gates), cstate, reinterpret_cast<__nv_bfloat16*>(y_full),
-                  reinterpret_cast<const __nv_bfloat16*>(whh), nullptr, nullptr, counters};
+                  reinterpret_cast<const __nv_bfloat16*>(whh), nullptr, nullptr, counters, trace};
   return lstm_forward(a, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* cstate, const void* whhT, const void* dy,
-                      void* dg, uint32_t* counters, ds_stream_t stream) {
+                      void* dg, uint32_t* counters, uint64_t* trace, ds_stream_t stream) {
   LstmLayerArgs a{B,
                   T,
                   const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(gates)),
@@ -558,7 +558,8 @@ int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* csta
                   reinterpret_cast<const __nv_bfloat16*>(whhT),
                   reinterpret_cast<const __nv_bfloat16*>(dy),
                   reinterpret_cast<__nv_bfloat16*>(dg),
-                  counters};
+                  counters,
+                  trace};
   return lstm_backward(a, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -11,45 +11,47 @@
 //                            and h_T read as zeros for either direction.
 // Gate rows are unit-interleaved: row r = unit*4 + gate (gate 0..3 = i,f,g,o),
 // so a CTA that owns 32 hidden units owns 128 contiguous gate rows and the
-// cell update is thread-local.
+// cell update is thread-local (one thread = one batch row).
 //
-// Forward CTA (dir, batch tile, unit block of 32):
+// Forward CTA (dir, batch tile of 128, unit block of 32):
 //   W_hh[dir][unit block] (128 x 512 bf16, 128 KB) stays resident in smem.
 //   step s: acc[128 batch, 128 gate rows] = h_prev[128, 512] . W^T (tcgen05,
-//   M=128 N=128 K=512, A streamed by TMA from L2), epilogue adds the input
-//   projection, applies sigmoid/tanh, updates c and h in registers/HBM, then
-//   releases a per-(dir, batch tile) counter; the producer of every CTA in
-//   that group acquires it before loading h_t for the next step.
+//   M=128 N=128 K=512, A streamed by TMA from L2 in 64-unit chunks); the
+//   epilogue (8 warps: 4 TMEM lane quadrants x 2 column halves) adds the
+//   prefetched input projection, applies sigmoid/tanh (MUFU tanh.approx),
+//   updates c (registers) and h, then publishes a per-CTA step flag.
 // Backward CTA (dir, batch tile, unit block of 32):
 //   W_hh^T[dir][unit block] (32 x 2048 bf16, 128 KB) resident.
-//   step s: acc[128 batch, 32 units] = dG_prev[128, 2048] . W^T  (dh from the
-//   recurrence), epilogue adds dY, runs the cell backward, writes dG_t.
+//   step s: acc[128 batch, 32 units] = dG_prev[128, 2048] . W^T, epilogue adds
+//   dY, runs the cell backward, writes dG_t and publishes its flag.
+// Dataflow instead of a group barrier: the producer of every CTA waits only
+// for the (one or two) CTAs that produced the 64-column chunk it is about to
+// load, so chunk k's MMA overlaps the epilogues still running elsewhere.
 // The grid (<= #SMs, one CTA per SM) is launched cooperatively so every CTA
 // of a group is co-resident.
 #include "ds_internal.h"
 #include "ds_ptx.cuh"
 #include "lstm_rec.h"
 
+#include <cstdlib>
+
 namespace ds {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
+constexpr int kEpiThreads = 256;
 constexpr int kUnits = 32;            // hidden units per CTA
 constexpr int kRows = 4 * kUnits;     // gate rows per CTA
 constexpr int kH = 512;               // hidden units per direction
-constexpr int kStages = 4;
+constexpr int kUblk = kH / kUnits;    // 16 unit blocks per direction
+constexpr int kStages = 6;
 constexpr int kTileA = 128 * 64 * 2;  // one 128x64 bf16 A box (16 KB)
+constexpr int kWBytes = 128 * 1024;   // resident weight slice
+constexpr size_t kSmemBytes = 1024 + kWBytes + kStages * kTileA + 256;
 
-// forward: W slice 8 boxes of [128 rows x 64] = 128 KB
-constexpr int kFwdWBytes = (kH / 64) * kRows * 64 * 2;
-// backward: W^T slice 32 boxes of [32 rows x 64] = 128 KB
-constexpr int kBwdWBytes = (4 * kH / 64) * kUnits * 64 * 2;
-constexpr size_t kSmemBytes = 1024 + 128 * 1024 + kStages * kTileA + 256;
-
-__device__ __forceinline__ void load_bf16x8(const __nv_bfloat16* p, float* out) {
-  uint4 w = *reinterpret_cast<const uint4*>(p);
+__device__ __forceinline__ void bf16x8_to_f32(uint4 w, float* out) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -58,7 +60,7 @@ __device__ __forceinline__ void load_bf16x8(const __nv_bfloat16* p, float* out) 
     out[2 * i + 1] = f.y;
   }
 }
-__device__ __forceinline__ void store_bf16x8(__nv_bfloat16* p, const float* v) {
+__device__ __forceinline__ uint4 f32_to_bf16x8(const float* v) {
   uint4 w;
   uint32_t* u = reinterpret_cast<uint32_t*>(&w);
 #pragma unroll
@@ -66,7 +68,7 @@ __device__ __forceinline__ void store_bf16x8(__nv_bfloat16* p, const float* v) {
     __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
     u[i] = *reinterpret_cast<uint32_t*>(&h);
   }
-  *reinterpret_cast<uint4*>(p) = w;
+  return w;
 }
 
 struct Smem {
@@ -84,7 +86,7 @@ __device__ __forceinline__ Smem carve(uint8_t* raw) {
   uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   Smem m;
   m.w = s;
-  m.a = s + 128 * 1024;
+  m.a = s + kWBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(m.a + kStages * kTileA);
   m.full = bars;
   m.empty = bars + kStages;
@@ -104,7 +106,7 @@ __device__ __forceinline__ void setup(const Smem& m, uint32_t ncols) {
     }
     mbar_init(m.wbar, 1);
     mbar_init(m.tfull, 1);
-    mbar_init(m.tempty, 128);
+    mbar_init(m.tempty, kEpiThreads);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(m.tmem_slot, ncols);
@@ -113,20 +115,39 @@ __device__ __forceinline__ void setup(const Smem& m, uint32_t ncols) {
   tc_fence_after();
 }
 
-__device__ __forceinline__ void wait_group(const uint32_t* ctr, uint32_t target) {
-  while (ld_acquire_gpu(ctr) < target) {
+// spin (relaxed, L1-bypassing) until *flag >= target, then acquire and make
+// the released generic-proxy writes visible to our async-proxy (TMA) reads.
+__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target) {
+  if (ld_relaxed_gpu(flag) < target) {
+    while (ld_relaxed_gpu(flag) < target) {
+    }
   }
+}
+__device__ __forceinline__ void acquire_for_tma(const uint32_t* flag, int variant) {
+  if (variant & 4)
+    (void)ld_acquire_gpu(flag);
+  else
+    fence_acq_rel_gpu();
   fence_proxy_async_global();
 }
 
-// signal: all 128 epilogue threads finished their global writes for this step
-__device__ __forceinline__ void epi_signal(uint32_t* ctr) {
-  fence_proxy_async_global();
-  named_bar_sync(1, 128);
+// all epilogue threads finished step s's global writes -> flag = s + 1
+__device__ __forceinline__ void publish(uint32_t* flag, uint32_t value, int variant) {
+  if (!(variant & 1)) fence_proxy_async_global();
+  if (variant & 64) fence_acq_rel_gpu();  // every thread drains its own stores
+  named_bar_sync(1, kEpiThreads);
   if (threadIdx.x == kEpiWarp0 * 32) {
-    __threadfence();
-    red_release_gpu_add(ctr, 1u);
+    if (!(variant & 2)) fence_acq_rel_gpu();
+    if (variant & 64)
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+    else
+      st_release_gpu(flag, value);
   }
+}
+
+constexpr int kTraceSlots = 6;
+__device__ __forceinline__ void trace_mark(uint64_t* trace, int T, int s, int k) {
+  if (trace) trace[((size_t)blockIdx.x * T + s) * kTraceSlots + k] = globaltimer();
 }
 
 // ============================================================================
@@ -134,11 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
   extern __shared__ uint8_t smem_raw[];
   Smem m = carve(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int n_ublk = kH / kUnits;  // 16
-  const int ublk = blockIdx.x % n_ublk;
-  const int btile = (blockIdx.x / n_ublk) % P.n_btile;
-  const int dir = blockIdx.x / (n_ublk * P.n_btile);
-  uint32_t* ctr = P.counters + dir * P.n_btile + btile;
+  const int ublk = blockIdx.x % kUblk;
+  const int btile = (blockIdx.x / kUblk) % P.n_btile;
+  const int dir = blockIdx.x / (kUblk * P.n_btile);
+  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kUblk;  // step counters of the group
   const int T = P.T, B = P.B;
   const int brow0 = P.b0 + btile * 128;  // first batch row of this tile
 
@@ -150,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
       tma_prefetch_desc(&P.tmA);
       tma_prefetch_desc(&P.tmW);
       // resident W_hh slice: rows dir*2048 + ublk*128 .. +128, K = 512
-      mbar_arrive_expect_tx(m.wbar, kFwdWBytes);
+      mbar_arrive_expect_tx(m.wbar, kWBytes);
       for (int kb = 0; kb < kH / 64; ++kb)
         tma_load_2d(m.w + kb * kRows * 128, &P.tmW, m.wbar, kb * 64, dir * 4 * kH + ublk * kRows);
       int stage = 0;
@@ -158,10 +178,20 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
       for (int s = 0; s < T; ++s) {
         const int t = dir == 0 ? s : T - 1 - s;
         const int tprev = dir == 0 ? t - 1 : t + 1;  // -1 / T hit the zero pads
-        if (s > 0) wait_group(ctr, (uint32_t)(n_ublk * s));
         const int arow = (tprev + 1) * B + brow0;
         for (int kb = 0; kb < kH / 64; ++kb) {
           mbar_wait(&m.empty[stage], phase ^ 1);
+          if (s > 0 && (P.variant & 8)) {  // barrier mode: all 16 producers of step s-1
+            if (kb == 0) {
+              for (int u = 0; u < kUblk; ++u) wait_flag(flags + u, (uint32_t)s);
+              acquire_for_tma(flags + kUblk - 1, P.variant);
+            }
+          } else if (s > 0) {  // chunk kb = units kb*64.. produced by unit blocks 2kb, 2kb+1
+            wait_flag(flags + 2 * kb, (uint32_t)s);
+            wait_flag(flags + 2 * kb + 1, (uint32_t)s);
+            acquire_for_tma(flags + 2 * kb + 1, P.variant);
+          }
+          if (kb == 0) trace_mark(P.trace, T, s, 0);
           mbar_arrive_expect_tx(&m.full[stage], kTileA);
           tma_load_2d(m.a + stage * kTileA, &P.tmA, &m.full[stage], dir * kH + kb * 64, arow);
           if (++stage == kStages) {
@@ -169,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
             phase ^= 1;
           }
         }
+        trace_mark(P.trace, T, s, 1);
       }
     }
   } else if (warp == 1) {
@@ -202,61 +233,86 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
       }
     }
   } else if (warp >= kEpiWarp0) {
-    const uint32_t q = warp - kEpiWarp0;
+    const uint32_t e = warp - kEpiWarp0;
+    const uint32_t q = e & 3;   // TMEM lane quadrant (== warp % 4)
+    const uint32_t hf = e >> 2; // column half: gate rows hf*64 .. +64 = units hf*16 .. +16
     const int r = q * 32 + lane;
     const int b = brow0 + r;
     const bool ok = (r + btile * 128 < P.nb) && b < B;
-    const uint32_t trow = tmem + ((q * 32) << 16);
-    float creg[kUnits];
+    const uint32_t tcol = tmem + ((q * 32) << 16) + hf * 64;
+    const int col_g = dir * 4 * kH + ublk * kRows + hf * 64;  // first gate column
+    const int col_u = dir * kH + ublk * kUnits + hf * 16;     // first unit column
+    float creg[16];
 #pragma unroll
-    for (int u = 0; u < kUnits; ++u) creg[u] = 0.f;
+    for (int u = 0; u < 16; ++u) creg[u] = 0.f;
     for (int s = 0; s < T; ++s) {
       const int t = dir == 0 ? s : T - 1 - s;
       const size_t n = (size_t)t * B + b;
+      __nv_bfloat16* grow = P.gates + n * (8 * kH) + col_g;
+      uint4 gpre[8];
+      if (ok) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) gpre[j] = reinterpret_cast<const uint4*>(grow)[j];
+      }
       mbar_wait(m.tfull, s & 1);
       tc_fence_after();
-      __nv_bfloat16* grow = P.gates + n * (8 * kH) + dir * 4 * kH + ublk * kRows;
-      float* crow = P.cstate + n * (2 * kH) + dir * kH + ublk * kUnits;
-      __nv_bfloat16* hrow = P.y + ((size_t)(t + 1) * B + b) * (2 * kH) + dir * kH + ublk * kUnits;
-#pragma unroll
-      for (int c = 0; c < kRows; c += 32) {
-        float v[32];
-        tmem_ld16(trow + c, v);
-        tmem_ld16(trow + c + 16, v + 16);
-        tmem_ld_wait();
-        if (ok) {
-          float gi[32];
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) load_bf16x8(grow + c + j, gi + j);
-          float act[32], hv[8], cv[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            float ai = v[4 * u + 0] + gi[4 * u + 0];
-            float af = v[4 * u + 1] + gi[4 * u + 1];
-            float ag = v[4 * u + 2] + gi[4 * u + 2];
-            float ao = v[4 * u + 3] + gi[4 * u + 3];
-            float ig = sigmoidf_(ai), fg = sigmoidf_(af), gg = tanhf_(ag), og = sigmoidf_(ao);
-            const int uu = c / 4 + u;
-            float cn = fg * creg[uu] + ig * gg;
-            creg[uu] = cn;
-            cv[u] = cn;
-            hv[u] = og * tanhf_(cn);
-            act[4 * u + 0] = ig;
-            act[4 * u + 1] = fg;
-            act[4 * u + 2] = gg;
-            act[4 * u + 3] = og;
-          }
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) store_bf16x8(grow + c + j, act + j);
-          float4* c4 = reinterpret_cast<float4*>(crow + c / 4);
-          c4[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
-          c4[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
-          store_bf16x8(hrow + c / 4, hv);
-        }
-      }
+      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
+      float v[64];
+      tmem_ld32(tcol, v);
+      tmem_ld32(tcol + 32, v + 32);
+      tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(m.tempty);
-      epi_signal(ctr);
+      float hv[16], cv[16];
+      uint4 actp[8];
+      if (ok) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float gi[8];
+          bf16x8_to_f32(gpre[j], gi);
+          float act[8];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int u = 2 * j + h2;
+            float ig, fg, gg, og;
+            if (P.variant & 16) {
+              ig = v[4 * u + 0]; fg = v[4 * u + 1]; gg = v[4 * u + 2]; og = v[4 * u + 3];
+            } else {
+              ig = sigmoid_fast(v[4 * u + 0] + gi[4 * h2 + 0]);
+              fg = sigmoid_fast(v[4 * u + 1] + gi[4 * h2 + 1]);
+              gg = tanh_fast(v[4 * u + 2] + gi[4 * h2 + 2]);
+              og = sigmoid_fast(v[4 * u + 3] + gi[4 * h2 + 3]);
+            }
+            const float cn = fmaf(fg, creg[u], ig * gg);
+            creg[u] = cn;
+            cv[u] = cn;
+            hv[u] = og * tanh_fast(cn);
+            act[4 * h2 + 0] = ig;
+            act[4 * h2 + 1] = fg;
+            act[4 * h2 + 2] = gg;
+            act[4 * h2 + 3] = og;
+          }
+          actp[j] = f32_to_bf16x8(act);
+        }
+        // h_t first: it is the only value the next step of the group reads
+        uint4* h4 = reinterpret_cast<uint4*>(P.y + ((size_t)(t + 1) * B + b) * (2 * kH) + col_u);
+        h4[0] = f32_to_bf16x8(hv);
+        h4[1] = f32_to_bf16x8(hv + 8);
+      }
+      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
+      if (P.trace && lane == 0)
+        atomicMax(reinterpret_cast<unsigned long long*>(P.trace + ((size_t)blockIdx.x * T + s) * kTraceSlots + 5),
+                  (unsigned long long)globaltimer());
+      publish(flags + ublk, (uint32_t)(s + 1), P.variant);
+      // saved state for BPTT (consumed by a later launch): off the critical path
+      if (ok && !(P.variant & 32)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) reinterpret_cast<uint4*>(grow)[j] = actp[j];
+        float4* c4 = reinterpret_cast<float4*>(P.cstate + n * (2 * kH) + col_u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c4[j] = make_float4(cv[4 * j], cv[4 * j + 1], cv[4 * j + 2], cv[4 * j + 3]);
+      }
+      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 4);
     }
   }
 
@@ -271,11 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   extern __shared__ uint8_t smem_raw[];
   Smem m = carve(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int n_ublk = kH / kUnits;
-  const int ublk = blockIdx.x % n_ublk;
-  const int btile = (blockIdx.x / n_ublk) % P.n_btile;
-  const int dir = blockIdx.x / (n_ublk * P.n_btile);
-  uint32_t* ctr = P.counters + dir * P.n_btile + btile;
+  const int ublk = blockIdx.x % kUblk;
+  const int btile = (blockIdx.x / kUblk) % P.n_btile;
+  const int dir = blockIdx.x / (kUblk * P.n_btile);
+  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kUblk;
   const int T = P.T, B = P.B;
   const int brow0 = P.b0 + btile * 128;
   constexpr int kKB = 4 * kH / 64;  // 32 k-blocks over the direction's 2048 gate rows
@@ -288,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       tma_prefetch_desc(&P.tmA);
       tma_prefetch_desc(&P.tmW);
       // resident W_hh^T slice: rows dir*512 + ublk*32 .. +32, K = 2048
-      mbar_arrive_expect_tx(m.wbar, kBwdWBytes);
+      mbar_arrive_expect_tx(m.wbar, kWBytes);
       for (int kb = 0; kb < kKB; ++kb)
         tma_load_2d(m.w + kb * kUnits * 128, &P.tmW, m.wbar, kb * 64, dir * kH + ublk * kUnits);
       int stage = 0;
@@ -296,10 +351,27 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       for (int s = 1; s < T; ++s) {
         const int t = dir == 0 ? T - 1 - s : s;
         const int tprev = dir == 0 ? t + 1 : t - 1;  // previously processed step
-        wait_group(ctr, (uint32_t)(n_ublk * s));
         const int arow = tprev * B + brow0;
         for (int kb = 0; kb < kKB; ++kb) {
           mbar_wait(&m.empty[stage], phase ^ 1);
+          uint64_t t_empty = 0, t_flag = 0;
+          if (P.trace && blockIdx.x == 0) t_empty = globaltimer();
+          if (P.variant & 8) {
+            if (kb == 0) {
+              for (int u = 0; u < kUblk; ++u) wait_flag(flags + u, (uint32_t)s);
+              acquire_for_tma(flags + kUblk - 1, P.variant);
+            }
+          } else if ((kb & 1) == 0) {  // gate rows kb*64.. belong to unit block kb/2
+            wait_flag(flags + kb / 2, (uint32_t)s);
+            acquire_for_tma(flags + kb / 2, P.variant);
+          }
+          if (P.trace && blockIdx.x == 0) {
+            t_flag = globaltimer();
+            uint64_t* t2 = P.trace + (size_t)gridDim.x * T * kTraceSlots + ((size_t)s * kKB + kb) * 2;
+            t2[0] = t_empty;
+            t2[1] = t_flag;
+          }
+          if (kb == 0) trace_mark(P.trace, T, s, 0);
           mbar_arrive_expect_tx(&m.full[stage], kTileA);
           tma_load_2d(m.a + stage * kTileA, &P.tmA, &m.full[stage], dir * 4 * kH + kb * 64, arow);
           if (++stage == kStages) {
@@ -307,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
             phase ^= 1;
           }
         }
+        trace_mark(P.trace, T, s, 1);
       }
     }
   } else if (warp == 1) {
@@ -340,85 +413,91 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       }
     }
   } else if (warp >= kEpiWarp0) {
-    const uint32_t q = warp - kEpiWarp0;
+    const uint32_t e = warp - kEpiWarp0;
+    const uint32_t q = e & 3;
+    const uint32_t hf = e >> 2;  // units hf*16 .. +16 of the block
     const int r = q * 32 + lane;
     const int b = brow0 + r;
     const bool ok = (r + btile * 128 < P.nb) && b < B;
-    const uint32_t trow = tmem + ((q * 32) << 16);
-    float dcc[kUnits];
+    const uint32_t tcol = tmem + ((q * 32) << 16) + hf * 16;
+    const int col_g = dir * 4 * kH + ublk * kRows + hf * 64;
+    const int col_u = dir * kH + ublk * kUnits + hf * 16;
+    float dcc[16];
 #pragma unroll
-    for (int u = 0; u < kUnits; ++u) dcc[u] = 0.f;
+    for (int u = 0; u < 16; ++u) dcc[u] = 0.f;
     for (int s = 0; s < T; ++s) {
       const int t = dir == 0 ? T - 1 - s : s;
       const int tc = dir == 0 ? t - 1 : t + 1;  // forward-order predecessor (c_prev)
       const bool has_cprev = tc >= 0 && tc < T;
       const size_t n = (size_t)t * B + b;
+      // prefetch everything this step reads before waiting on the recurrence
+      uint4 apre[8], dypre[2];
+      float4 cpre[4], cppre[4];
+      if (ok) {
+        const uint4* ap = reinterpret_cast<const uint4*>(P.gates + n * (8 * kH) + col_g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) apre[j] = ap[j];
+        const uint4* dp = reinterpret_cast<const uint4*>(P.dy + n * (2 * kH) + col_u);
+        dypre[0] = dp[0];
+        dypre[1] = dp[1];
+        const float4* cp = reinterpret_cast<const float4*>(P.cstate + n * (2 * kH) + col_u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cpre[j] = cp[j];
+        if (has_cprev) {
+          const float4* pp = reinterpret_cast<const float4*>(P.cstate + ((size_t)tc * B + b) * (2 * kH) + col_u);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cppre[j] = pp[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cppre[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      float dh[16];
       if (s > 0) {
         mbar_wait(m.tfull, (s - 1) & 1);
         tc_fence_after();
-      }
-      const __nv_bfloat16* arow = P.gates + n * (8 * kH) + dir * 4 * kH + ublk * kRows;
-      const float* crow = P.cstate + n * (2 * kH) + dir * kH + ublk * kUnits;
-      const float* cprow = P.cstate + ((size_t)tc * B + b) * (2 * kH) + dir * kH + ublk * kUnits;
-      const __nv_bfloat16* dyrow = P.dy + n * (2 * kH) + dir * kH + ublk * kUnits;
-      __nv_bfloat16* dgrow = P.dg + n * (8 * kH) + dir * 4 * kH + ublk * kRows;
-#pragma unroll
-      for (int c = 0; c < kUnits; c += 16) {
-        float dh[16];
-        if (s > 0) {
-          tmem_ld16(trow + c, dh);
-          tmem_ld_wait();
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) dh[i] = 0.f;
-        }
-        if (ok) {
-          float dyv[16];
-          load_bf16x8(dyrow + c, dyv);
-          load_bf16x8(dyrow + c + 8, dyv + 8);
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            float act[32];
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) load_bf16x8(arow + 4 * (c + 8 * half) + j, act + j);
-            float cc[8], cp[8];
-            const float4* c4 = reinterpret_cast<const float4*>(crow + c + 8 * half);
-            float4 x0 = c4[0], x1 = c4[1];
-            cc[0] = x0.x; cc[1] = x0.y; cc[2] = x0.z; cc[3] = x0.w;
-            cc[4] = x1.x; cc[5] = x1.y; cc[6] = x1.z; cc[7] = x1.w;
-            if (has_cprev) {
-              const float4* p4 = reinterpret_cast<const float4*>(cprow + c + 8 * half);
-              float4 y0 = p4[0], y1 = p4[1];
-              cp[0] = y0.x; cp[1] = y0.y; cp[2] = y0.z; cp[3] = y0.w;
-              cp[4] = y1.x; cp[5] = y1.y; cp[6] = y1.z; cp[7] = y1.w;
-            } else {
-#pragma unroll
-              for (int u = 0; u < 8; ++u) cp[u] = 0.f;
-            }
-            float dgv[32];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int uu = c + 8 * half + u;
-              const float ig = act[4 * u + 0], fg = act[4 * u + 1], gg = act[4 * u + 2], og = act[4 * u + 3];
-              const float dht = dh[8 * half + u] + dyv[8 * half + u];
-              const float tcn = tanhf_(cc[u]);
-              const float dct = dht * og * (1.f - tcn * tcn) + dcc[uu];
-              dgv[4 * u + 0] = dct * gg * ig * (1.f - ig);
-              dgv[4 * u + 1] = dct * cp[u] * fg * (1.f - fg);
-              dgv[4 * u + 2] = dct * ig * (1.f - gg * gg);
-              dgv[4 * u + 3] = dht * tcn * og * (1.f - og);
-              dcc[uu] = dct * fg;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) store_bf16x8(dgrow + 4 * (c + 8 * half) + j, dgv + j);
-          }
-        }
-      }
-      if (s > 0) {
+        if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
+        tmem_ld16(tcol, dh);
+        tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(m.tempty);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dh[i] = 0.f;
       }
-      epi_signal(ctr);
+      if (ok) {
+        float dyv[16], cc[16], cp[16];
+        bf16x8_to_f32(dypre[0], dyv);
+        bf16x8_to_f32(dypre[1], dyv + 8);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          cc[4 * j] = cpre[j].x; cc[4 * j + 1] = cpre[j].y; cc[4 * j + 2] = cpre[j].z; cc[4 * j + 3] = cpre[j].w;
+          cp[4 * j] = cppre[j].x; cp[4 * j + 1] = cppre[j].y; cp[4 * j + 2] = cppre[j].z; cp[4 * j + 3] = cppre[j].w;
+        }
+        uint4* dgrow = reinterpret_cast<uint4*>(P.dg + n * (8 * kH) + col_g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float act[8], dgv[8];
+          bf16x8_to_f32(apre[j], act);
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int u = 2 * j + h2;
+            const float ig = act[4 * h2 + 0], fg = act[4 * h2 + 1], gg = act[4 * h2 + 2], og = act[4 * h2 + 3];
+            const float dht = dh[u] + dyv[u];
+            const float tcn = tanh_fast(cc[u]);
+            const float dct = fmaf(dht * og, 1.f - tcn * tcn, dcc[u]);
+            dgv[4 * h2 + 0] = dct * gg * ig * (1.f - ig);
+            dgv[4 * h2 + 1] = dct * cp[u] * fg * (1.f - fg);
+            dgv[4 * h2 + 2] = dct * ig * (1.f - gg * gg);
+            dgv[4 * h2 + 3] = dht * tcn * og * (1.f - og);
+            dcc[u] = dct * fg;
+          }
+          dgrow[j] = f32_to_bf16x8(dgv);
+        }
+      }
+      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
+      publish(flags + ublk, (uint32_t)(s + 1), P.variant);
+      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 4);
     }
   }
 
@@ -446,6 +525,9 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
   return DS_OK;
 }
 
+int lstm_max_tiles() { return num_sms() / (2 * kUblk); }
+int lstm_counter_words(int B) { return 2 * kUblk * ((B + 127) / 128); }
+
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -454,7 +536,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     attr_set = true;
   }
   const int B = a.B, T = a.T;
-  const int max_tiles = num_sms() / (2 * (kH / kUnits));  // co-resident tiles per launch
+  const int max_tiles = lstm_max_tiles();
   if (max_tiles < 1) return fail_arg("device too small for the recurrent kernel");
   LstmParams P;
   memset(&P, 0, sizeof(P));
@@ -476,6 +558,11 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   P.y = a.y_full;
   P.dy = a.dy;
   P.dg = a.dg;
+  P.trace = a.trace;
+  {
+    const char* v = getenv("DS_LSTM_VARIANT");
+    P.variant = v ? atoi(v) : 7;  // 7: acquire by ld.acquire, no writer-side fences
+  }
   P.B = B;
   P.T = T;
   const int chunk_rows = max_tiles * 128;
@@ -484,11 +571,12 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.b0 = b0;
     P.nb = nb;
     P.n_btile = (nb + 127) / 128;
-    P.counters = a.counters + (b0 / 128) * 2;
-    DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * P.n_btile, stream));
-    const int grid = 2 * (kH / kUnits) * P.n_btile;
+    P.counters = a.counters + (b0 / 128) * 2 * kUblk;
+    DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * kUblk * P.n_btile, stream));
+    const int grid = 2 * kUblk * P.n_btile;
     rc = launch_coop(fwd ? (const void*)lstm_fwd_kernel : (const void*)lstm_bwd_kernel, grid, P, stream);
     if (rc) return rc;
+    P.trace = nullptr;  // trace only the first chunk
   }
   return DS_OK;
 }

@@ -16,7 +16,9 @@ struct LstmParams {
   const __nv_bfloat16* dy;
   __nv_bfloat16* dg;
   uint32_t* counters;
+  uint64_t* trace;  // optional per-(CTA, step) globaltimer marks (debug)
   int B, T, b0, nb, n_btile;
+  int variant;  // debug: bit0 skip writer proxy fence, bit1 skip release fence
 };
 
 struct LstmLayerArgs {
@@ -27,9 +29,12 @@ struct LstmLayerArgs {
   const __nv_bfloat16* w;   // forward: W_hh bf16 [4096, 512]; backward: W_hh^T bf16 [1024, 2048]
   const __nv_bfloat16* dy;  // backward: [T*B, 1024]
   __nv_bfloat16* dg;        // backward: [T*B, 4096]
-  uint32_t* counters;       // >= 2 * ceil(B / 128)
+  uint32_t* counters;       // >= lstm_counter_words(B)
+  uint64_t* trace = nullptr;
 };
 
+int lstm_max_tiles();
+int lstm_counter_words(int B);
 int lstm_forward(const LstmLayerArgs& a, cudaStream_t stream);
 int lstm_backward(const LstmLayerArgs& a, cudaStream_t stream);
 

@@ -62,24 +62,38 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int ncols, f
 }
 
 // --------------------------------------------------------------------------
-// soft-max / CE combine: lse[m] = logsumexp over column tiles of (max, sumexp)
-// partials; loss_sum += lse - target_logit (one block, deterministic order).
-__global__ void ce_combine_kernel(const float2* __restrict__ stats, int ntiles, int64_t ld, const float* __restrict__ tgt,
-                                  int M, float* __restrict__ lse, float* __restrict__ loss_sum, int* __restrict__ flag) {
-  __shared__ float red[1024];
-  float acc = 0.f;
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+// soft-max / CE combine: lse[m] = logsumexp over column-tile (max, sumexp)
+// partials; per-block loss partials, then one ordered sum (deterministic).
+constexpr int kCeRows = 256;
+__global__ void ce_rows_kernel(const float2* __restrict__ stats, int ntiles, int64_t ld, const float* __restrict__ tgt,
+                               int M, float* __restrict__ lse, float* __restrict__ part) {
+  __shared__ float red[kCeRows];
+  const int m = blockIdx.x * kCeRows + threadIdx.x;
+  float loss = 0.f;
+  if (m < M) {
     float mx = -INFINITY;
     for (int j = 0; j < ntiles; ++j) mx = fmaxf(mx, stats[j * ld + m].x);
     float s = 0.f;
     for (int j = 0; j < ntiles; ++j) {
-      float2 st = stats[j * ld + m];
+      const float2 st = stats[j * ld + m];
       s += st.y * __expf(st.x - mx);
     }
-    float l = mx + __logf(s);
+    const float l = mx + __logf(s);
     lse[m] = l;
-    acc += l - tgt[m];
+    loss = l - tgt[m];
   }
+  red[threadIdx.x] = loss;
+  __syncthreads();
+  for (int w = kCeRows / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+__global__ void ce_sum_kernel(const float* __restrict__ part, int n, float* __restrict__ loss_sum, int* __restrict__ flag) {
+  __shared__ float red[256];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -87,9 +101,8 @@ __global__ void ce_combine_kernel(const float2* __restrict__ stats, int ntiles, 
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    float tot = red[0];
-    *loss_sum = tot;
-    if (flag && !isfinite(tot)) atomicOr(flag, 1);
+    *loss_sum = red[0];
+    if (flag && !isfinite(red[0])) atomicOr(flag, 1);
   }
 }
 
@@ -260,9 +273,11 @@ int op_colsum(const __nv_bfloat16* x, int64_t rows, int ncols, int64_t ld, float
 }
 int64_t op_colsum_scratch(int ncols) { return (int64_t)kColSplit * ncols; }
 
-int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt, int M, float* lse, float* loss_sum,
-                  int* flag, cudaStream_t s) {
-  ce_combine_kernel<<<1, 1024, 0, s>>>(stats, ntiles, ld, tgt, M, lse, loss_sum, flag);
+int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt, int M, float* lse, float* scratch,
+                  float* loss_sum, int* flag, cudaStream_t s) {
+  const int nblk = (M + kCeRows - 1) / kCeRows;
+  ce_rows_kernel<<<nblk, kCeRows, 0, s>>>(stats, ntiles, ld, tgt, M, lse, scratch);
+  ce_sum_kernel<<<1, 256, 0, s>>>(scratch, nblk, loss_sum, flag);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }

@@ -118,9 +118,9 @@ def test_lstm_recurrent_fwd_bwd(B, T):
     gates = G.clone()
     cstate = torch.zeros(N, 2 * H, device=DEV)
     yfull = torch.zeros((T + 2) * B, 2 * H, device=DEV, dtype=torch.bfloat16)
-    counters = torch.zeros(64, device=DEV, dtype=torch.int32)
+    counters = torch.zeros(1024, device=DEV, dtype=torch.int32)
     rc = lib.ds_debug_lstm_fwd(B, T, gates.data_ptr(), cstate.data_ptr(), yfull.data_ptr(), W.data_ptr(),
-                               counters.data_ptr(), _lib.stream_ptr())
+                               counters.data_ptr(), None, _lib.stream_ptr())
     _lib.check(rc, "lstm_fwd")
     torch.cuda.synchronize()
     Y, C, A = _lstm_ref_fwd(G, W, B, T)
@@ -134,7 +134,7 @@ def test_lstm_recurrent_fwd_bwd(B, T):
     dY = torch.randn(N, 2 * H, device=DEV, generator=g).bfloat16()
     dg = torch.zeros(N, 8 * H, device=DEV, dtype=torch.bfloat16)
     rc = lib.ds_debug_lstm_bwd(B, T, gates.data_ptr(), cstate.data_ptr(), WT.data_ptr(), dY.data_ptr(),
-                               dg.data_ptr(), counters.data_ptr(), _lib.stream_ptr())
+                               dg.data_ptr(), counters.data_ptr(), None, _lib.stream_ptr())
     _lib.check(rc, "lstm_bwd")
     torch.cuda.synchronize()
     ref = _lstm_ref_bwd(gates, cstate, dY, WT, B, T)
