@@ -323,58 +323,92 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
 }
 
 // ============================================================================
+// Backward: split-K over a 4-CTA cluster.
+//   cluster = (dir, batch tile, unit group ug of 64 units); CTA rank ks holds
+//   W_hh^T[64 units of ug][gate rows ks*512 .. +512] (64 KB) and streams the
+//   matching 512-row K slice of dG_prev (128 KB, all 8 chunks in flight).
+//   Partial dh[128 batch, 64 units] (TMEM) is exchanged through DSMEM: CTA ks
+//   finalises units ug*64 + ks*16 .. +16, runs their cell backward and writes
+//   exactly one 64-gate-row chunk (chunk id ug*4 + ks) of dG_t.
+namespace bwd {
+constexpr int kKS = 4;                       // cluster size (K splits)
+constexpr int kGU = 64;                      // units per cluster
+constexpr int kFU = kGU / kKS;               // 16 units finalised per CTA
+constexpr int kKSlice = 4 * kH / kKS;        // 512 gate rows per CTA
+constexpr int kChunks = kKSlice / 64;        // 8 A chunks per step
+constexpr int kStagesB = 8;
+constexpr int kWBytesB = kGU * kKSlice * 2;  // 64 KB
+constexpr int kRecvSlot = 128 * kFU * 4;     // 8 KB: one source's [128 rows x 16 units] fp32
+constexpr int kRecvBytes = kKS * kRecvSlot;  // 4 sources
+constexpr size_t kSmem = 1024 + kWBytesB + kStagesB * kTileA + kRecvBytes + 512;
+}  // namespace bwd
+
 __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_constant__ LstmParams P) {
+  using namespace bwd;
   extern __shared__ uint8_t smem_raw[];
-  Smem m = carve(smem_raw);
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = sm;
+  uint8_t* sA = sW + kWBytesB;
+  float* recv = reinterpret_cast<float*>(sA + kStagesB * kTileA);  // [kKS][128][16]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(recv) + kRecvBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStagesB;
+  uint64_t* wbar = empty + kStagesB;
+  uint64_t* tfull = wbar + 1;
+  uint64_t* tempty = tfull + 1;
+  uint64_t* rfull = tempty + 1;  // recv buffer complete (all 4 sources)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 1);
+
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int ublk = blockIdx.x % kUblk;
-  const int btile = (blockIdx.x / kUblk) % P.n_btile;
-  const int dir = blockIdx.x / (kUblk * P.n_btile);
-  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kUblk;
+  const int ks = (int)cluster_ctarank();
+  const int ug = (blockIdx.x / kKS) % (kH / kGU);
+  const int btile = (blockIdx.x / (kKS * (kH / kGU))) % P.n_btile;
+  const int dir = blockIdx.x / (kKS * (kH / kGU) * P.n_btile);
+  constexpr int kFlagsPerGroup = 4 * kH / 64;  // 32 chunks per (dir, btile)
+  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kFlagsPerGroup;
   const int T = P.T, B = P.B;
   const int brow0 = P.b0 + btile * 128;
-  constexpr int kKB = 4 * kH / 64;  // 32 k-blocks over the direction's 2048 gate rows
+  const int my_chunk = ug * kKS + ks;
 
-  setup(m, 32);
-  const uint32_t tmem = *m.tmem_slot;
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < kStagesB; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(wbar, 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kEpiThreads);
+    mbar_init(rfull, kKS * 4);  // 4 source CTAs x 4 writer warps
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 64);
+  tc_fence_before();
+  cluster_sync_all();  // peers' barriers initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch_desc(&P.tmA);
       tma_prefetch_desc(&P.tmW);
-      // resident W_hh^T slice: rows dir*512 + ublk*32 .. +32, K = 2048
-      mbar_arrive_expect_tx(m.wbar, kWBytes);
-      for (int kb = 0; kb < kKB; ++kb)
-        tma_load_2d(m.w + kb * kUnits * 128, &P.tmW, m.wbar, kb * 64, dir * kH + ublk * kUnits);
+      mbar_arrive_expect_tx(wbar, kWBytesB);
+      for (int j = 0; j < kChunks; ++j)
+        tma_load_2d(sW + j * kGU * 128, &P.tmW, wbar, ks * kKSlice + j * 64, dir * kH + ug * kGU);
       int stage = 0;
       uint32_t phase = 0;
       for (int s = 1; s < T; ++s) {
         const int t = dir == 0 ? T - 1 - s : s;
-        const int tprev = dir == 0 ? t + 1 : t - 1;  // previously processed step
+        const int tprev = dir == 0 ? t + 1 : t - 1;
         const int arow = tprev * B + brow0;
-        for (int kb = 0; kb < kKB; ++kb) {
-          mbar_wait(&m.empty[stage], phase ^ 1);
-          uint64_t t_empty = 0, t_flag = 0;
-          if (P.trace && blockIdx.x == 0) t_empty = globaltimer();
-          if (P.variant & 8) {
-            if (kb == 0) {
-              for (int u = 0; u < kUblk; ++u) wait_flag(flags + u, (uint32_t)s);
-              acquire_for_tma(flags + kUblk - 1, P.variant);
-            }
-          } else if ((kb & 1) == 0) {  // gate rows kb*64.. belong to unit block kb/2
-            wait_flag(flags + kb / 2, (uint32_t)s);
-            acquire_for_tma(flags + kb / 2, P.variant);
-          }
-          if (P.trace && blockIdx.x == 0) {
-            t_flag = globaltimer();
-            uint64_t* t2 = P.trace + (size_t)gridDim.x * T * kTraceSlots + ((size_t)s * kKB + kb) * 2;
-            t2[0] = t_empty;
-            t2[1] = t_flag;
-          }
-          if (kb == 0) trace_mark(P.trace, T, s, 0);
-          mbar_arrive_expect_tx(&m.full[stage], kTileA);
-          tma_load_2d(m.a + stage * kTileA, &P.tmA, &m.full[stage], dir * 4 * kH + kb * 64, arow);
-          if (++stage == kStages) {
+        for (int j = 0; j < kChunks; ++j) {
+          const int chunk = ks * kChunks + j;
+          mbar_wait(&empty[stage], phase ^ 1);
+          wait_flag(flags + chunk, (uint32_t)s);
+          acquire_for_tma(flags + chunk, P.variant);
+          if (j == 0) trace_mark(P.trace, T, s, 0);
+          mbar_arrive_expect_tx(&full[stage], kTileA);
+          tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
+          if (++stage == kStagesB) {
             stage = 0;
             phase ^= 1;
           }
@@ -383,30 +417,30 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       }
     }
   } else if (warp == 1) {
-    mbar_wait(m.wbar, 0);
-    const uint32_t idesc = idesc_bf16_f32(128, kUnits, 0, 0);
-    const uint32_t wbase = smem_u32(m.w);
+    mbar_wait(wbar, 0);
+    const uint32_t idesc = idesc_bf16_f32(128, kGU, 0, 0);
+    const uint32_t wbase = smem_u32(sW);
     int stage = 0;
     uint32_t phase = 0;
     for (int s = 1; s < T; ++s) {
-      mbar_wait(m.tempty, ((s - 1) & 1) ^ 1);
+      mbar_wait(tempty, ((s - 1) & 1) ^ 1);
       tc_fence_after();
-      for (int kb = 0; kb < kKB; ++kb) {
-        mbar_wait(&m.full[stage], phase);
+      for (int j = 0; j < kChunks; ++j) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t abase = smem_u32(m.a + stage * kTileA);
+          const uint32_t abase = smem_u32(sA + stage * kTileA);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             uint64_t ad = smem_desc_sw128(abase + k * 32, 16, 1024);
-            uint64_t bd = smem_desc_sw128(wbase + kb * kUnits * 128 + k * 32, 16, 1024);
-            mma_bf16_ss(tmem, ad, bd, idesc, (kb | k) != 0);
+            uint64_t bd = smem_desc_sw128(wbase + j * kGU * 128 + k * 32, 16, 1024);
+            mma_bf16_ss(tmem, ad, bd, idesc, (j | k) != 0);
           }
-          mma_commit(&m.empty[stage]);
-          if (kb == kKB - 1) mma_commit(m.tfull);
+          mma_commit(&empty[stage]);
+          if (j == kChunks - 1) mma_commit(tfull);
         }
         __syncwarp();
-        if (++stage == kStages) {
+        if (++stage == kStagesB) {
           stage = 0;
           phase ^= 1;
         }
@@ -415,68 +449,99 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   } else if (warp >= kEpiWarp0) {
     const uint32_t e = warp - kEpiWarp0;
     const uint32_t q = e & 3;
-    const uint32_t hf = e >> 2;  // units hf*16 .. +16 of the block
+    const uint32_t hf = e >> 2;
     const int r = q * 32 + lane;
     const int b = brow0 + r;
     const bool ok = (r + btile * 128 < P.nb) && b < B;
-    const uint32_t tcol = tmem + ((q * 32) << 16) + hf * 16;
-    const int col_g = dir * 4 * kH + ublk * kRows + hf * 64;
-    const int col_u = dir * kH + ublk * kUnits + hf * 16;
-    float dcc[16];
+    // exchange: this thread's partial columns hf*32 .. +32 = finalisers 2hf, 2hf+1
+    const uint32_t tcol = tmem + ((q * 32) << 16) + hf * 32;
+    // cell backward: row r, units ug*64 + ks*16 + hf*8 .. +8
+    const int unit0 = ug * kGU + ks * kFU + hf * 8;
+    const int col_g = dir * 4 * kH + unit0 * 4;
+    const int col_u = dir * kH + unit0;
+    const uint32_t recv_base = smem_u32(recv);
+    float dcc[8];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) dcc[u] = 0.f;
+    for (int u = 0; u < 8; ++u) dcc[u] = 0.f;
     for (int s = 0; s < T; ++s) {
       const int t = dir == 0 ? T - 1 - s : s;
-      const int tc = dir == 0 ? t - 1 : t + 1;  // forward-order predecessor (c_prev)
+      const int tc = dir == 0 ? t - 1 : t + 1;
       const bool has_cprev = tc >= 0 && tc < T;
       const size_t n = (size_t)t * B + b;
-      // prefetch everything this step reads before waiting on the recurrence
-      uint4 apre[8], dypre[2];
-      float4 cpre[4], cppre[4];
+      uint4 apre[4], dypre;
+      float4 cpre[2], cppre[2];
       if (ok) {
         const uint4* ap = reinterpret_cast<const uint4*>(P.gates + n * (8 * kH) + col_g);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) apre[j] = ap[j];
-        const uint4* dp = reinterpret_cast<const uint4*>(P.dy + n * (2 * kH) + col_u);
-        dypre[0] = dp[0];
-        dypre[1] = dp[1];
+        for (int j = 0; j < 4; ++j) apre[j] = ap[j];
+        dypre = *reinterpret_cast<const uint4*>(P.dy + n * (2 * kH) + col_u);
         const float4* cp = reinterpret_cast<const float4*>(P.cstate + n * (2 * kH) + col_u);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) cpre[j] = cp[j];
+        cpre[0] = cp[0];
+        cpre[1] = cp[1];
         if (has_cprev) {
           const float4* pp = reinterpret_cast<const float4*>(P.cstate + ((size_t)tc * B + b) * (2 * kH) + col_u);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) cppre[j] = pp[j];
+          cppre[0] = pp[0];
+          cppre[1] = pp[1];
         } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) cppre[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          cppre[0] = cppre[1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
-      float dh[16];
+      float dh[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dh[u] = 0.f;
+      // the finalisers we feed must have consumed the previous exchange
+      // (checked before the MMA wait so the L2 round trip overlaps it)
+      if (s >= 2 && lane == 0) {
+        wait_flag(flags + ug * kKS + 2 * hf, (uint32_t)s);
+        wait_flag(flags + ug * kKS + 2 * hf + 1, (uint32_t)s);
+      }
+      __syncwarp();
       if (s > 0) {
-        mbar_wait(m.tfull, (s - 1) & 1);
+        mbar_wait(tfull, (s - 1) & 1);
         tc_fence_after();
         if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
-        tmem_ld16(tcol, dh);
+        float v[32];
+        tmem_ld32(tcol, v);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(m.tempty);
-      } else {
+        mbar_arrive(tempty);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) dh[i] = 0.f;
+        for (int f2 = 0; f2 < 2; ++f2) {
+          const int f = 2 * hf + f2;
+          const uint32_t local = recv_base + (uint32_t)((ks * 128 + r) * kFU * 4);
+          const uint32_t dst = mapa_shared(local, (uint32_t)f);
+#pragma unroll
+          for (int i = 0; i < kFU; i += 4)
+            st_cluster_v4(dst + i * 4, v[f2 * kFU + i], v[f2 * kFU + i + 1], v[f2 * kFU + i + 2],
+                          v[f2 * kFU + i + 3]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int f2 = 0; f2 < 2; ++f2)
+            mbar_arrive_remote_release(mapa_shared(smem_u32(rfull), (uint32_t)(2 * hf + f2)));
+        }
+        mbar_wait_acq_cluster(rfull, (s - 1) & 1);
+        if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 5);
+        const float* rb = recv;
+#pragma unroll
+        for (int src = 0; src < kKS; ++src) {
+          const float4* p4 = reinterpret_cast<const float4*>(rb + ((size_t)src * 128 + r) * kFU + hf * 8);
+          const float4 x0 = p4[0], x1 = p4[1];
+          dh[0] += x0.x; dh[1] += x0.y; dh[2] += x0.z; dh[3] += x0.w;
+          dh[4] += x1.x; dh[5] += x1.y; dh[6] += x1.z; dh[7] += x1.w;
+        }
       }
       if (ok) {
-        float dyv[16], cc[16], cp[16];
-        bf16x8_to_f32(dypre[0], dyv);
-        bf16x8_to_f32(dypre[1], dyv + 8);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          cc[4 * j] = cpre[j].x; cc[4 * j + 1] = cpre[j].y; cc[4 * j + 2] = cpre[j].z; cc[4 * j + 3] = cpre[j].w;
-          cp[4 * j] = cppre[j].x; cp[4 * j + 1] = cppre[j].y; cp[4 * j + 2] = cppre[j].z; cp[4 * j + 3] = cppre[j].w;
-        }
+        float dyv[8], cc[8], cp[8];
+        bf16x8_to_f32(dypre, dyv);
+        cc[0] = cpre[0].x; cc[1] = cpre[0].y; cc[2] = cpre[0].z; cc[3] = cpre[0].w;
+        cc[4] = cpre[1].x; cc[5] = cpre[1].y; cc[6] = cpre[1].z; cc[7] = cpre[1].w;
+        cp[0] = cppre[0].x; cp[1] = cppre[0].y; cp[2] = cppre[0].z; cp[3] = cppre[0].w;
+        cp[4] = cppre[1].x; cp[5] = cppre[1].y; cp[6] = cppre[1].z; cp[7] = cppre[1].w;
         uint4* dgrow = reinterpret_cast<uint4*>(P.dg + n * (8 * kH) + col_g);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 4; ++j) {
           float act[8], dgv[8];
           bf16x8_to_f32(apre[j], act);
 #pragma unroll
@@ -496,47 +561,63 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         }
       }
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
-      publish(flags + ublk, (uint32_t)(s + 1), P.variant);
+      publish(flags + my_chunk, (uint32_t)(s + 1), P.variant);
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 4);
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // no CTA leaves while a peer may still touch its smem
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 32);
+  if (warp == 2) tmem_dealloc(tmem, 64);
 }
 
 }  // namespace
 
-static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream_t stream) {
+static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream_t stream, size_t smem,
+                       int cluster) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  } else {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   void* args[] = {const_cast<LstmParams*>(&P)};
   DS_CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, args));
   return DS_OK;
 }
 
+// batch tiles per launch: forward 32 CTAs / tile; backward 64 CTAs / tile in
+// clusters of 4 (cluster placement leaves some SMs unusable: keep <= 128)
 int lstm_max_tiles() { return num_sms() / (2 * kUblk); }
-int lstm_counter_words(int B) { return 2 * kUblk * ((B + 127) / 128); }
+static int lstm_bwd_max_tiles() { return (num_sms() >= 132 ? 128 : num_sms()) / 64; }
+int lstm_counter_words(int B) { return 2 * 32 * ((B + 127) / 128); }
 
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
     DS_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
-    DS_CUDA_TRY(cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    DS_CUDA_TRY(
+        cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmem));
     attr_set = true;
   }
   const int B = a.B, T = a.T;
-  const int max_tiles = lstm_max_tiles();
+  const int max_tiles = fwd ? lstm_max_tiles() : lstm_bwd_max_tiles();
   if (max_tiles < 1) return fail_arg("device too small for the recurrent kernel");
   LstmParams P;
   memset(&P, 0, sizeof(P));
@@ -550,7 +631,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   } else {
     rc = make_tmap_2d(&P.tmA, a.dg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 8 * kH, (uint64_t)T * B, 8 * kH * 2, 64, 128);
     if (rc) return rc;
-    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4 * kH, 2 * kH, 4 * kH * 2, 64, kUnits);
+    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4 * kH, 2 * kH, 4 * kH * 2, 64, bwd::kGU);
     if (rc) return rc;
   }
   P.gates = a.gates;
@@ -571,10 +652,12 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.b0 = b0;
     P.nb = nb;
     P.n_btile = (nb + 127) / 128;
-    P.counters = a.counters + (b0 / 128) * 2 * kUblk;
-    DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * kUblk * P.n_btile, stream));
-    const int grid = 2 * kUblk * P.n_btile;
-    rc = launch_coop(fwd ? (const void*)lstm_fwd_kernel : (const void*)lstm_bwd_kernel, grid, P, stream);
+    P.counters = a.counters + (b0 / 128) * 2 * 32;
+    DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * 32 * P.n_btile, stream));
+    if (fwd)
+      rc = launch_coop((const void*)lstm_fwd_kernel, 2 * kUblk * P.n_btile, P, stream, kSmemBytes, 1);
+    else
+      rc = launch_coop((const void*)lstm_bwd_kernel, 64 * P.n_btile, P, stream, bwd::kSmem, bwd::kKS);
     if (rc) return rc;
     P.trace = nullptr;  // trace only the first chunk
   }

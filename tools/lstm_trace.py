@@ -26,7 +26,7 @@ dY = torch.randn(N, 2 * H, device=dev).bfloat16()
 dg = torch.zeros(N, 8 * H, device=dev, dtype=torch.bfloat16)
 ntile = (B + 127) // 128
 grid = 32 * ntile
-trace = torch.zeros(grid * T * 6 + T * 32 * 2, device=dev, dtype=torch.int64)
+trace = torch.zeros(2 * grid * T * 6 + T * 32 * 2, device=dev, dtype=torch.int64)
 s = _lib.stream_ptr()
 
 
@@ -57,8 +57,9 @@ for name, fn in (("fwd", fwd), ("bwd", bwd)):
     fn(trace.data_ptr())
     torch.cuda.synchronize()
     full = trace.cpu().numpy().astype(np.float64)
-    tr = full[:grid * T * 6].reshape(grid, T, 6)
-    t2 = full[grid * T * 6:].reshape(T, 32, 2)
+    g = grid if name == "fwd" else 2 * grid
+    tr = full[:g * T * 6].reshape(g, T, 6)
+    t2 = full[g * T * 6:g * T * 6 + T * 64].reshape(T, 32, 2)
     base = tr[tr > 0].min()
     tr = np.where(tr > 0, tr - base, np.nan) / 1e3
     # per step: median over CTAs of (ready, issued, mma_done, published)
@@ -68,7 +69,7 @@ for name, fn in (("fwd", fwd), ("bwd", bwd)):
         print(f"  step {st:2d} med ready {med[0]:7.2f} issued {med[1]:7.2f} mma {med[2]:7.2f} stored {med[3]:7.2f}"
               f" lastwarp {med[5]:7.2f} pub {med[4]:7.2f} | max pub {mx[4]:7.2f}")
     pub = np.nanmax(tr[:, :, 4], axis=0)
-    if name == "bwd":
+    if False:
         b2 = np.where(t2 > 0, t2 - base, np.nan) / 1e3
         for st in (5, 6):
             print("  cta0 step", st, "stage-ready:", np.round(b2[st, :, 0], 2))
