@@ -92,7 +92,20 @@ int ds_adpsgd_mix(float* theta_a, float* theta_b, int64_t n, ds_stream_t stream)
  * snap_owners may be NULL or hold per-member handles to refresh. */
 int ds_group_reduce(int32_t world, int32_t rank, float* const* grads, float* const* thetas, float* const* vels,
                     ds_blstm* const* snap_owners, int64_t n, int32_t nchunks, float lr, float mu, int32_t mode,
-                    ds_stream_t stream);
+                    float divisor, ds_stream_t stream);
+/* `divisor` (mode 0): g_mean = canonical_sum / divisor; <= 0 selects `world`
+ * (the SSGD `/ learners` of engines/ssgd.py:85).  H-ADPSGD passes 1 with
+ * member gradients already scaled by 1/(group frames). */
+
+/* K12: consensus out = (((x_0 + x_1) + ...) + x_{n-1}) / n in member order
+ * (np.mean(np.stack(..)) of engines/adpsgd.py:293-295 / :339-342). */
+int ds_average(int32_t n, float* const* srcs, float* out, int64_t dim, ds_stream_t stream);
+
+/* CE gradient divisor override for the following ds_blstm_fwd_bwd calls:
+ * frames_total > 0 scales dlogits by 1/frames_total instead of 1/(B*T) so a
+ * group's member gradients sum to the gradient of the union batch (H-ADPSGD,
+ * SURVEY §8 a19).  0 restores the per-batch mean. */
+int ds_blstm_set_grad_scale(ds_blstm* h, float frames_total);
 
 /* Phase profiling (bench/tests): when enabled the step is issued without the
  * CUDA graph and CUDA events bracket every phase; ds_blstm_profile_read sums

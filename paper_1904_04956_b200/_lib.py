@@ -34,7 +34,9 @@ SIGNATURES = {
     "ds_blstm_loss": (_I32, [_VP, _VP, _I32, _VP, _VP, _VP]),
     "ds_sgd_momentum": (_I32, [_VP, _VP, _VP, _F32, _F32, _I64, _VP, _VP, _VP]),
     "ds_adpsgd_mix": (_I32, [_VP, _VP, _I64, _VP]),
-    "ds_group_reduce": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _I64, _I32, _F32, _F32, _I32, _VP]),
+    "ds_group_reduce": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _I64, _I32, _F32, _F32, _I32, _F32, _VP]),
+    "ds_average": (_I32, [_I32, _VP, _VP, _I64, _VP]),
+    "ds_blstm_set_grad_scale": (_I32, [_VP, _F32]),
     "ds_blstm_set_profile": (_I32, [_VP, _I32]),
     "ds_blstm_profile_read": (_I32, [_VP, _VP, _I32]),
     "ds_blstm_kernel_count": (_I32, [_VP]),

@@ -129,7 +129,7 @@ class Learner:
     simulated learners sharing a GPU)."""
 
     def __init__(self, obj: BlstmObjective, data: DeviceDataset, max_batch: int, device: int = 0,
-                 theta0: np.ndarray | None = None, momentum: float = 0.9):
+                 theta0: np.ndarray | None = None, momentum: float = 0.9, stream=None):
         import torch
 
         if data.frames != obj.frames or data.input_dim != obj.input_dim:
@@ -156,7 +156,7 @@ class Learner:
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.idx = torch.zeros(max_batch, dtype=torch.int64, device=dev)
         self.idx_host = torch.zeros(max_batch, dtype=torch.int64).pin_memory()
-        self.stream = torch.cuda.Stream(device=dev)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
         self.batch = 0
         if theta0 is not None:
             self.set_weights(theta0)
@@ -220,6 +220,10 @@ class Learner:
         _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self.idx.data_ptr(), B, self.grad.data_ptr(),
                                         self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
                    "ds_blstm_fwd_bwd")
+
+    def set_grad_scale(self, frames_total: float) -> None:
+        """CE gradient divisor for the next gradients (0 = this batch's frames)."""
+        _lib.check(_lib.load().ds_blstm_set_grad_scale(self.handle, float(frames_total)), "ds_blstm_set_grad_scale")
 
     def set_profile(self, on: bool) -> None:
         _lib.check(_lib.load().ds_blstm_set_profile(self.handle, 1 if on else 0), "ds_blstm_set_profile")

@@ -56,8 +56,10 @@ struct ds_blstm {
     float* loss;
     int* flag;
     int bwd;
+    float gscale;
     bool operator==(const Key& o) const {
-      return B == o.B && idx == o.idx && grad == o.grad && loss == o.loss && flag == o.flag && bwd == o.bwd;
+      return B == o.B && idx == o.idx && grad == o.grad && loss == o.loss && flag == o.flag && bwd == o.bwd &&
+             gscale == o.gscale;
     }
   };
   struct Entry {
@@ -70,6 +72,7 @@ struct ds_blstm {
   std::vector<cudaEvent_t> ev;
   std::vector<int> ev_kind;
   int launches = 0;  // kernel launches issued by the last step
+  float grad_frames = 0.f;  // CE gradient divisor override (0: B*T)
 };
 
 namespace {
@@ -242,7 +245,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.lse = h->lse;
     p.out = h->dlogits;
     p.ldo = C;
-    p.scale = 1.0f / (float)N;
+    p.scale = 1.0f / (h->grad_frames > 0.f ? h->grad_frames : (float)N);
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     nl += 1;
@@ -352,7 +355,7 @@ int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, i
   DS_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
   if (!use_graphs() || h->profile || cs != cudaStreamCaptureStatusNone)
     return issue_step(h, idx, B, grad, loss, flag, s);
-  ds_blstm::Key key{B, idx, grad, loss, flag, grad != nullptr};
+  ds_blstm::Key key{B, idx, grad, loss, flag, grad != nullptr, h->grad_frames};
   for (auto& e : h->graphs)
     if (e.key == key) {
       DS_CUDA_TRY(cudaGraphLaunch(e.exec, s));
@@ -486,7 +489,7 @@ int ds_adpsgd_mix(float* a, float* b, int64_t n, ds_stream_t stream) {
 
 int ds_group_reduce(int32_t world, int32_t rank, float* const* grads, float* const* thetas, float* const* vels,
                     ds_blstm* const* snap_owners, int64_t n, int32_t nchunks, float lr, float mu, int32_t mode,
-                    ds_stream_t stream) {
+                    float divisor, ds_stream_t stream) {
   if (!thetas || n < 1) return fail_arg("null argument");
   if (rank < 0 || rank >= world) return fail_arg("rank out of range");
   if (mode != 0 && mode != 1) return fail_arg("mode must be 0 (sgd) or 1 (average)");
@@ -499,8 +502,20 @@ int ds_group_reduce(int32_t world, int32_t rank, float* const* grads, float* con
         snaps[r] = snap_owners[r]->snap;
         any = true;
       }
-  return op_group_reduce(world, rank, grads, thetas, vels, any ? snaps : nullptr, n, nchunks, lr, mu, mode,
+  return op_group_reduce(world, rank, grads, thetas, vels, any ? snaps : nullptr, n, nchunks, lr, mu, mode, divisor,
                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_average(int32_t n, float* const* srcs, float* out, int64_t dim, ds_stream_t stream) {
+  if (!srcs || !out || dim < 1) return fail_arg("null argument");
+  return op_average(n, srcs, out, dim, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_blstm_set_grad_scale(ds_blstm* h, float frames_total) {
+  if (!h) return fail_arg("null handle");
+  if (frames_total < 0.f) return fail_arg("frames_total must be >= 0");
+  h->grad_frames = frames_total;
+  return DS_OK;
 }
 
 int ds_blstm_set_profile(ds_blstm* h, int32_t enable) {

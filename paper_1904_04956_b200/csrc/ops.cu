@@ -221,7 +221,7 @@ struct GroupPtrs {
 };
 
 __global__ void group_reduce_kernel(GroupPtrs p, int world, int rank, int64_t dim, int64_t chunk, int nchunks,
-                                    float lr, float mu, int mode) {
+                                    float lr, float mu, int mode, float divisor) {
   for (int j = rank; j < nchunks; j += world) {
     const int64_t lo = min(dim, (int64_t)j * chunk), hi = min(dim, (int64_t)(j + 1) * chunk);
     const int owner = j % world;
@@ -229,7 +229,7 @@ __global__ void group_reduce_kernel(GroupPtrs p, int world, int rank, int64_t di
       const float* const* src = mode == 0 ? p.g : p.theta;
       float s = src[owner][i];
       for (int k = 1; k < world; ++k) s = __fadd_rn(s, src[(owner + k) % world][i]);
-      const float mean = __fdiv_rn(s, (float)world);
+      const float mean = __fdiv_rn(s, divisor);
       if (mode == 0) {
         for (int r = 0; r < world; ++r) {
           float vv = __fadd_rn(__fmul_rn(p.v[r][i], mu), mean);
@@ -245,6 +245,16 @@ __global__ void group_reduce_kernel(GroupPtrs p, int world, int rank, int64_t di
         }
       }
     }
+  }
+}
+
+// consensus: out = (((x0 + x1) + x2) + ...) / n, members in id order
+// (np.mean(np.stack(...), axis=0) of engines/adpsgd.py:293-295, in fp32)
+__global__ void average_kernel(GroupPtrs p, int n, int64_t dim, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = p.theta[0][i];
+    for (int k = 1; k < n; ++k) s = __fadd_rn(s, p.theta[k][i]);
+    out[i] = __fdiv_rn(s, (float)n);
   }
 }
 
@@ -322,7 +332,7 @@ int op_mix(float* a, float* b, int64_t n, cudaStream_t s) {
 }
 
 int op_group_reduce(int world, int rank, float* const* g, float* const* theta, float* const* v, __nv_bfloat16* const* snap,
-                    int64_t dim, int nchunks, float lr, float mu, int mode, cudaStream_t s) {
+                    int64_t dim, int nchunks, float lr, float mu, int mode, float divisor, cudaStream_t s) {
   if (world < 1 || world > kMaxGroup) return fail_arg("group size out of range");
   if (nchunks < world) return fail_arg("chunk_count must be >= world");
   GroupPtrs p;
@@ -335,7 +345,18 @@ int op_group_reduce(int world, int rank, float* const* g, float* const* theta, f
   }
   if (mode == 0 && (!g || !v)) return fail_arg("SGD allreduce needs gradient and velocity buffers");
   const int64_t chunk = (dim + nchunks - 1) / nchunks;
-  group_reduce_kernel<<<ew_grid(chunk), kEW, 0, s>>>(p, world, rank, dim, chunk, nchunks, lr, mu, mode);
+  group_reduce_kernel<<<ew_grid(chunk), kEW, 0, s>>>(p, world, rank, dim, chunk, nchunks, lr, mu, mode,
+                                                     divisor > 0.f ? divisor : (float)world);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+int op_average(int n, float* const* srcs, float* out, int64_t dim, cudaStream_t s) {
+  if (n < 1 || n > kMaxGroup) return fail_arg("average: member count out of range");
+  GroupPtrs p;
+  memset(&p, 0, sizeof(p));
+  for (int k = 0; k < n; ++k) p.theta[k] = srcs[k];
+  average_kernel<<<ew_grid(dim), kEW, 0, s>>>(p, n, dim, out);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }

@@ -22,6 +22,8 @@ int op_snapshot_aux(const float* theta, const ModelLayout& L, const int64_t* d_w
                     __nv_bfloat16* wih0pad, float* bias_snap, cudaStream_t s);
 int op_mix(float* a, float* b, int64_t n, cudaStream_t s);
 int op_group_reduce(int world, int rank, float* const* g, float* const* theta, float* const* v,
-                    __nv_bfloat16* const* snap, int64_t dim, int nchunks, float lr, float mu, int mode, cudaStream_t s);
+                    __nv_bfloat16* const* snap, int64_t dim, int nchunks, float lr, float mu, int mode, float divisor,
+                    cudaStream_t s);
+int op_average(int n, float* const* srcs, float* out, int64_t dim, cudaStream_t s);
 
 }  // namespace ds

@@ -119,7 +119,7 @@ def test_group_reduce_canonical_order(world, chunks):
     V = [torch.from_numpy(v.copy()).cuda() for _ in range(world)]
     ptrs = ctypes_arr
     for r in range(world):
-        _lib.check(lib.ds_group_reduce(world, r, ptrs(G), ptrs(TH), ptrs(V), None, n, chunks, 0.1, 0.9, 0,
+        _lib.check(lib.ds_group_reduce(world, r, ptrs(G), ptrs(TH), ptrs(V), None, n, chunks, 0.1, 0.9, 0, 0.0,
                                        _lib.stream_ptr()))
     torch.cuda.synchronize()
     size = -(-n // chunks)
