@@ -75,6 +75,12 @@ class GpuBackend:
             L._gscale = frames_total
         L.gradient(np.asarray(batch))
 
+    def zero_grad(self, L: Learner) -> None:
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            L.grad.zero_()
+
     def sgd_step(self, L: Learner, lr: float) -> None:
         L.sgd_step(lr)
 

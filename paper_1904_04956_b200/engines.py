@@ -330,9 +330,10 @@ class _Unit:
         # gradient of the union batch
         total = _frames(dataset, batch)
         for m, part in zip(self.members, np.array_split(np.asarray(batch), len(self.members))):
-            if len(part) == 0:
-                raise ValueError("H-ADPSGD group larger than the drawn batch")
-            self.be.gradient(m, part, frames_total=float(total))
+            if len(part) == 0:  # short final batch: this member contributes nothing
+                self.be.zero_grad(m)
+            else:
+                self.be.gradient(m, part, frames_total=float(total))
 
     def update(self, lr):
         if len(self.members) == 1:

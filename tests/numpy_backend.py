@@ -38,9 +38,14 @@ class NumpyBackend:
 
     def gradient(self, L, batch, frames_total: float = 0.0):
         g = self.grad_fn(self.obj, L.snap, batch, self.data)
-        if frames_total:
-            g = g * (len(batch) / frames_total)
+        if frames_total:  # member of an H-ADPSGD group: frame-weighted share of the union batch
+            x = self.data.inputs
+            per = x.shape[1] if x.ndim == 3 else 1
+            g = g * (len(batch) * per / frames_total)
         L.g = g
+
+    def zero_grad(self, L):
+        L.g = np.zeros(self.param_dim)
 
     def _step(self, L, g, lr):
         L.v *= L.mu
