@@ -177,9 +177,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     L = Learner(obj, data, max_batch=B, device=local_rank, theta0=initial_weights(obj, 0))
     sched = baseline_schedule(0.1)
     # the run_single draw order; rank r of an SSGD group takes every world-th batch (static_partition)
-    pool = epoch_minibatches(train, B, seed=0, epoch=1)
-    pool = [b for b in pool if len(b) == B]
-    mine = pool[rank::world] if world > 1 else pool
+    from paper_1904_04956_b200.distributed import rank_batches
+
+    mine = [b for b in rank_batches(train, B, 0, 1, rank, world) if len(b) == B]
     q = len(mine)
     idx_dev = torch.from_numpy(np.stack(mine)).to(torch.device("cuda", local_rank))
     stream = L.stream

@@ -151,50 +151,102 @@ __device__ __forceinline__ void trace_mark(uint64_t* trace, int T, int s, int k)
 }
 
 // ============================================================================
-__global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_constant__ LstmParams P) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem m = carve(smem_raw);
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const int ublk = blockIdx.x % kUblk;
-  const int btile = (blockIdx.x / kUblk) % P.n_btile;
-  const int dir = blockIdx.x / (kUblk * P.n_btile);
-  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kUblk;  // step counters of the group
-  const int T = P.T, B = P.B;
-  const int brow0 = P.b0 + btile * 128;  // first batch row of this tile
+// Forward: CTA = (dir, batch tile, unit block of 32 units = 128 gate rows),
+// clusters of 8 unit blocks.  W_hh slice 128 x 512 bf16 (128 KB) resident.
+// The h_prev tile (128 rows x 512) is shared by all CTAs of a group, so each
+// of its eight 64-unit chunks is fetched from L2 ONCE per cluster: cluster
+// rank k waits for the flags of the two unit blocks that produce chunk k and
+// multicasts it into all eight CTAs; every CTA's MMA completion is multicast
+// back to the issuers' stage-empty barriers.  Warp 3 publishes the step flag
+// after the epilogue warps stored h_t; the BPTT state (gates, c) is written
+// after that hand-off so its stores are not drained on the critical path.
+namespace fwd {
+template <int U>
+struct Cfg {
+  static constexpr int kU = U;                        // units per CTA (16 or 32)
+  static constexpr int kR = 4 * U;                    // gate rows per CTA
+  static constexpr int kUb = kH / U;                  // unit blocks per direction
+  // cluster size: 8-CTA clusters cannot all be co-resident at 128 CTAs (only
+  // ~15 fit), so the 128-CTA U=16 grid uses clusters of 4
+  static constexpr int kCl = U == 32 ? 8 : 4;
+  static constexpr int kWB = kR * kH * 2;             // resident W slice bytes
+  static constexpr int kStagesF = U == 32 ? 6 : 8;    // U=16: the whole h tile in flight
+  static constexpr size_t kSmem = 1024 + kWB + kStagesF * kTileA + 256;
+  static constexpr int kUT = U / 2;                   // units per epilogue thread
+};
+constexpr int kPubBar = 2;  // named barriers 2/3: epilogue <-> publisher warp hand-offs
+}  // namespace fwd
 
-  setup(m, 128);
-  const uint32_t tmem = *m.tmem_slot;
+template <int U>
+__global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_constant__ LstmParams P) {
+  using C = fwd::Cfg<U>;
+  constexpr int kU = C::kU, kR = C::kR, kUb = C::kUb, kCl = C::kCl, kWB = C::kWB, kStagesF = C::kStagesF;
+  constexpr int kUT = C::kUT;
+  using fwd::kPubBar;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = sm;
+  uint8_t* sA = sW + kWB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sA + kStagesF * kTileA);
+  uint64_t* empty = full + kStagesF;
+  uint64_t* wbar = empty + kStagesF;
+  uint64_t* tfull = wbar + 1;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int ublk = blockIdx.x % kUb;
+  const int btile = (blockIdx.x / kUb) % P.n_btile;
+  const int dir = blockIdx.x / (kUb * P.n_btile);
+  const int crank = (int)cluster_ctarank();  // == ublk % kCl
+  const uint16_t all = (uint16_t)((1u << kCl) - 1);
+  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * 32;
+  const int T = P.T, B = P.B;
+  const int brow0 = P.b0 + btile * 128;
+
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < kStagesF; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kCl);  // one multicast commit per cluster CTA
+    }
+    mbar_init(wbar, 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kEpiThreads);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, kR);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch_desc(&P.tmA);
       tma_prefetch_desc(&P.tmW);
-      // resident W_hh slice: rows dir*2048 + ublk*128 .. +128, K = 512
-      mbar_arrive_expect_tx(m.wbar, kWBytes);
+      mbar_arrive_expect_tx(wbar, kWB);
       for (int kb = 0; kb < kH / 64; ++kb)
-        tma_load_2d(m.w + kb * kRows * 128, &P.tmW, m.wbar, kb * 64, dir * 4 * kH + ublk * kRows);
+        tma_load_2d(sW + kb * kR * 128, &P.tmW, wbar, kb * 64, dir * 4 * kH + ublk * kR);
       int stage = 0;
       uint32_t phase = 0;
       for (int s = 0; s < T; ++s) {
         const int t = dir == 0 ? s : T - 1 - s;
-        const int tprev = dir == 0 ? t - 1 : t + 1;  // -1 / T hit the zero pads
+        const int tprev = dir == 0 ? t - 1 : t + 1;
         const int arow = (tprev + 1) * B + brow0;
         for (int kb = 0; kb < kH / 64; ++kb) {
-          mbar_wait(&m.empty[stage], phase ^ 1);
-          if (s > 0 && (P.variant & 8)) {  // barrier mode: all 16 producers of step s-1
-            if (kb == 0) {
-              for (int u = 0; u < kUblk; ++u) wait_flag(flags + u, (uint32_t)s);
-              acquire_for_tma(flags + kUblk - 1, P.variant);
+          mbar_wait(&empty[stage], phase ^ 1);  // every cluster CTA freed this stage
+          mbar_arrive_expect_tx(&full[stage], kTileA);
+          if (kb % kCl == crank) {
+            if (s > 0) {  // chunk kb = units kb*64 .. +64 <- unit blocks kb*64/kU ..
+              constexpr int kPer = 64 / kU;
+#pragma unroll
+              for (int u = 0; u < kPer; ++u) wait_flag(flags + kPer * kb + u, (uint32_t)s);
+              acquire_for_tma(flags + kPer * kb + kPer - 1, P.variant);
             }
-          } else if (s > 0) {  // chunk kb = units kb*64.. produced by unit blocks 2kb, 2kb+1
-            wait_flag(flags + 2 * kb, (uint32_t)s);
-            wait_flag(flags + 2 * kb + 1, (uint32_t)s);
-            acquire_for_tma(flags + 2 * kb + 1, P.variant);
+            tma_load_2d_mc(sA + stage * kTileA, &P.tmA, &full[stage], dir * kH + kb * 64, arow, all);
           }
           if (kb == 0) trace_mark(P.trace, T, s, 0);
-          mbar_arrive_expect_tx(&m.full[stage], kTileA);
-          tma_load_2d(m.a + stage * kTileA, &P.tmA, &m.full[stage], dir * kH + kb * 64, arow);
-          if (++stage == kStages) {
+          if (++stage == kStagesF) {
             stage = 0;
             phase ^= 1;
           }
@@ -203,123 +255,127 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
       }
     }
   } else if (warp == 1) {
-    mbar_wait(m.wbar, 0);
-    const uint32_t idesc = idesc_bf16_f32(128, kRows, 0, 0);
-    const uint32_t wbase = smem_u32(m.w);
+    mbar_wait(wbar, 0);
+    const uint32_t idesc = idesc_bf16_f32(128, kR, 0, 0);
+    const uint32_t wbase = smem_u32(sW);
     int stage = 0;
     uint32_t phase = 0;
     for (int s = 0; s < T; ++s) {
-      mbar_wait(m.tempty, (s & 1) ^ 1);
+      mbar_wait(tempty, (s & 1) ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < kH / 64; ++kb) {
-        mbar_wait(&m.full[stage], phase);
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t abase = smem_u32(m.a + stage * kTileA);
+          const uint32_t abase = smem_u32(sA + stage * kTileA);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             uint64_t ad = smem_desc_sw128(abase + k * 32, 16, 1024);
-            uint64_t bd = smem_desc_sw128(wbase + kb * kRows * 128 + k * 32, 16, 1024);
+            uint64_t bd = smem_desc_sw128(wbase + kb * kR * 128 + k * 32, 16, 1024);
             mma_bf16_ss(tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          mma_commit(&m.empty[stage]);
-          if (kb == kH / 64 - 1) mma_commit(m.tfull);
+          mma_commit_mc(&empty[stage], all);
+          if (kb == kH / 64 - 1) mma_commit(tfull);
         }
         __syncwarp();
-        if (++stage == kStages) {
+        if (++stage == kStagesF) {
           stage = 0;
           phase ^= 1;
         }
       }
     }
+  } else if (warp == 3) {
+    // publisher: h_t of all 256 epilogue threads stored -> release the flag
+    for (int s = 0; s < T; ++s) {
+      named_bar_sync(kPubBar, kEpiThreads + 32);
+      if (lane == 0) {
+        trace_mark(P.trace, T, s, 5);
+        st_release_gpu(flags + ublk, (uint32_t)(s + 1));
+        trace_mark(P.trace, T, s, 4);
+      }
+      __syncwarp();
+      // let the epilogue write the BPTT state only once the release is out
+      asm volatile("bar.arrive %0, %1;" ::"n"(kPubBar + 1), "n"(kEpiThreads + 32) : "memory");
+    }
   } else if (warp >= kEpiWarp0) {
     const uint32_t e = warp - kEpiWarp0;
-    const uint32_t q = e & 3;   // TMEM lane quadrant (== warp % 4)
-    const uint32_t hf = e >> 2; // column half: gate rows hf*64 .. +64 = units hf*16 .. +16
+    const uint32_t q = e & 3;
+    const uint32_t hf = e >> 2;  // gate rows hf*4kUT .. = units hf*kUT .. +kUT of the block
     const int r = q * 32 + lane;
     const int b = brow0 + r;
     const bool ok = (r + btile * 128 < P.nb) && b < B;
-    const uint32_t tcol = tmem + ((q * 32) << 16) + hf * 64;
-    const int col_g = dir * 4 * kH + ublk * kRows + hf * 64;  // first gate column
-    const int col_u = dir * kH + ublk * kUnits + hf * 16;     // first unit column
-    float creg[16];
+    const uint32_t tcol = tmem + ((q * 32) << 16) + hf * 4 * kUT;
+    const int col_g = dir * 4 * kH + ublk * kR + hf * 4 * kUT;
+    const int col_u = dir * kH + ublk * kU + hf * kUT;
+    float creg[kUT];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) creg[u] = 0.f;
+    for (int u = 0; u < kUT; ++u) creg[u] = 0.f;
     for (int s = 0; s < T; ++s) {
       const int t = dir == 0 ? s : T - 1 - s;
       const size_t n = (size_t)t * B + b;
       __nv_bfloat16* grow = P.gates + n * (8 * kH) + col_g;
-      uint4 gpre[8];
+      uint4 gpre[kUT / 2];
       if (ok) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) gpre[j] = reinterpret_cast<const uint4*>(grow)[j];
+        for (int j = 0; j < kUT / 2; ++j) gpre[j] = reinterpret_cast<const uint4*>(grow)[j];
       }
-      mbar_wait(m.tfull, s & 1);
+      mbar_wait(tfull, s & 1);
       tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
-      float v[64];
-      tmem_ld32(tcol, v);
-      tmem_ld32(tcol + 32, v + 32);
+      float v[4 * kUT];
+#pragma unroll
+      for (int c = 0; c < 4 * kUT; c += 32) tmem_ld32(tcol + c, v + c);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(m.tempty);
-      float hv[16], cv[16];
-      uint4 actp[8];
-      if (ok) {
+      mbar_arrive(tempty);
+      float hv[kUT], cv[kUT];
+      uint4 actp[kUT / 2];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float gi[8];
-          bf16x8_to_f32(gpre[j], gi);
-          float act[8];
+      for (int j = 0; j < kUT / 2; ++j) {
+        float gi[8];
+        bf16x8_to_f32(gpre[j], gi);
+        float act[8];
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int u = 2 * j + h2;
-            float ig, fg, gg, og;
-            if (P.variant & 16) {
-              ig = v[4 * u + 0]; fg = v[4 * u + 1]; gg = v[4 * u + 2]; og = v[4 * u + 3];
-            } else {
-              ig = sigmoid_fast(v[4 * u + 0] + gi[4 * h2 + 0]);
-              fg = sigmoid_fast(v[4 * u + 1] + gi[4 * h2 + 1]);
-              gg = tanh_fast(v[4 * u + 2] + gi[4 * h2 + 2]);
-              og = sigmoid_fast(v[4 * u + 3] + gi[4 * h2 + 3]);
-            }
-            const float cn = fmaf(fg, creg[u], ig * gg);
-            creg[u] = cn;
-            cv[u] = cn;
-            hv[u] = og * tanh_fast(cn);
-            act[4 * h2 + 0] = ig;
-            act[4 * h2 + 1] = fg;
-            act[4 * h2 + 2] = gg;
-            act[4 * h2 + 3] = og;
-          }
-          actp[j] = f32_to_bf16x8(act);
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int u = 2 * j + h2;
+          const float ig = sigmoid_fast(v[4 * u + 0] + gi[4 * h2 + 0]);
+          const float fg = sigmoid_fast(v[4 * u + 1] + gi[4 * h2 + 1]);
+          const float gg = tanh_fast(v[4 * u + 2] + gi[4 * h2 + 2]);
+          const float og = sigmoid_fast(v[4 * u + 3] + gi[4 * h2 + 3]);
+          const float cn = fmaf(fg, creg[u], ig * gg);
+          creg[u] = cn;
+          cv[u] = cn;
+          hv[u] = og * tanh_fast(cn);
+          act[4 * h2 + 0] = ig;
+          act[4 * h2 + 1] = fg;
+          act[4 * h2 + 2] = gg;
+          act[4 * h2 + 3] = og;
         }
-        // h_t first: it is the only value the next step of the group reads
+        actp[j] = f32_to_bf16x8(act);
+      }
+      if (ok) {
         uint4* h4 = reinterpret_cast<uint4*>(P.y + ((size_t)(t + 1) * B + b) * (2 * kH) + col_u);
-        h4[0] = f32_to_bf16x8(hv);
-        h4[1] = f32_to_bf16x8(hv + 8);
+#pragma unroll
+        for (int j = 0; j < kUT / 8; ++j) h4[j] = f32_to_bf16x8(hv + 8 * j);
       }
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
-      if (P.trace && lane == 0)
-        atomicMax(reinterpret_cast<unsigned long long*>(P.trace + ((size_t)blockIdx.x * T + s) * kTraceSlots + 5),
-                  (unsigned long long)globaltimer());
-      publish(flags + ublk, (uint32_t)(s + 1), P.variant);
-      // saved state for BPTT (consumed by a later launch): off the critical path
-      if (ok && !(P.variant & 32)) {
+      asm volatile("bar.arrive %0, %1;" ::"n"(kPubBar), "n"(kEpiThreads + 32) : "memory");
+      named_bar_sync(kPubBar + 1, kEpiThreads + 32);
+      if (ok) {  // BPTT state, after the flag release (not drained by it)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) reinterpret_cast<uint4*>(grow)[j] = actp[j];
+        for (int j = 0; j < kUT / 2; ++j) reinterpret_cast<uint4*>(grow)[j] = actp[j];
         float4* c4 = reinterpret_cast<float4*>(P.cstate + n * (2 * kH) + col_u);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) c4[j] = make_float4(cv[4 * j], cv[4 * j + 1], cv[4 * j + 2], cv[4 * j + 3]);
+        for (int j = 0; j < kUT / 4; ++j) c4[j] = make_float4(cv[4 * j], cv[4 * j + 1], cv[4 * j + 2], cv[4 * j + 3]);
       }
-      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 4);
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // no CTA exits while peers may still multicast into it
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 128);
+  if (warp == 2) tmem_dealloc(tmem, kR);
 }
 
 // ============================================================================
@@ -331,7 +387,12 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
 //   finalises units ug*64 + ks*16 .. +16, runs their cell backward and writes
 //   exactly one 64-gate-row chunk (chunk id ug*4 + ks) of dG_t.
 namespace bwd {
-constexpr int kKS = 4;                       // cluster size (K splits)
+constexpr int kKS = 4;                       // K splits (DSMEM exchange group)
+// Multicasting each A slice to the two unit groups of an 8-CTA cluster halves
+// the L2 reads but measured slower (one batch-tile group ran ~3x behind), so
+// the kernel runs with 4-CTA clusters and per-CTA loads.
+constexpr bool kMulticastB = false;
+constexpr int kClB = kMulticastB ? 8 : 4;
 constexpr int kGU = 64;                      // units per cluster
 constexpr int kFU = kGU / kKS;               // 16 units finalised per CTA
 constexpr int kKSlice = 4 * kH / kKS;        // 512 gate rows per CTA
@@ -360,7 +421,11 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int ks = (int)cluster_ctarank();
+  const int crank = (int)cluster_ctarank();
+  const int ks = crank % kKS;
+  const int upair = crank / kKS;              // which unit group of the cluster
+  const uint32_t rbase = (uint32_t)(upair * kKS);  // cluster rank of (this ug, ks = 0)
+  const uint16_t pair_mask = (uint16_t)((1u << ks) | (1u << (kKS + ks)));
   const int ug = (blockIdx.x / kKS) % (kH / kGU);
   const int btile = (blockIdx.x / (kKS * (kH / kGU))) % P.n_btile;
   const int dir = blockIdx.x / (kKS * (kH / kGU) * P.n_btile);
@@ -373,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < kStagesB; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], kMulticastB ? 2 : 1);  // both CTAs of a multicast pair free the stage
     }
     mbar_init(wbar, 1);
     mbar_init(tfull, 1);
@@ -402,12 +467,21 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         const int arow = tprev * B + brow0;
         for (int j = 0; j < kChunks; ++j) {
           const int chunk = ks * kChunks + j;
-          mbar_wait(&empty[stage], phase ^ 1);
-          wait_flag(flags + chunk, (uint32_t)s);
-          acquire_for_tma(flags + chunk, P.variant);
-          if (j == 0) trace_mark(P.trace, T, s, 0);
+          mbar_wait(&empty[stage], phase ^ 1);  // both CTAs of the pair freed it
           mbar_arrive_expect_tx(&full[stage], kTileA);
-          tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
+          if (kMulticastB) {  // the pair alternates chunks; multicast to both
+            if ((j & 1) == upair) {
+              wait_flag(flags + chunk, (uint32_t)s);
+              acquire_for_tma(flags + chunk, P.variant);
+              tma_load_2d_mc(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow,
+                             pair_mask);
+            }
+          } else {
+            wait_flag(flags + chunk, (uint32_t)s);
+            acquire_for_tma(flags + chunk, P.variant);
+            tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
+          }
+          if (j == 0) trace_mark(P.trace, T, s, 0);
           if (++stage == kStagesB) {
             stage = 0;
             phase ^= 1;
@@ -436,7 +510,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
             uint64_t bd = smem_desc_sw128(wbase + j * kGU * 128 + k * 32, 16, 1024);
             mma_bf16_ss(tmem, ad, bd, idesc, (j | k) != 0);
           }
-          mma_commit(&empty[stage]);
+          if (kMulticastB)
+            mma_commit_mc(&empty[stage], pair_mask);
+          else
+            mma_commit(&empty[stage]);
           if (j == kChunks - 1) mma_commit(tfull);
         }
         __syncwarp();
@@ -509,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         for (int f2 = 0; f2 < 2; ++f2) {
           const int f = 2 * hf + f2;
           const uint32_t local = recv_base + (uint32_t)((ks * 128 + r) * kFU * 4);
-          const uint32_t dst = mapa_shared(local, (uint32_t)f);
+          const uint32_t dst = mapa_shared(local, rbase + (uint32_t)f);
 #pragma unroll
           for (int i = 0; i < kFU; i += 4)
             st_cluster_v4(dst + i * 4, v[f2 * kFU + i], v[f2 * kFU + i + 1], v[f2 * kFU + i + 2],
@@ -519,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         if (lane == 0) {
 #pragma unroll
           for (int f2 = 0; f2 < 2; ++f2)
-            mbar_arrive_remote_release(mapa_shared(smem_u32(rfull), (uint32_t)(2 * hf + f2)));
+            mbar_arrive_remote_release(mapa_shared(smem_u32(rfull), rbase + (uint32_t)(2 * hf + f2)));
         }
         mbar_wait_acq_cluster(rfull, (s - 1) & 1);
         if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 5);
@@ -604,14 +681,25 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
 
 // batch tiles per launch: forward 32 CTAs / tile; backward 64 CTAs / tile in
 // clusters of 4 (cluster placement leaves some SMs unusable: keep <= 128)
-int lstm_max_tiles() { return num_sms() / (2 * kUblk); }
+static int fwd_units() {
+  static int u = 0;
+  if (!u) {
+    const char* e = getenv("DS_FWD_UNITS");
+    u = (e && atoi(e) == 32) ? 32 : 16;  // default U=16 (measured 6.8 vs 8.0 us per step)
+  }
+  return u;
+}
+int lstm_max_tiles() { return num_sms() / (2 * (kH / fwd_units())); }
 static int lstm_bwd_max_tiles() { return (num_sms() >= 132 ? 128 : num_sms()) / 64; }
 int lstm_counter_words(int B) { return 2 * 32 * ((B + 127) / 128); }
 
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    DS_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    DS_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)fwd::Cfg<32>::kSmem));
+    DS_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)fwd::Cfg<16>::kSmem));
     DS_CUDA_TRY(
         cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmem));
     attr_set = true;
@@ -626,7 +714,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     rc = make_tmap_2d(&P.tmA, a.y_full, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2 * kH, (uint64_t)(T + 2) * B,
                       2 * kH * 2, 64, 128);
     if (rc) return rc;
-    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, 64, kRows);
+    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, 64, 4 * fwd_units());
     if (rc) return rc;
   } else {
     rc = make_tmap_2d(&P.tmA, a.dg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 8 * kH, (uint64_t)T * B, 8 * kH * 2, 64, 128);
@@ -655,9 +743,13 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.counters = a.counters + (b0 / 128) * 2 * 32;
     DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * 32 * P.n_btile, stream));
     if (fwd)
-      rc = launch_coop((const void*)lstm_fwd_kernel, 2 * kUblk * P.n_btile, P, stream, kSmemBytes, 1);
+      rc = fwd_units() == 16
+               ? launch_coop((const void*)lstm_fwd_kernel<16>, 2 * fwd::Cfg<16>::kUb * P.n_btile, P, stream,
+                             fwd::Cfg<16>::kSmem, fwd::Cfg<16>::kCl)
+               : launch_coop((const void*)lstm_fwd_kernel<32>, 2 * fwd::Cfg<32>::kUb * P.n_btile, P, stream,
+                             fwd::Cfg<32>::kSmem, fwd::Cfg<32>::kCl);
     else
-      rc = launch_coop((const void*)lstm_bwd_kernel, 64 * P.n_btile, P, stream, bwd::kSmem, bwd::kKS);
+      rc = launch_coop((const void*)lstm_bwd_kernel, 64 * P.n_btile, P, stream, bwd::kSmem, bwd::kClB);
     if (rc) return rc;
     P.trace = nullptr;  // trace only the first chunk
   }

@@ -1,6 +1,7 @@
 """Time one bidirectional layer's recurrent forward/backward kernels at the
 paper shape and print per-step phase marks from the in-kernel globaltimer
 trace (producer ready / loads issued / MMA done / step published)."""
+import os
 import sys
 
 import numpy as np
@@ -25,8 +26,8 @@ counters = torch.zeros(4096, device=dev, dtype=torch.int32)
 dY = torch.randn(N, 2 * H, device=dev).bfloat16()
 dg = torch.zeros(N, 8 * H, device=dev, dtype=torch.bfloat16)
 ntile = (B + 127) // 128
-grid = 32 * ntile
-trace = torch.zeros(2 * grid * T * 6 + T * 32 * 2, device=dev, dtype=torch.int64)
+grid = 64 * ntile
+trace = torch.zeros(grid * T * 6 + T * 32 * 2, device=dev, dtype=torch.int64)
 s = _lib.stream_ptr()
 
 
@@ -57,7 +58,7 @@ for name, fn in (("fwd", fwd), ("bwd", bwd)):
     fn(trace.data_ptr())
     torch.cuda.synchronize()
     full = trace.cpu().numpy().astype(np.float64)
-    g = grid if name == "fwd" else 2 * grid
+    g = (grid // 2 if os.environ.get("DS_FWD_UNITS", "32") != "16" else grid) if name == "fwd" else grid
     tr = full[:g * T * 6].reshape(g, T, 6)
     t2 = full[g * T * 6:g * T * 6 + T * 64].reshape(T, 32, 2)
     base = tr[tr > 0].min()
@@ -69,6 +70,9 @@ for name, fn in (("fwd", fwd), ("bwd", bwd)):
         print(f"  step {st:2d} med ready {med[0]:7.2f} issued {med[1]:7.2f} mma {med[2]:7.2f} stored {med[3]:7.2f}"
               f" lastwarp {med[5]:7.2f} pub {med[4]:7.2f} | max pub {mx[4]:7.2f}")
     pub = np.nanmax(tr[:, :, 4], axis=0)
+    late = np.argsort(-np.nan_to_num(tr[:, 8, 4]))[:6]
+    print("  slowest CTAs at step 8:", [(int(c), round(float(tr[c, 8, 4]), 1)) for c in late],
+          "first-step ready of those:", [round(float(np.nanmin(tr[c, :, 0])), 1) for c in late])
     if False:
         b2 = np.where(t2 > 0, t2 - base, np.nan) / 1e3
         for st in (5, 6):
