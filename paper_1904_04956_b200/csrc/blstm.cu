@@ -47,6 +47,7 @@ struct ds_blstm {
   __nv_bfloat16* dy = nullptr;
   __nv_bfloat16* dg = nullptr;
   float* colpart = nullptr;
+  float* biaspart = nullptr;  // fused bias-gradient partials (CE grad epilogue / BPTT kernel)
   uint32_t* counters = nullptr;
   // graph cache
   struct Key {
@@ -117,6 +118,12 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   h->dg = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
   int64_t cp = op_colsum_scratch(L.classes > kGates2 ? L.classes : kGates2);
   h->colpart = a.take<float>(base, cp);
+  {
+    const int64_t tiles_m = (N + kGemmBM - 1) / kGemmBM;
+    const int64_t a1 = tiles_m * 4 * L.classes;
+    const int64_t a2 = (int64_t)((h->Bmax + 127) / 128) * 4 * kGates2;
+    h->biaspart = a.take<float>(base, a1 > a2 ? a1 : a2);
+  }
   h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64);
   *total = a.off + 256;
   return DS_OK;
@@ -246,9 +253,12 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.out = h->dlogits;
     p.ldo = C;
     p.scale = 1.0f / (h->grad_frames > 0.f ? h->grad_frames : (float)N);
+    p.colpart = h->biaspart;
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
-    nl += 1;
+    MARK(PH_OTHER);
+    TRY(op_rowsum(h->biaspart, p.tiles_m * 4, C, grad + L.off_bo, s));
+    nl += 2;
   }
   {
     GemmBatch gb;
@@ -265,9 +275,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p1.out = h->dz;
     p1.ldo = bott;
     TRY(gemm_launch(&gb, s));
-    MARK(PH_OTHER);
-    TRY(op_colsum(h->dlogits, N, C, C, h->colpart, grad + L.off_bo, s));
-    nl += 3;
+    nl += 1;
   }
   {
     GemmBatch gb;
@@ -291,7 +299,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   }
   for (int l = Lh - 1; l >= 0; --l) {
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->whhT + (size_t)l * kGates2 * kHidden, h->dy,
-                     h->dg, h->counters};
+                     h->dg, h->counters, nullptr, h->biaspart};
     MARK(PH_LSTM_BWD);
     TRY(lstm_backward(la, s));
     nl += 1 + (B - 1) / (128 * lstm_max_tiles());
@@ -325,11 +333,11 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       p3.ldo = kLayerOut;
       gb.nprob = 4;
     }
+    MARK(PH_OTHER);
+    TRY(op_rowsum(h->biaspart, ((B + 127) / 128) * 4, kGates2, grad + L.off_b[l], s));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
-    MARK(PH_OTHER);
-    TRY(op_colsum(h->dg, N, kGates2, kGates2, h->colpart, grad + L.off_b[l], s));
-    nl += 3;
+    nl += 2;
   }
   MARK(PH_END);
 #undef MARK

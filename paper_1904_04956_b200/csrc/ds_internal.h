@@ -76,6 +76,7 @@ struct GemmProblem {
   float2* stats;          // [tiles_n][stats_ld]
   float* tgt;             // [m_valid]
   int stats_ld;
+  float* colpart;         // EPI_CE_GRAD: optional [tiles_m*4][n_valid] column-sum partials
 };
 
 struct GemmBatch {

@@ -234,6 +234,25 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N, ui
 }
 
 // ----------------------------------------------------------------------------
+// Column sums of a warp's 32 x 32 block (lane = row, v[j] = column j): a
+// butterfly reduce-scatter (16+8+4+2+1 = 31 shuffles); on return lane L's
+// v[0] holds the sum of column L over the 32 lanes (fixed order: deterministic).
+DS_DEV float warp_colsum32(float* v) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const float send = up ? v[j] : v[j + off];
+      const float keep = up ? v[j + off] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+// ----------------------------------------------------------------------------
 // math helpers
 // One MUFU op; max relative error ~2^-11 (PTX ISA tanh.approx.f32).
 DS_DEV float tanh_fast(float x) {

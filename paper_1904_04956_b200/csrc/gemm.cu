@@ -266,10 +266,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               if (lbl == nb + i) v[i] -= 1.f;
           }
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= P.scale;
+          for (int i = 0; i < 32; ++i) v[i] = row_ok ? v[i] * P.scale : 0.f;
           if (row_ok) {
             store_bf16x16(orow + nb, v);
             store_bf16x16(orow + nb + 16, v + 16);
+          }
+          if (P.colpart) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
+            const float cs = warp_colsum32(v);
+            P.colpart[(size_t)(tc.tm * 4 + q) * P.n_valid + nb + lane] = cs;
           }
         }
       } else if (P.epi == EPI_BF16) {

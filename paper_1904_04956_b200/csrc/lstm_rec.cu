@@ -537,9 +537,11 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
     const int col_g = dir * 4 * kH + unit0 * 4;
     const int col_u = dir * kH + unit0;
     const uint32_t recv_base = smem_u32(recv);
-    float dcc[8];
+    float dcc[8], dbacc[32];
 #pragma unroll
     for (int u = 0; u < 8; ++u) dcc[u] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) dbacc[i] = 0.f;
     for (int s = 0; s < T; ++s) {
       const int t = dir == 0 ? T - 1 - s : s;
       const int tc = dir == 0 ? t - 1 : t + 1;
@@ -635,11 +637,17 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
             dcc[u] = dct * fg;
           }
           dgrow[j] = f32_to_bf16x8(dgv);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) dbacc[8 * j + i] += dgv[i];
         }
       }
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
       publish(flags + my_chunk, (uint32_t)(s + 1), P.variant);
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 4);
+    }
+    if (P.dbpart) {  // fused bias gradient: sum over this warp's 32 batch rows and all steps
+      const float cs = warp_colsum32(dbacc);
+      P.dbpart[((size_t)(P.b0 / 128 + btile) * 4 + q) * (8 * kH) + col_g + lane] = cs;
     }
   }
 
@@ -728,6 +736,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   P.dy = a.dy;
   P.dg = a.dg;
   P.trace = a.trace;
+  P.dbpart = a.dbpart;
   {
     const char* v = getenv("DS_LSTM_VARIANT");
     P.variant = v ? atoi(v) : 7;  // 7: acquire by ld.acquire, no writer-side fences

@@ -17,6 +17,7 @@ struct LstmParams {
   __nv_bfloat16* dg;
   uint32_t* counters;
   uint64_t* trace;  // optional per-(CTA, step) globaltimer marks (debug)
+  float* dbpart;    // backward: optional [(B/128)*4][4096] bias-gradient partials
   int B, T, b0, nb, n_btile;
   int variant;  // debug: bit0 skip writer proxy fence, bit1 skip release fence
 };
@@ -31,6 +32,7 @@ struct LstmLayerArgs {
   __nv_bfloat16* dg;        // backward: [T*B, 4096]
   uint32_t* counters;       // >= lstm_counter_words(B)
   uint64_t* trace = nullptr;
+  float* dbpart = nullptr;  // backward: per-(batch tile, lane quadrant) column sums of dG
 };
 
 int lstm_max_tiles();

@@ -61,6 +61,15 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int ncols, f
   out[col] = s;
 }
 
+// out[c] = sum_r part[r][c], rows in order (deterministic)
+__global__ void rowsum_kernel(const float* __restrict__ part, int nrows, int ncols, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  float s = 0.f;
+  for (int r = 0; r < nrows; ++r) s += part[(int64_t)r * ncols + c];
+  out[c] = s;
+}
+
 // --------------------------------------------------------------------------
 // soft-max / CE combine: lse[m] = logsumexp over column-tile (max, sumexp)
 // partials; per-block loss partials, then one ordered sum (deterministic).
@@ -282,6 +291,12 @@ int op_colsum(const __nv_bfloat16* x, int64_t rows, int ncols, int64_t ld, float
   return DS_OK;
 }
 int64_t op_colsum_scratch(int ncols) { return (int64_t)kColSplit * ncols; }
+
+int op_rowsum(const float* part, int nrows, int ncols, float* out, cudaStream_t s) {
+  rowsum_kernel<<<(ncols + 255) / 256, 256, 0, s>>>(part, nrows, ncols, out);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
 
 int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt, int M, float* lse, float* scratch,
                   float* loss_sum, int* flag, cudaStream_t s) {
