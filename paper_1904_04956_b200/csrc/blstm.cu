@@ -48,6 +48,7 @@ struct ds_blstm {
   __nv_bfloat16* dg = nullptr;
   float* colpart = nullptr;
   float* biaspart = nullptr;  // fused bias-gradient partials (CE grad epilogue / BPTT kernel)
+  float* splitk = nullptr;    // split-K fp32 partials of dZ
   uint32_t* counters = nullptr;
   // graph cache
   struct Key {
@@ -77,6 +78,14 @@ struct ds_blstm {
 };
 
 namespace {
+
+// dZ = dlogits . W_o has K = classes (500 k-blocks at 32000): split it so its
+// tiles match the length of the concurrent dW_o tiles (K = frames).
+constexpr int kDzSplit = 5;
+int dz_split(int classes) {
+  const int nkb = (classes + kGemmBK - 1) / kGemmBK;
+  return (nkb % kDzSplit == 0 && nkb >= 4 * kDzSplit) ? kDzSplit : 1;
+}
 
 struct Arena {
   size_t off = 0;
@@ -124,6 +133,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
     const int64_t a2 = (int64_t)((h->Bmax + 127) / 128) * 4 * kGates2;
     h->biaspart = a.take<float>(base, a1 > a2 ? a1 : a2);
   }
+  h->splitk = a.take<float>(base, (size_t)kDzSplit * N * L.bottleneck);
   h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64);
   *total = a.off + 256;
   return DS_OK;
@@ -269,13 +279,27 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p0.epi = EPI_F32;
     p0.out = grad + L.off_wo;
     p0.ldo = bott;
-    GemmProblem& p1 = gb.p[1];  // dZ = dlogits W_o
+    GemmProblem& p1 = gb.p[1];  // dZ = dlogits W_o (split-K, fp32 partials)
     TRY(gemm_problem(&p1, h->dlogits, C, 0, h->snap + L.off_wo, bott, 1, N, bott, C));
-    p1.epi = EPI_BF16;
-    p1.out = h->dz;
-    p1.ldo = bott;
+    const int S = dz_split(C);
+    if (S > 1) {
+      p1.epi = EPI_F32;
+      p1.out = h->splitk;
+      p1.ldo = bott;
+      p1.ksplit = S;
+      p1.split_stride = (long long)N * bott;
+      // longest tiles first: dZ split tiles lead the persistent schedule
+      GemmProblem tmp = gb.p[0];
+      gb.p[0] = gb.p[1];
+      gb.p[1] = tmp;
+    } else {
+      p1.epi = EPI_BF16;
+      p1.out = h->dz;
+      p1.ldo = bott;
+    }
     TRY(gemm_launch(&gb, s));
-    nl += 1;
+    if (S > 1) TRY(op_splitk_bf16(h->splitk, S, (int64_t)N * bott, h->dz, s));
+    nl += S > 1 ? 2 : 1;
   }
   {
     GemmBatch gb;

@@ -77,6 +77,8 @@ struct GemmProblem {
   float* tgt;             // [m_valid]
   int stats_ld;
   float* colpart;         // EPI_CE_GRAD: optional [tiles_m*4][n_valid] column-sum partials
+  int ksplit;             // split-K factor (EPI_F32 only): split s writes out + s*split_stride
+  long long split_stride;
 };
 
 struct GemmBatch {

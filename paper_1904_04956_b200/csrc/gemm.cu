@@ -34,7 +34,7 @@ constexpr uint32_t kTmemCols = 512;
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
 
 struct TileCoord {
-  int prob, tm, tn;
+  int prob, tm, tn, ks;
 };
 
 __device__ __forceinline__ TileCoord locate(const GemmBatch& b, int tile) {
@@ -46,8 +46,18 @@ __device__ __forceinline__ TileCoord locate(const GemmBatch& b, int tile) {
   TileCoord c;
   c.prob = p;
   c.tm = local % b.p[p].tiles_m;
-  c.tn = local / b.p[p].tiles_m;
+  const int rest = local / b.p[p].tiles_m;
+  c.tn = rest % b.p[p].tiles_n;
+  c.ks = rest / b.p[p].tiles_n;
   return c;
+}
+
+// k-block range of split `ks`
+__device__ __forceinline__ void kb_range(const GemmProblem& P, int ks, int& kb0, int& kb1) {
+  const int nkb = (P.K + BK - 1) / BK;
+  const int per = (nkb + P.ksplit - 1) / P.ksplit;
+  kb0 = ks * per;
+  kb1 = min(nkb, kb0 + per);
 }
 
 __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v) {
@@ -108,8 +118,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         TileCoord tc = locate(batch, tile);
         const GemmProblem& P = batch.p[tc.prob];
         const int m0 = tc.tm * BM, n0 = tc.tn * BN;
-        const int nkb = (P.K + BK - 1) / BK;
-        for (int kb = 0; kb < nkb; ++kb) {
+        int kb0, kb1;
+        kb_range(P, tc.ks, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * kStageBytes;
           uint8_t* sB = sA + kABytes;
@@ -142,14 +153,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
       TileCoord tc = locate(batch, tile);
       const GemmProblem& P = batch.p[tc.prob];
-      const int nkb = (P.K + BK - 1) / BK;
+      int kb0, kb1;
+      kb_range(P, tc.ks, kb0, kb1);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const uint32_t idesc = idesc_bf16_f32(BM, BN, P.a_mn, P.b_mn);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
@@ -161,10 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                                  : smem_desc_sw128(aBase + k * 32, 16, 1024);
             uint64_t bd = P.b_mn ? smem_desc_sw128(bBase + k * 2048, 8192, 1024)
                                  : smem_desc_sw128(bBase + k * 32, 16, 1024);
-            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
           }
           mma_commit(&empty[stage]);
-          if (kb == nkb - 1) mma_commit(&tfull[acc]);
+          if (kb == kb1 - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == kStages) {
@@ -301,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
       } else {  // EPI_F32
-        float* orow = reinterpret_cast<float*>(P.out) + (size_t)row * P.ldo;
+        float* orow = reinterpret_cast<float*>(P.out) + (size_t)tc.ks * P.split_stride + (size_t)row * P.ldo;
 #pragma unroll 1
         for (int c = 0; c < kHalf; c += 32) {
           float v[32];
@@ -366,6 +378,7 @@ int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const v
   p->n_valid = N;
   p->m_valid = M;
   p->scale = 1.f;
+  p->ksplit = 1;
   return DS_OK;
 }
 
@@ -377,8 +390,13 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   }
   int total = 0;
   for (int i = 0; i < b->nprob; ++i) {
-    b->p[i].tile_begin = total;
-    total += b->p[i].tiles_m * b->p[i].tiles_n;
+    GemmProblem& P = b->p[i];
+    if (P.ksplit < 1) P.ksplit = 1;
+    const int nkb = (P.K + BK - 1) / BK;
+    if (P.ksplit > 1 && (P.epi != EPI_F32 || P.accumulate || nkb % P.ksplit))
+      return fail_arg("split-K needs EPI_F32, no accumulate and an even k-block split");
+    P.tile_begin = total;
+    total += P.tiles_m * P.tiles_n * P.ksplit;
   }
   b->total_tiles = total;
   if (total == 0) return DS_OK;

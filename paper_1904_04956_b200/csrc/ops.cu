@@ -70,6 +70,15 @@ __global__ void rowsum_kernel(const float* __restrict__ part, int nrows, int nco
   out[c] = s;
 }
 
+// split-K finish: out(bf16)[m][n] = sum_s part[s][m][n] in split order
+__global__ void splitk_bf16_kernel(const float* __restrict__ part, int S, int64_t n, __nv_bfloat16* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = part[i];
+    for (int k = 1; k < S; ++k) s += part[(int64_t)k * n + i];
+    out[i] = __float2bfloat16_rn(s);
+  }
+}
+
 // --------------------------------------------------------------------------
 // soft-max / CE combine: lse[m] = logsumexp over column-tile (max, sumexp)
 // partials; per-block loss partials, then one ordered sum (deterministic).
@@ -291,6 +300,12 @@ int op_colsum(const __nv_bfloat16* x, int64_t rows, int ncols, int64_t ld, float
   return DS_OK;
 }
 int64_t op_colsum_scratch(int ncols) { return (int64_t)kColSplit * ncols; }
+
+int op_splitk_bf16(const float* part, int S, int64_t n, __nv_bfloat16* out, cudaStream_t s) {
+  splitk_bf16_kernel<<<ew_grid(n), kEW, 0, s>>>(part, S, n, out);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
 
 int op_rowsum(const float* part, int nrows, int ncols, float* out, cudaStream_t s) {
   rowsum_kernel<<<(ncols + 255) / 256, 256, 0, s>>>(part, nrows, ncols, out);

@@ -13,6 +13,7 @@ int op_gather(const int64_t* idx, int B, int T, const __nv_bfloat16* feats, cons
               __nv_bfloat16* x0, int32_t* lab, int* flag, cudaStream_t s);
 int op_colsum(const __nv_bfloat16* x, int64_t rows, int ncols, int64_t ld, float* part, float* out, cudaStream_t s);
 int64_t op_colsum_scratch(int ncols);
+int op_splitk_bf16(const float* part, int S, int64_t n, __nv_bfloat16* out, cudaStream_t s);
 int op_rowsum(const float* part, int nrows, int ncols, float* out, cudaStream_t s);
 int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt, int M, float* lse, float* scratch,
                   float* loss_sum, int* flag, cudaStream_t s);
