@@ -118,7 +118,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
     h->yfull[l] = a.take<__nv_bfloat16>(base, (size_t)(h->T + 2) * h->Bmax * kLayerOut);
   }
   h->z = a.take<__nv_bfloat16>(base, (size_t)N * L.bottleneck);
-  h->stats = a.take<float2>(base, (size_t)2 * h->ntiles_c * N);  // two column halves per tile
+  h->stats = a.take<float2>(base, (size_t)4 * h->ntiles_c * N);  // four column quarters per tile
   h->tgt = a.take<float>(base, N);
   h->lse = a.take<float>(base, N);
   h->dlogits = a.take<__nv_bfloat16>(base, (size_t)N * L.classes);
@@ -241,7 +241,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.tgt = h->tgt;
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
-    TRY(op_ce_combine(h->stats, 2 * p.tiles_n, h->Nmax, h->tgt, N, h->lse, h->colpart, loss, flag, s));
+    TRY(op_ce_combine(h->stats, 4 * p.tiles_n, h->Nmax, h->tgt, N, h->lse, h->colpart, loss, flag, s));
     nl += 4;  // gather, ce stats gemm, combine (2 kernels)
   }
   if (!grad) {

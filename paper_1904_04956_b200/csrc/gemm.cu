@@ -8,12 +8,12 @@
 // whose epilogue computes soft-max statistics (forward) or
 // (softmax - onehot)/N (backward) without ever materialising fp32 logits.
 //
-// Structure (one CTA per SM, 384 threads):
+// Structure (one CTA per SM, 640 threads):
 //   warp 0      : TMA producer (one elected lane), 4-stage smem ring
 //   warp 1      : tcgen05.mma issuer (one elected lane)
 //   warp 2      : TMEM allocator (512 columns = 2 x 128x256 fp32 accumulators)
-//   warps 4..11 : epilogue, thread = accumulator row (TMEM lane); warps
-//                 4..7 take columns 0..127 of the tile, 8..11 columns 128..255
+//   warps 4..19 : epilogue, thread = accumulator row (TMEM lane); warp 4+e
+//                 takes lane quadrant e%4 and columns 64*(e/4) .. +64
 // Tiles are walked round-robin over the persistent grid; the two TMEM
 // accumulators let the epilogue of tile i overlap the main loop of tile i+1.
 #include "ds_internal.h"
@@ -28,7 +28,7 @@ constexpr int kStages = 4;
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 constexpr int kBBytes = BN * BK * 2;  // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kThreads = 384;  // warps 0-3 roles, 4-11 epilogue (4 lane quadrants x 2 column halves)
+constexpr int kThreads = 640;  // warps 0-3 roles, 4-19 epilogue (4 lane quadrants x 4 column quarters)
 constexpr int kEpiWarp0 = 4;
 constexpr uint32_t kTmemCols = 512;
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 256);
+      mbar_init(&tempty[a], 512);
     }
     fence_barrier_init();
   }
@@ -188,50 +188,65 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   } else if (warp >= kEpiWarp0) {
     // ---------------- epilogue ----------------
     const uint32_t e = warp - kEpiWarp0;
-    const uint32_t q = e & 3;    // TMEM lane quadrant (== warp % 4)
-    const uint32_t hf = e >> 2;  // column half of the 256-wide tile
-    constexpr int kHalf = BN / 2;
+    const uint32_t q = e & 3;     // TMEM lane quadrant (== warp % 4)
+    const uint32_t part = e >> 2; // column quarter of the 256-wide tile
+    constexpr int kCols = BN / 4; // 64 columns per thread
     constexpr float kLog2e = 1.4426950408889634f;
     int it = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
       TileCoord tc = locate(batch, tile);
       const GemmProblem& P = batch.p[tc.prob];
+      // problem fields into registers once per tile (P is indexed dynamically)
+      const int epi = P.epi, n_valid = P.n_valid;
+      const float* __restrict__ bias = P.bias;
+      const float scale = P.scale;
+      const long long ldo = P.ldo;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int row = tc.tm * BM + q * 32 + lane;
-      const int n0 = tc.tn * BN + hf * kHalf;
+      const int n0 = tc.tn * BN + part * kCols;
       const bool row_ok = row < P.m_valid;
+      const bool full_cols = n0 + kCols <= n_valid;
       // per-row epilogue inputs, fetched before the accumulator wait
       int lbl = -1;
       float l = 0.f;
-      if (P.epi >= EPI_CE_STATS && row_ok) {
+      if (epi >= EPI_CE_STATS && row_ok) {
         lbl = P.labels[row];
-        if (P.epi == EPI_CE_GRAD) l = P.lse[row];
+        if (epi == EPI_CE_GRAD) l = P.lse[row];
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + acc * BN + ((q * 32) << 16) + hf * kHalf;
+      const uint32_t t_row = tmem_base + acc * BN + ((q * 32) << 16) + part * kCols;
 
-      if (P.epi == EPI_CE_STATS) {
-        // online (max, sum exp) over this thread's 128 columns, log2 domain
+      if (epi == EPI_CE_STATS) {
+        // online (max, sum exp) over this thread's 64 columns, log2 domain
         float mx = -INFINITY, se = 0.f, tg = 0.f;
         bool have_t = false;
 #pragma unroll 1
-        for (int c = 0; c < kHalf; c += 32) {
+        for (int c = 0; c < kCols; c += 32) {
           float v[32];
           tmem_ld32(t_row + c, v);
           tmem_ld_wait();
           const int nb = n0 + c;
           float cm = -INFINITY;
+          if (full_cols) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 bb = (P.bias && nb + i < P.n_valid) ? __ldg(reinterpret_cast<const float4*>(P.bias + nb + i))
-                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-            v[i] = (nb + i < P.n_valid) ? (v[i] + bb.x) * kLog2e : -INFINITY;
-            v[i + 1] = (nb + i + 1 < P.n_valid) ? (v[i + 1] + bb.y) * kLog2e : -INFINITY;
-            v[i + 2] = (nb + i + 2 < P.n_valid) ? (v[i + 2] + bb.z) * kLog2e : -INFINITY;
-            v[i + 3] = (nb + i + 3 < P.n_valid) ? (v[i + 3] + bb.w) * kLog2e : -INFINITY;
-            cm = fmaxf(cm, fmaxf(fmaxf(v[i], v[i + 1]), fmaxf(v[i + 2], v[i + 3])));
+            for (int i = 0; i < 32; i += 4) {
+              const float4 bb = bias ? __ldg(reinterpret_cast<const float4*>(bias + nb + i))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+              v[i] = (v[i] + bb.x) * kLog2e;
+              v[i + 1] = (v[i + 1] + bb.y) * kLog2e;
+              v[i + 2] = (v[i + 2] + bb.z) * kLog2e;
+              v[i + 3] = (v[i + 3] + bb.w) * kLog2e;
+              cm = fmaxf(cm, fmaxf(fmaxf(v[i], v[i + 1]), fmaxf(v[i + 2], v[i + 3])));
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const bool in = nb + i < n_valid;
+              v[i] = in ? (v[i] + (bias ? __ldg(bias + nb + i) : 0.f)) * kLog2e : -INFINITY;
+              cm = fmaxf(cm, v[i]);
+            }
           }
           if (lbl >= nb && lbl < nb + 32) {
 #pragma unroll
@@ -241,32 +256,38 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
           if (cm > -INFINITY) {
             const float nm = fmaxf(mx, cm);
-            float sacc = 0.f;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // independent chains
 #pragma unroll
-            for (int i = 0; i < 32; ++i) sacc += ex2_fast(v[i] - nm);
-            se = se * ex2_fast(mx - nm) + sacc;
+            for (int i = 0; i < 32; i += 4) {
+              s0 += ex2_fast(v[i] - nm);
+              s1 += ex2_fast(v[i + 1] - nm);
+              s2 += ex2_fast(v[i + 2] - nm);
+              s3 += ex2_fast(v[i + 3] - nm);
+            }
+            se = se * ex2_fast(mx - nm) + ((s0 + s1) + (s2 + s3));
             mx = nm;
           }
         }
         if (row_ok) {
           // stats in natural-log units: max, sum exp(x - max)
-          P.stats[(size_t)(tc.tn * 2 + hf) * P.stats_ld + row] = make_float2(mx / kLog2e, se);
+          P.stats[(size_t)(tc.tn * 4 + part) * P.stats_ld + row] = make_float2(mx / kLog2e, se);
           if (have_t) P.tgt[row] = tg / kLog2e;
         }
-      } else if (P.epi == EPI_CE_GRAD) {
-        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)row * P.ldo;
+      } else if (epi == EPI_CE_GRAD) {
+        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)row * ldo;
+        float* colpart = P.colpart;
         const float l2 = l * kLog2e;
 #pragma unroll 1
-        for (int c = 0; c < kHalf; c += 32) {
+        for (int c = 0; c < kCols; c += 32) {
           float v[32];
           tmem_ld32(t_row + c, v);
           tmem_ld_wait();
           const int nb = n0 + c;
-          if (nb >= P.n_valid) continue;
+          if (nb >= n_valid) continue;
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 bb = P.bias ? __ldg(reinterpret_cast<const float4*>(P.bias + nb + i))
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 bb = bias ? __ldg(reinterpret_cast<const float4*>(bias + nb + i))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
             v[i] = ex2_fast(fmaf(v[i] + bb.x, kLog2e, -l2));
             v[i + 1] = ex2_fast(fmaf(v[i + 1] + bb.y, kLog2e, -l2));
             v[i + 2] = ex2_fast(fmaf(v[i + 2] + bb.z, kLog2e, -l2));
@@ -277,30 +298,31 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             for (int i = 0; i < 32; ++i)
               if (lbl == nb + i) v[i] -= 1.f;
           }
+          const float sc = row_ok ? scale : 0.f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = row_ok ? v[i] * P.scale : 0.f;
+          for (int i = 0; i < 32; ++i) v[i] *= sc;
           if (row_ok) {
             store_bf16x16(orow + nb, v);
             store_bf16x16(orow + nb + 16, v + 16);
           }
-          if (P.colpart) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
+          if (colpart) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
             const float cs = warp_colsum32(v);
-            P.colpart[(size_t)(tc.tm * 4 + q) * P.n_valid + nb + lane] = cs;
+            colpart[(size_t)(tc.tm * 4 + q) * n_valid + nb + lane] = cs;
           }
         }
-      } else if (P.epi == EPI_BF16) {
-        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)row * P.ldo;
+      } else if (epi == EPI_BF16) {
+        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)row * ldo;
 #pragma unroll 1
-        for (int c = 0; c < kHalf; c += 32) {
+        for (int c = 0; c < kCols; c += 32) {
           float v[32];
           tmem_ld32(t_row + c, v);
           tmem_ld_wait();
           const int nb = n0 + c;
-          if (nb >= P.n_valid) continue;
-          if (P.bias) {
+          if (nb >= n_valid) continue;
+          if (bias) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
-              const float4 bb = __ldg(reinterpret_cast<const float4*>(P.bias + nb + i));
+              const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + nb + i));
               v[i] += bb.x;
               v[i + 1] += bb.y;
               v[i + 2] += bb.z;
@@ -309,31 +331,32 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
           if (row_ok) {
             store_bf16x16(orow + nb, v);
-            if (nb + 16 < P.n_valid) store_bf16x16(orow + nb + 16, v + 16);
+            if (nb + 16 < n_valid) store_bf16x16(orow + nb + 16, v + 16);
           }
         }
       } else {  // EPI_F32
-        float* orow = reinterpret_cast<float*>(P.out) + (size_t)tc.ks * P.split_stride + (size_t)row * P.ldo;
+        float* orow = reinterpret_cast<float*>(P.out) + (size_t)tc.ks * P.split_stride + (size_t)row * ldo;
+        const int accumulate = P.accumulate;
 #pragma unroll 1
-        for (int c = 0; c < kHalf; c += 32) {
+        for (int c = 0; c < kCols; c += 32) {
           float v[32];
           tmem_ld32(t_row + c, v);
           tmem_ld_wait();
           const int nb = n0 + c;
-          if (!row_ok || nb >= P.n_valid) continue;
-          const bool vec = (nb + 32 <= P.n_valid) && ((P.ldo & 3) == 0) && !P.accumulate;
+          if (!row_ok || nb >= n_valid) continue;
+          const bool vec = (nb + 32 <= n_valid) && ((ldo & 3) == 0) && !accumulate;
           if (vec) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4)
               *reinterpret_cast<float4*>(orow + nb + i) =
-                  make_float4(v[i] * P.scale, v[i + 1] * P.scale, v[i + 2] * P.scale, v[i + 3] * P.scale);
+                  make_float4(v[i] * scale, v[i + 1] * scale, v[i + 2] * scale, v[i + 3] * scale);
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int n = nb + i;
-              if (n < P.n_valid) {
-                float x = v[i] * P.scale;
-                if (P.accumulate) x += orow[n];
+              if (n < n_valid) {
+                float x = v[i] * scale;
+                if (accumulate) x += orow[n];
                 orow[n] = x;
               }
             }
