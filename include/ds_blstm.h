@@ -114,6 +114,9 @@ int ds_blstm_set_grad_scale(ds_blstm* h, float frames_total);
  * 3 = gather / soft-max combine / bias column sums. */
 int ds_blstm_set_profile(ds_blstm* h, int32_t enable);
 int ds_blstm_profile_read(ds_blstm* h, float* ms_by_kind, int32_t nkinds);
+/* Individual phase intervals (in issue order) since the last read, without
+ * clearing them (call before ds_blstm_profile_read). */
+int ds_blstm_profile_list(ds_blstm* h, float* ms, int32_t* kinds, int32_t max_n, int32_t* n_out);
 /* Kernel launches issued by the last ds_blstm_fwd_bwd / ds_blstm_loss. */
 int32_t ds_blstm_kernel_count(ds_blstm* h);
 

@@ -75,6 +75,7 @@ struct ds_blstm {
   std::vector<int> ev_kind;
   int launches = 0;  // kernel launches issued by the last step
   float grad_frames = 0.f;  // CE gradient divisor override (0: B*T)
+  int pad_B = -1;           // batch size the Y_full zero pads were laid out for
 };
 
 namespace {
@@ -185,10 +186,6 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
 
   MARK(PH_OTHER);
   TRY(op_gather(idx, B, T, h->feats, h->labels, h->n_seq, h->x0, h->lab, flag, s));
-  for (int l = 0; l < Lh; ++l) {
-    DS_CUDA_TRY(cudaMemsetAsync(h->yfull[l], 0, (size_t)B * kLayerOut * 2, s));
-    DS_CUDA_TRY(cudaMemsetAsync(h->yfull[l] + (size_t)(T + 1) * B * kLayerOut, 0, (size_t)B * kLayerOut * 2, s));
-  }
   auto Y = [&](int l) { return h->yfull[l] + (size_t)B * kLayerOut; };
 
   // ---- forward ----
@@ -205,6 +202,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.out = h->gates[l];
     p.ldo = kGates2;
     p.bias = bias_l + (size_t)l * kGates2;
+    TRY(gemm_bf16_output(&p));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], nullptr, nullptr,
@@ -223,8 +221,10 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.out = h->z;
     p.ldo = bott;
     p.bias = bias_b;
+    TRY(gemm_bf16_output(&p));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
+    MARK(PH_GEMM);
     nl += 1;
   }
   {
@@ -264,11 +264,13 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.ldo = C;
     p.scale = 1.0f / (h->grad_frames > 0.f ? h->grad_frames : (float)N);
     p.colpart = h->biaspart;
+    TRY(gemm_bf16_output(&p));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
     TRY(op_rowsum(h->biaspart, p.tiles_m * 4, C, grad + L.off_bo, s));
     nl += 2;
+    MARK(PH_GEMM);
   }
   {
     GemmBatch gb;
@@ -315,6 +317,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p1.epi = EPI_BF16;
     p1.out = h->dy;
     p1.ldo = kLayerOut;
+    TRY(gemm_bf16_output(&p1));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
@@ -355,6 +358,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       p3.epi = EPI_BF16;
       p3.out = h->dy;
       p3.ldo = kLayerOut;
+      TRY(gemm_bf16_output(&p3));
       gb.nprob = 4;
     }
     MARK(PH_OTHER);
@@ -383,6 +387,14 @@ int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, i
   if (!h->feats) return fail_arg("dataset not bound (ds_blstm_set_dataset)");
   if (!loss) return fail_arg("loss_sum pointer is required");
   DS_CUDA_TRY(cudaSetDevice(h->device));
+  if (h->pad_B != B) {  // zero rows of Y_full (h_{-1}, h_T): no kernel ever writes them
+    for (int l = 0; l < h->L.layers; ++l) {
+      DS_CUDA_TRY(cudaMemsetAsync(h->yfull[l], 0, (size_t)B * kLayerOut * 2, s));
+      DS_CUDA_TRY(
+          cudaMemsetAsync(h->yfull[l] + (size_t)(h->T + 1) * B * kLayerOut, 0, (size_t)B * kLayerOut * 2, s));
+    }
+    h->pad_B = B;
+  }
   cudaStreamCaptureStatus cs;
   DS_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
   if (!use_graphs() || h->profile || cs != cudaStreamCaptureStatusNone)
@@ -574,6 +586,19 @@ int ds_blstm_profile_read(ds_blstm* h, float* ms_by_kind, int32_t nkinds) {
 }
 
 int32_t ds_blstm_kernel_count(ds_blstm* h) { return h ? h->launches : -1; }
+
+int ds_blstm_profile_list(ds_blstm* h, float* ms, int32_t* kinds, int32_t max_n, int32_t* n_out) {
+  if (!h || !ms || !kinds || !n_out) return fail_arg("null argument");
+  DS_CUDA_TRY(cudaSetDevice(h->device));
+  if (!h->ev.empty()) DS_CUDA_TRY(cudaEventSynchronize(h->ev.back()));
+  int n = 0;
+  for (size_t i = 0; i + 1 < h->ev.size() && n < max_n; ++i, ++n) {
+    DS_CUDA_TRY(cudaEventElapsedTime(&ms[n], h->ev[i], h->ev[i + 1]));
+    kinds[n] = h->ev_kind[i];
+  }
+  *n_out = n;
+  return DS_OK;
+}
 
 int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C,
                        int64_t ldc, int32_t M, int32_t N, int32_t K, ds_stream_t stream) {

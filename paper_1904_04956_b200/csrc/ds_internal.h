@@ -35,7 +35,8 @@ int num_sms();
 // bytes; box = box_inner x box_outer elements; SWIZZLE_128B (box_inner *
 // elem_bytes must be 128).
 int make_tmap_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t outer,
-                 uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer);
+                 uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                 CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B);
 
 // ---------------------------------------------------------------------------
 // GEMM: C[m, n] = sum_k A[m, k] * B[n, k], bf16 operands, fp32 accumulate in
@@ -59,6 +60,7 @@ constexpr int kMaxProblems = 4;
 struct GemmProblem {
   CUtensorMap tmA;  // 64-byte aligned (first member)
   CUtensorMap tmB;
+  CUtensorMap tmC;  // bf16 outputs (EPI_BF16 / EPI_CE_GRAD): [m_valid][n_valid], 32x32 boxes, SW64
   int M, N, K;
   int a_mn, b_mn;
   int epi;
@@ -77,6 +79,7 @@ struct GemmProblem {
   float* tgt;             // [m_valid]
   int stats_ld;
   float* colpart;         // EPI_CE_GRAD: optional [tiles_m*4][n_valid] column-sum partials
+  int c_tma;              // bf16 output stored through smem staging + TMA (tmC valid)
   int ksplit;             // split-K factor (EPI_F32 only): split s writes out + s*split_stride
   long long split_stride;
 };
@@ -93,5 +96,7 @@ struct GemmBatch {
 int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const void* B, long long ldb, int b_mn,
                  int M, int N, int K);
 int gemm_launch(GemmBatch* batch, cudaStream_t stream);
+// Attach the TMA store map for a bf16 output (call after setting out/ldo/n_valid/m_valid).
+int gemm_bf16_output(GemmProblem* p);
 
 }  // namespace ds

@@ -31,7 +31,9 @@ constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 640;  // warps 0-3 roles, 4-19 epilogue (4 lane quadrants x 4 column quarters)
 constexpr int kEpiWarp0 = 4;
 constexpr uint32_t kTmemCols = 512;
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
+constexpr int kStageC = 32 * 32 * 2;  // per-epilogue-warp bf16 staging box (32 rows x 32 cols, SW64)
+constexpr int kEpiWarps = 16;
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + kEpiWarps * kStageC + 256;
 
 struct TileCoord {
   int prob, tm, tn, ks;
@@ -72,10 +74,37 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v
   reinterpret_cast<uint4*>(dst)[1] = w[1];
 }
 
+// Stage this warp's 32 rows x 32 bf16 columns (lane = row) in smem with the
+// 64-byte swizzle and TMA-store the box at (col, row0): full 64 B row
+// segments reach L2 instead of 16 B pieces of 32 different rows.
+__device__ __forceinline__ void store_box_tma(const CUtensorMap* map, uint8_t* stg, const float* v, int col, int row0) {
+  const uint32_t lane = lane_id();
+  if (lane == 0) bulk_wait_read0();  // the previous box has left this buffer
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 w;
+    uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]);
+      u[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = w;
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map, stg, col, row0);
+    bulk_commit();
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmBatch batch) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint8_t* cstage = smem + kStages * kStageBytes;  // [kEpiWarps][32x32 bf16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(cstage + kEpiWarps * kStageC);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -301,7 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const float sc = row_ok ? scale : 0.f;
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] *= sc;
-          if (row_ok) {
+          if (P.c_tma) {
+            store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, tc.tm * BM + q * 32);
+          } else if (row_ok) {
             store_bf16x16(orow + nb, v);
             store_bf16x16(orow + nb + 16, v + 16);
           }
@@ -329,7 +360,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               v[i + 3] += bb.w;
             }
           }
-          if (row_ok) {
+          if (P.c_tma) {
+            store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, tc.tm * BM + q * 32);
+          } else if (row_ok) {
             store_bf16x16(orow + nb, v);
             if (nb + 16 < n_valid) store_bf16x16(orow + nb + 16, v + 16);
           }
@@ -366,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait0();  // staged output stores complete before exit
   }
 
   tc_fence_before();
@@ -402,6 +436,15 @@ int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const v
   p->m_valid = M;
   p->scale = 1.f;
   p->ksplit = 1;
+  return DS_OK;
+}
+
+int gemm_bf16_output(GemmProblem* p) {
+  if (p->epi != EPI_BF16 && p->epi != EPI_CE_GRAD) return fail_arg("TMA store only for bf16 epilogues");
+  int rc = make_tmap_2d(&p->tmC, p->out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)p->n_valid, (uint64_t)p->m_valid,
+                        (uint64_t)p->ldo * 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (rc) return rc;
+  p->c_tma = 1;
   return DS_OK;
 }
 

@@ -41,23 +41,30 @@ __global__ void gather_kernel(const int64_t* __restrict__ idx, int B, int T, con
 
 // --------------------------------------------------------------------------
 // column sums of a bf16 [rows, ld] matrix, deterministic two-stage.
-constexpr int kColSplit = 32;
+constexpr int kColSplit = 32;  // minimum split count (scratch is sized for 32 x the widest matrix)
+inline int colsum_splits(int ncols) {
+  const int cb = (ncols + 255) / 256;
+  int sp = 1024 / cb;
+  sp = sp < kColSplit ? kColSplit : sp;
+  const long long cap = (long long)kColSplit * (ncols > kGates2 ? ncols : kGates2) / ncols;
+  return (int)(sp > cap ? cap : sp);
+}
 __global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int ncols, int64_t ld,
                                       float* __restrict__ part) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int split = blockIdx.y;
   if (col >= ncols) return;
-  const int64_t per = (rows + kColSplit - 1) / kColSplit;
+  const int64_t per = (rows + gridDim.y - 1) / gridDim.y;
   const int64_t r0 = split * per, r1 = min(rows, r0 + per);
   float s = 0.f;
   for (int64_t r = r0; r < r1; ++r) s += __bfloat162float(x[r * ld + col]);
   part[(int64_t)split * ncols + col] = s;
 }
-__global__ void colsum_final_kernel(const float* __restrict__ part, int ncols, float* __restrict__ out) {
+__global__ void colsum_final_kernel(const float* __restrict__ part, int ncols, int splits, float* __restrict__ out) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= ncols) return;
   float s = 0.f;
-  for (int k = 0; k < kColSplit; ++k) s += part[(int64_t)k * ncols + col];
+  for (int k = 0; k < splits; ++k) s += part[(int64_t)k * ncols + col];
   out[col] = s;
 }
 
@@ -66,7 +73,15 @@ __global__ void rowsum_kernel(const float* __restrict__ part, int nrows, int nco
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncols) return;
   float s = 0.f;
-  for (int r = 0; r < nrows; ++r) s += part[(int64_t)r * ncols + c];
+  int r = 0;
+  for (; r + 8 <= nrows; r += 8) {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = part[(int64_t)(r + k) * ncols + c];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; r < nrows; ++r) s += part[(int64_t)r * ncols + c];
   out[c] = s;
 }
 
@@ -82,34 +97,48 @@ __global__ void splitk_bf16_kernel(const float* __restrict__ part, int S, int64_
 // --------------------------------------------------------------------------
 // soft-max / CE combine: lse[m] = logsumexp over column-tile (max, sumexp)
 // partials; per-block loss partials, then one ordered sum (deterministic).
-constexpr int kCeRows = 256;
+constexpr int kCeRows = 32;  // rows per block (lane = row: coalesced stats reads)
+constexpr int kCeGroups = 8;  // tile groups per block (warps)
 __global__ void ce_rows_kernel(const float2* __restrict__ stats, int ntiles, int64_t ld, const float* __restrict__ tgt,
                                int M, float* __restrict__ lse, float* __restrict__ part) {
-  __shared__ float red[kCeRows];
-  const int m = blockIdx.x * kCeRows + threadIdx.x;
-  float loss = 0.f;
+  __shared__ float smx[kCeGroups][kCeRows], ssum[kCeGroups][kCeRows];
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * kCeRows + lane;
+  float mx = -INFINITY, s = 0.f;
   if (m < M) {
-    float mx = -INFINITY;
-    for (int j = 0; j < ntiles; ++j) mx = fmaxf(mx, stats[j * ld + m].x);
-    float s = 0.f;
-    for (int j = 0; j < ntiles; ++j) {
+    for (int j = g; j < ntiles; j += kCeGroups) {  // online combine of this group's tiles
       const float2 st = stats[j * ld + m];
-      s += st.y * __expf(st.x - mx);
+      if (!(st.y > 0.f)) continue;  // fully masked column block
+      if (st.x > mx) {
+        s = s * __expf(mx - st.x) + st.y;
+        mx = st.x;
+      } else {
+        s += st.y * __expf(st.x - mx);
+      }
     }
-    const float l = mx + __logf(s);
-    lse[m] = l;
-    loss = l - tgt[m];
   }
-  red[threadIdx.x] = loss;
+  smx[g][lane] = mx;
+  ssum[g][lane] = s;
   __syncthreads();
-  for (int w = kCeRows / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
+  if (g == 0) {
+    float loss = 0.f;
+    if (m < M) {
+      float M2 = -INFINITY;
+      for (int k = 0; k < kCeGroups; ++k) M2 = fmaxf(M2, smx[k][lane]);
+      float S = 0.f;
+      for (int k = 0; k < kCeGroups; ++k)
+        if (ssum[k][lane] > 0.f) S += ssum[k][lane] * __expf(smx[k][lane] - M2);
+      const float l = M2 + __logf(S);
+      lse[m] = l;
+      loss = l - tgt[m];
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, off);
+    if (lane == 0) part[blockIdx.x] = loss;
   }
-  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
 __global__ void ce_sum_kernel(const float* __restrict__ part, int n, float* __restrict__ loss_sum, int* __restrict__ flag) {
-  __shared__ float red[256];
+  __shared__ float red[1024];
   float acc = 0.f;
   for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
   red[threadIdx.x] = acc;
@@ -293,9 +322,10 @@ int op_gather(const int64_t* idx, int B, int T, const __nv_bfloat16* feats, cons
 }
 
 int op_colsum(const __nv_bfloat16* x, int64_t rows, int ncols, int64_t ld, float* part, float* out, cudaStream_t s) {
-  dim3 g1((ncols + 255) / 256, kColSplit);
+  const int sp = colsum_splits(ncols);
+  dim3 g1((ncols + 255) / 256, sp);
   colsum_partial_kernel<<<g1, 256, 0, s>>>(x, rows, ncols, ld, part);
-  colsum_final_kernel<<<(ncols + 255) / 256, 256, 0, s>>>(part, ncols, out);
+  colsum_final_kernel<<<(ncols + 255) / 256, 256, 0, s>>>(part, ncols, sp, out);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
@@ -316,8 +346,8 @@ int op_rowsum(const float* part, int nrows, int ncols, float* out, cudaStream_t 
 int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt, int M, float* lse, float* scratch,
                   float* loss_sum, int* flag, cudaStream_t s) {
   const int nblk = (M + kCeRows - 1) / kCeRows;
-  ce_rows_kernel<<<nblk, kCeRows, 0, s>>>(stats, ntiles, ld, tgt, M, lse, scratch);
-  ce_sum_kernel<<<1, 256, 0, s>>>(scratch, nblk, loss_sum, flag);
+  ce_rows_kernel<<<nblk, kCeGroups * 32, 0, s>>>(stats, ntiles, ld, tgt, M, lse, scratch);
+  ce_sum_kernel<<<1, 1024, 0, s>>>(scratch, nblk, loss_sum, flag);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
