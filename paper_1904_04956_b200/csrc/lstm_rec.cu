@@ -128,7 +128,7 @@ __device__ __forceinline__ void acquire_for_tma(const uint32_t* flag, int varian
     (void)ld_acquire_gpu(flag);
   else
     fence_acq_rel_gpu();
-  fence_proxy_async_global();
+  if (!(variant & 128)) fence_proxy_async_global();
 }
 
 // all epilogue threads finished step s's global writes -> flag = s + 1
@@ -710,6 +710,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
                                      (int)fwd::Cfg<16>::kSmem));
     DS_CUDA_TRY(
         cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmem));
+
     attr_set = true;
   }
   const int B = a.B, T = a.T;
