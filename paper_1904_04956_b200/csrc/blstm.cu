@@ -263,7 +263,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.out = h->dlogits;
     p.ldo = C;
     p.scale = 1.0f / (h->grad_frames > 0.f ? h->grad_frames : (float)N);
-    p.colpart = h->biaspart;
+    p.colpart = getenv("DS_NO_COLSUM") ? nullptr : h->biaspart;
     TRY(gemm_bf16_output(&p));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));

@@ -123,6 +123,31 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target)
     }
   }
 }
+// wait until all four consecutive flags (16-byte aligned) reach `target`,
+// polling them with one acquire vector load per round trip
+__device__ __forceinline__ void wait_flags4(const uint32_t* flags4, uint32_t target) {
+  while (true) {
+    const uint4 v = ld_acquire_gpu_v4(flags4);
+    if (min(min(v.x, v.y), min(v.z, v.w)) >= target) break;
+  }
+}
+// chunk-flag cache for issuers walking consecutive chunk flags
+struct FlagCache {
+  uint4 v;
+  int base;
+};
+__device__ __forceinline__ void wait_flag_cached(FlagCache& c, const uint32_t* flags, int idx, uint32_t target) {
+  const int base = idx & ~3;
+  while (true) {
+    if (c.base == base) {
+      const uint32_t x = (idx & 3) == 0 ? c.v.x : (idx & 3) == 1 ? c.v.y : (idx & 3) == 2 ? c.v.z : c.v.w;
+      if (x >= target) return;
+    }
+    c.v = ld_acquire_gpu_v4(flags + base);
+    c.base = base;
+  }
+}
+
 __device__ __forceinline__ void acquire_for_tma(const uint32_t* flag, int variant) {
   if (variant & 4)
     (void)ld_acquire_gpu(flag);
@@ -239,11 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
           if (kb % kCl == crank) {
             if (s > 0) {  // chunk kb = units kb*64 .. +64 <- unit blocks kb*64/kU ..
               constexpr int kPer = 64 / kU;
+              if (kPer == 4) {
+                wait_flags4(flags + 4 * kb, (uint32_t)s);  // acquire included
+              } else {
 #pragma unroll
-              for (int u = 0; u < kPer; ++u) wait_flag(flags + kPer * kb + u, (uint32_t)s);
-              acquire_for_tma(flags + kPer * kb + kPer - 1, P.variant);
+                for (int u = 0; u < kPer; ++u) wait_flag(flags + kPer * kb + u, (uint32_t)s);
+                (void)ld_acquire_gpu(flags + kPer * kb + kPer - 1);
+              }
+              fence_proxy_async_global();
             }
             tma_load_2d_mc(sA + stage * kTileA, &P.tmA, &full[stage], dir * kH + kb * 64, arow, all);
+            if (P.trace && blockIdx.x < kCl)  // debug: chunk issue times of cluster 0
+              P.trace[(size_t)gridDim.x * T * kTraceSlots + ((size_t)s * 8 + kb) * 2] = globaltimer();
           }
           if (kb == 0) trace_mark(P.trace, T, s, 0);
           if (++stage == kStagesF) {
@@ -266,6 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
       for (int kb = 0; kb < kH / 64; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (P.trace && blockIdx.x == 0 && lane == 0)  // debug: chunk arrival times at CTA 0
+          P.trace[(size_t)gridDim.x * T * kTraceSlots + ((size_t)s * 8 + kb) * 2 + 1] = globaltimer();
         if (elect_one()) {
           const uint32_t abase = smem_u32(sA + stage * kTileA);
 #pragma unroll
@@ -461,6 +495,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         tma_load_2d(sW + j * kGU * 128, &P.tmW, wbar, ks * kKSlice + j * 64, dir * kH + ug * kGU);
       int stage = 0;
       uint32_t phase = 0;
+      FlagCache fc;
+      fc.base = -1;
       for (int s = 1; s < T; ++s) {
         const int t = dir == 0 ? T - 1 - s : s;
         const int tprev = dir == 0 ? t + 1 : t - 1;
@@ -477,8 +513,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
                              pair_mask);
             }
           } else {
-            wait_flag(flags + chunk, (uint32_t)s);
-            acquire_for_tma(flags + chunk, P.variant);
+            wait_flag_cached(fc, flags, chunk, (uint32_t)s);  // acquire vector poll
+            fence_proxy_async_global();
             tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
           }
           if (j == 0) trace_mark(P.trace, T, s, 0);
@@ -570,9 +606,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       for (int u = 0; u < 8; ++u) dh[u] = 0.f;
       // the finalisers we feed must have consumed the previous exchange
       // (checked before the MMA wait so the L2 round trip overlaps it)
-      if (s >= 2 && lane == 0) {
-        wait_flag(flags + ug * kKS + 2 * hf, (uint32_t)s);
-        wait_flag(flags + ug * kKS + 2 * hf + 1, (uint32_t)s);
+      if (s >= 2 && lane == 0) {  // the finalisers 4ug .. 4ug+3 (one vector poll)
+        wait_flags4(flags + ug * kKS, (uint32_t)s);
       }
       __syncwarp();
       if (s > 0) {
