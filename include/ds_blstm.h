@@ -127,7 +127,7 @@ int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, 
 
 /* Recurrent-kernel self-test hooks (tests only): run one bidirectional layer's
  * forward / backward recurrence on caller buffers (layouts of lstm_rec.cu).
- * counters: >= 32*ceil(B/128) words; trace (nullable): [grid][T][4] u64
+ * counters: >= 512*ceil(B/128) words; trace (nullable): [grid][T][4] u64
  * globaltimer marks (producer ready, loads issued, MMA done, step published). */
 int ds_debug_lstm_fwd(int32_t B, int32_t T, void* gates, float* cstate, void* y_full, const void* whh,
                       uint32_t* counters, uint64_t* trace, ds_stream_t stream);

@@ -155,7 +155,11 @@ class Learner:
         self.loss_sum = torch.zeros(1, dtype=torch.float32, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.idx = torch.zeros(max_batch, dtype=torch.int64, device=dev)
-        self.idx_host = torch.zeros(max_batch, dtype=torch.int64).pin_memory()
+        # ring of pinned staging buffers: a batch upload only waits for the
+        # copy that used the same slot several uploads ago
+        self._ring = [torch.zeros(max_batch, dtype=torch.int64).pin_memory() for _ in range(4)]
+        self._ring_ev = [None] * 4
+        self._ring_i = 0
         self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
         self.batch = 0
         if theta0 is not None:
@@ -189,10 +193,17 @@ class Learner:
         B = len(batch)
         if not 1 <= B <= self.max_batch:
             raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
-        self.stream.synchronize()  # pinned staging buffer reuse
-        self.idx_host[:B] = torch.from_numpy(np.asarray(batch, dtype=np.int64))
+        k = self._ring_i
+        self._ring_i = (k + 1) % len(self._ring)
+        if self._ring_ev[k] is not None:
+            self._ring_ev[k].synchronize()  # slot's previous H2D copy has finished
+        host = self._ring[k]
+        host[:B] = torch.from_numpy(np.asarray(batch, dtype=np.int64))
         with torch.cuda.stream(self.stream):
-            self.idx[:B].copy_(self.idx_host[:B], non_blocking=True)
+            self.idx[:B].copy_(host[:B], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        self._ring_ev[k] = ev
         return B
 
     def gradient(self, batch: np.ndarray) -> None:

@@ -158,6 +158,14 @@ DS_DEV void st_cluster_v4(uint32_t caddr, float a, float b, float c, float d) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(caddr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
 }
+// smem -> (remote) smem bulk copy through the async engine; completes `bytes`
+// on the destination CTA's mbarrier (shared::cluster addresses from mapa).
+DS_DEV void bulk_copy_s2cluster(uint32_t dst_caddr, const void* src, uint32_t bytes, uint32_t mbar_caddr) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_caddr),
+      "r"(smem_u32(src)), "r"(bytes), "r"(mbar_caddr)
+      : "memory");
+}
 DS_DEV void mbar_arrive_remote_release(uint32_t caddr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }

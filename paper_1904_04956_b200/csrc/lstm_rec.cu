@@ -71,50 +71,6 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* v) {
   return w;
 }
 
-struct Smem {
-  uint8_t* w;
-  uint8_t* a;
-  uint64_t* full;
-  uint64_t* empty;
-  uint64_t* wbar;
-  uint64_t* tfull;
-  uint64_t* tempty;
-  uint32_t* tmem_slot;
-};
-
-__device__ __forceinline__ Smem carve(uint8_t* raw) {
-  uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  Smem m;
-  m.w = s;
-  m.a = s + kWBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(m.a + kStages * kTileA);
-  m.full = bars;
-  m.empty = bars + kStages;
-  m.wbar = bars + 2 * kStages;
-  m.tfull = m.wbar + 1;
-  m.tempty = m.tfull + 1;
-  m.tmem_slot = reinterpret_cast<uint32_t*>(m.tempty + 1);
-  return m;
-}
-
-__device__ __forceinline__ void setup(const Smem& m, uint32_t ncols) {
-  const uint32_t warp = warp_id(), lane = lane_id();
-  if (warp == 1 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&m.full[s], 1);
-      mbar_init(&m.empty[s], 1);
-    }
-    mbar_init(m.wbar, 1);
-    mbar_init(m.tfull, 1);
-    mbar_init(m.tempty, kEpiThreads);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(m.tmem_slot, ncols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-}
-
 // spin (relaxed, L1-bypassing) until *flag >= target, then acquire and make
 // the released generic-proxy writes visible to our async-proxy (TMA) reads.
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target) {
@@ -123,6 +79,12 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target)
     }
   }
 }
+// Step flags: 32 per (dir, batch tile) group, four per 128-byte line so the
+// pollers of one line are few (a single hot line serialised ~128 pollers).
+constexpr int kFlagLine = 32;                   // words per line
+constexpr int kGroupFlagWords = 8 * kFlagLine;  // 32 flags
+__device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int f) { return base + (f >> 2) * kFlagLine + (f & 3); }
+
 // wait until all four consecutive flags (16-byte aligned) reach `target`,
 // polling them with one acquire vector load per round trip
 __device__ __forceinline__ void wait_flags4(const uint32_t* flags4, uint32_t target) {
@@ -143,7 +105,7 @@ __device__ __forceinline__ void wait_flag_cached(FlagCache& c, const uint32_t* f
       const uint32_t x = (idx & 3) == 0 ? c.v.x : (idx & 3) == 1 ? c.v.y : (idx & 3) == 2 ? c.v.z : c.v.w;
       if (x >= target) return;
     }
-    c.v = ld_acquire_gpu_v4(flags + base);
+    c.v = ld_acquire_gpu_v4(flags + (base >> 2) * kFlagLine);
     c.base = base;
   }
 }
@@ -215,9 +177,9 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
   uint64_t* full = reinterpret_cast<uint64_t*>(sA + kStagesF * kTileA);
   uint64_t* empty = full + kStagesF;
   uint64_t* wbar = empty + kStagesF;
-  uint64_t* tfull = wbar + 1;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tfull = wbar + 1;    // [2] double-buffered accumulators: step s uses buffer s & 1
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int ublk = blockIdx.x % kUb;
@@ -225,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
   const int dir = blockIdx.x / (kUb * P.n_btile);
   const int crank = (int)cluster_ctarank();  // == ublk % kCl
   const uint16_t all = (uint16_t)((1u << kCl) - 1);
-  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * 32;
+  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kGroupFlagWords;
   const int T = P.T, B = P.B;
   const int brow0 = P.b0 + btile * 128;
 
@@ -235,11 +197,13 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
       mbar_init(&empty[i], kCl);  // one multicast commit per cluster CTA
     }
     mbar_init(wbar, 1);
-    mbar_init(tfull, 1);
-    mbar_init(tempty, kEpiThreads);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiThreads);
+    }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, kR);
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * kR);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -265,11 +229,11 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
             if (s > 0) {  // chunk kb = units kb*64 .. +64 <- unit blocks kb*64/kU ..
               constexpr int kPer = 64 / kU;
               if (kPer == 4) {
-                wait_flags4(flags + 4 * kb, (uint32_t)s);  // acquire included
+                wait_flags4(flag_at(flags, 4 * kb), (uint32_t)s);  // acquire included
               } else {
 #pragma unroll
-                for (int u = 0; u < kPer; ++u) wait_flag(flags + kPer * kb + u, (uint32_t)s);
-                (void)ld_acquire_gpu(flags + kPer * kb + kPer - 1);
+                for (int u = 0; u < kPer; ++u) wait_flag(flag_at(flags, kPer * kb + u), (uint32_t)s);
+                (void)ld_acquire_gpu(flag_at(flags, kPer * kb + kPer - 1));
               }
               fence_proxy_async_global();
             }
@@ -293,8 +257,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
     int stage = 0;
     uint32_t phase = 0;
     for (int s = 0; s < T; ++s) {
-      mbar_wait(tempty, (s & 1) ^ 1);
+      const int acc = s & 1;
+      mbar_wait(&tempty[acc], ((s >> 1) & 1) ^ 1);
       tc_fence_after();
+      const uint32_t dacc = tmem + acc * kR;
       for (int kb = 0; kb < kH / 64; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -306,10 +272,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
           for (int k = 0; k < 4; ++k) {
             uint64_t ad = smem_desc_sw128(abase + k * 32, 16, 1024);
             uint64_t bd = smem_desc_sw128(wbase + kb * kR * 128 + k * 32, 16, 1024);
-            mma_bf16_ss(tmem, ad, bd, idesc, (kb | k) != 0);
+            mma_bf16_ss(dacc, ad, bd, idesc, (kb | k) != 0);
           }
           mma_commit_mc(&empty[stage], all);
-          if (kb == kH / 64 - 1) mma_commit(tfull);
+          if (kb == kH / 64 - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == kStagesF) {
@@ -324,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
       named_bar_sync(kPubBar, kEpiThreads + 32);
       if (lane == 0) {
         trace_mark(P.trace, T, s, 5);
-        st_release_gpu(flags + ublk, (uint32_t)(s + 1));
+        st_release_gpu(flag_at(flags, ublk), (uint32_t)(s + 1));
         trace_mark(P.trace, T, s, 4);
       }
       __syncwarp();
@@ -353,15 +319,15 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
 #pragma unroll
         for (int j = 0; j < kUT / 2; ++j) gpre[j] = reinterpret_cast<const uint4*>(grow)[j];
       }
-      mbar_wait(tfull, s & 1);
+      mbar_wait(&tfull[s & 1], (s >> 1) & 1);
       tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
       float v[4 * kUT];
 #pragma unroll
-      for (int c = 0; c < 4 * kUT; c += 32) tmem_ld32(tcol + c, v + c);
+      for (int c = 0; c < 4 * kUT; c += 32) tmem_ld32(tcol + (s & 1) * kR + c, v + c);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(tempty);
+      mbar_arrive(&tempty[s & 1]);
       float hv[kUT], cv[kUT];
       uint4 actp[kUT / 2];
 #pragma unroll
@@ -409,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
   __syncthreads();
   cluster_sync_all();  // no CTA exits while peers may still multicast into it
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, kR);
+  if (warp == 2) tmem_dealloc(tmem, 2 * kR);
 }
 
 // ============================================================================
@@ -431,11 +397,14 @@ constexpr int kGU = 64;                      // units per cluster
 constexpr int kFU = kGU / kKS;               // 16 units finalised per CTA
 constexpr int kKSlice = 4 * kH / kKS;        // 512 gate rows per CTA
 constexpr int kChunks = kKSlice / 64;        // 8 A chunks per step
-constexpr int kStagesB = 8;
+constexpr int kStagesB = 6;
 constexpr int kWBytesB = kGU * kKSlice * 2;  // 64 KB
 constexpr int kRecvSlot = 128 * kFU * 4;     // 8 KB: one source's [128 rows x 16 units] fp32
 constexpr int kRecvBytes = kKS * kRecvSlot;  // 4 sources
-constexpr size_t kSmem = 1024 + kWBytesB + kStagesB * kTileA + kRecvBytes + 512;
+constexpr int kSendBytes = (kKS - 1) * kRecvSlot;  // staged partials for the 3 peers
+constexpr size_t kSmem = 1024 + kWBytesB + kStagesB * kTileA + kRecvBytes + kSendBytes + 512;
+// [128 rows][16 fp32] slots, 16-byte chunk c of row r stored at chunk c ^ ((r >> 1) & 3)
+__device__ __forceinline__ uint32_t slot_off(int r, int c) { return (uint32_t)(r * 64 + 16 * (c ^ ((r >> 1) & 3))); }
 }  // namespace bwd
 
 __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_constant__ LstmParams P) {
@@ -444,14 +413,15 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = sm;
   uint8_t* sA = sW + kWBytesB;
-  float* recv = reinterpret_cast<float*>(sA + kStagesB * kTileA);  // [kKS][128][16]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(recv) + kRecvBytes);
+  float* recv = reinterpret_cast<float*>(sA + kStagesB * kTileA);  // [kKS][128][16] (swizzled rows)
+  uint8_t* send = reinterpret_cast<uint8_t*>(recv) + kRecvBytes;    // [kKS-1][128][16]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(send + kSendBytes);
   uint64_t* full = bars;
   uint64_t* empty = full + kStagesB;
   uint64_t* wbar = empty + kStagesB;
-  uint64_t* tfull = wbar + 1;
-  uint64_t* tempty = tfull + 1;
-  uint64_t* rfull = tempty + 1;  // recv buffer complete (all 4 sources)
+  uint64_t* tfull = wbar + 1;    // [2] double-buffered accumulators: MMA iteration i = s-1 uses i & 1
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rfull = tempty + 2;  // recv buffer complete (all 4 sources)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -463,8 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   const int ug = (blockIdx.x / kKS) % (kH / kGU);
   const int btile = (blockIdx.x / (kKS * (kH / kGU))) % P.n_btile;
   const int dir = blockIdx.x / (kKS * (kH / kGU) * P.n_btile);
-  constexpr int kFlagsPerGroup = 4 * kH / 64;  // 32 chunks per (dir, btile)
-  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kFlagsPerGroup;
+  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kGroupFlagWords;
   const int T = P.T, B = P.B;
   const int brow0 = P.b0 + btile * 128;
   const int my_chunk = ug * kKS + ks;
@@ -475,12 +444,14 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       mbar_init(&empty[i], kMulticastB ? 2 : 1);  // both CTAs of a multicast pair free the stage
     }
     mbar_init(wbar, 1);
-    mbar_init(tfull, 1);
-    mbar_init(tempty, kEpiThreads);
-    mbar_init(rfull, kKS * 4);  // 4 source CTAs x 4 writer warps
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiThreads);
+    }
+    mbar_init(rfull, 1);  // local expect_tx arrive; peers complete 3 x 8 KB of tx
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 64);
+  if (warp == 2) tmem_alloc(tmem_slot, 128);
   tc_fence_before();
   cluster_sync_all();  // peers' barriers initialised before any remote arrive
   tc_fence_after();
@@ -507,15 +478,17 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
           mbar_arrive_expect_tx(&full[stage], kTileA);
           if (kMulticastB) {  // the pair alternates chunks; multicast to both
             if ((j & 1) == upair) {
-              wait_flag(flags + chunk, (uint32_t)s);
-              acquire_for_tma(flags + chunk, P.variant);
+              wait_flag(flag_at(flags, chunk), (uint32_t)s);
+              acquire_for_tma(flag_at(flags, chunk), P.variant);
               tma_load_2d_mc(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow,
                              pair_mask);
             }
           } else {
             wait_flag_cached(fc, flags, chunk, (uint32_t)s);  // acquire vector poll
-            fence_proxy_async_global();
+            if (!(P.variant & 128)) fence_proxy_async_global();
             tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
+            if (P.trace && blockIdx.x == 0)
+              P.trace[(size_t)gridDim.x * T * kTraceSlots + ((size_t)s * 8 + j) * 2] = globaltimer();
           }
           if (j == 0) trace_mark(P.trace, T, s, 0);
           if (++stage == kStagesB) {
@@ -533,24 +506,28 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
     int stage = 0;
     uint32_t phase = 0;
     for (int s = 1; s < T; ++s) {
-      mbar_wait(tempty, ((s - 1) & 1) ^ 1);
+      const int it = s - 1, acc = it & 1;
+      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
+      const uint32_t dacc = tmem + acc * kGU;
       for (int j = 0; j < kChunks; ++j) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (P.trace && blockIdx.x == 0 && lane == 0)
+          P.trace[(size_t)gridDim.x * T * kTraceSlots + ((size_t)s * 8 + j) * 2 + 1] = globaltimer();
         if (elect_one()) {
           const uint32_t abase = smem_u32(sA + stage * kTileA);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             uint64_t ad = smem_desc_sw128(abase + k * 32, 16, 1024);
             uint64_t bd = smem_desc_sw128(wbase + j * kGU * 128 + k * 32, 16, 1024);
-            mma_bf16_ss(tmem, ad, bd, idesc, (j | k) != 0);
+            mma_bf16_ss(dacc, ad, bd, idesc, (j | k) != 0);
           }
           if (kMulticastB)
             mma_commit_mc(&empty[stage], pair_mask);
           else
             mma_commit(&empty[stage]);
-          if (j == kChunks - 1) mma_commit(tfull);
+          if (j == kChunks - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == kStagesB) {
@@ -607,41 +584,54 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       // the finalisers we feed must have consumed the previous exchange
       // (checked before the MMA wait so the L2 round trip overlaps it)
       if (s >= 2 && lane == 0) {  // the finalisers 4ug .. 4ug+3 (one vector poll)
-        wait_flags4(flags + ug * kKS, (uint32_t)s);
+        wait_flags4(flag_at(flags, ug * kKS), (uint32_t)s);
       }
       __syncwarp();
       if (s > 0) {
-        mbar_wait(tfull, (s - 1) & 1);
+        const int it = s - 1;
+        mbar_wait(&tfull[it & 1], (it >> 1) & 1);
         tc_fence_after();
         if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
         float v[32];
-        tmem_ld32(tcol, v);
+        tmem_ld32(tcol + (it & 1) * kGU, v);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(tempty);
+        mbar_arrive(&tempty[it & 1]);
+        const bool issuer = (threadIdx.x == kEpiWarp0 * 32);
+        if (issuer && s >= 2) bulk_wait_read0();  // last step's copies have read `send`
+        named_bar_sync(3, kEpiThreads);
+        // my partial for finalisers 2hf, 2hf+1: own slot in recv, peers' in send
 #pragma unroll
         for (int f2 = 0; f2 < 2; ++f2) {
           const int f = 2 * hf + f2;
-          const uint32_t local = recv_base + (uint32_t)((ks * 128 + r) * kFU * 4);
-          const uint32_t dst = mapa_shared(local, rbase + (uint32_t)f);
+          uint8_t* slot = f == ks ? reinterpret_cast<uint8_t*>(recv) + ks * kRecvSlot
+                                  : send + (f < ks ? f : f - 1) * kRecvSlot;
 #pragma unroll
-          for (int i = 0; i < kFU; i += 4)
-            st_cluster_v4(dst + i * 4, v[f2 * kFU + i], v[f2 * kFU + i + 1], v[f2 * kFU + i + 2],
-                          v[f2 * kFU + i + 3]);
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<float4*>(slot + slot_off(r, c)) =
+                make_float4(v[f2 * kFU + 4 * c], v[f2 * kFU + 4 * c + 1], v[f2 * kFU + 4 * c + 2],
+                            v[f2 * kFU + 4 * c + 3]);
         }
-        __syncwarp();
-        if (lane == 0) {
-#pragma unroll
-          for (int f2 = 0; f2 < 2; ++f2)
-            mbar_arrive_remote_release(mapa_shared(smem_u32(rfull), rbase + (uint32_t)(2 * hf + f2)));
+        fence_proxy_async_smem();
+        named_bar_sync(3, kEpiThreads);
+        if (issuer) {
+          for (int f = 0; f < kKS; ++f) {
+            if (f == ks) continue;
+            const uint32_t peer = rbase + (uint32_t)f;
+            const uint32_t dst = mapa_shared(smem_u32(reinterpret_cast<uint8_t*>(recv) + ks * kRecvSlot), peer);
+            bulk_copy_s2cluster(dst, send + (f < ks ? f : f - 1) * kRecvSlot, kRecvSlot,
+                                mapa_shared(smem_u32(rfull), peer));
+          }
+          bulk_commit();
+          mbar_arrive_expect_tx(rfull, (kKS - 1) * kRecvSlot);
         }
-        mbar_wait_acq_cluster(rfull, (s - 1) & 1);
+        mbar_wait(rfull, (s - 1) & 1);
         if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 5);
-        const float* rb = recv;
+        const uint8_t* rb = reinterpret_cast<const uint8_t*>(recv);
 #pragma unroll
         for (int src = 0; src < kKS; ++src) {
-          const float4* p4 = reinterpret_cast<const float4*>(rb + ((size_t)src * 128 + r) * kFU + hf * 8);
-          const float4 x0 = p4[0], x1 = p4[1];
+          const float4 x0 = *reinterpret_cast<const float4*>(rb + src * kRecvSlot + slot_off(r, 2 * hf));
+          const float4 x1 = *reinterpret_cast<const float4*>(rb + src * kRecvSlot + slot_off(r, 2 * hf + 1));
           dh[0] += x0.x; dh[1] += x0.y; dh[2] += x0.z; dh[3] += x0.w;
           dh[4] += x1.x; dh[5] += x1.y; dh[6] += x1.z; dh[7] += x1.w;
         }
@@ -677,9 +667,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         }
       }
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
-      publish(flags + my_chunk, (uint32_t)(s + 1), P.variant);
+      publish(flag_at(flags, my_chunk), (uint32_t)(s + 1), P.variant);
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 4);
     }
+    if (threadIdx.x == kEpiWarp0 * 32) bulk_wait0();  // outgoing exchange copies complete
     if (P.dbpart) {  // fused bias gradient: sum over this warp's 32 batch rows and all steps
       const float cs = warp_colsum32(dbacc);
       P.dbpart[((size_t)(P.b0 / 128 + btile) * 4 + q) * (8 * kH) + col_g + lane] = cs;
@@ -690,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   __syncthreads();
   cluster_sync_all();  // no CTA leaves while a peer may still touch its smem
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 64);
+  if (warp == 2) tmem_dealloc(tmem, 128);
 }
 
 }  // namespace
@@ -734,7 +725,7 @@ static int fwd_units() {
 }
 int lstm_max_tiles() { return num_sms() / (2 * (kH / fwd_units())); }
 static int lstm_bwd_max_tiles() { return (num_sms() >= 132 ? 128 : num_sms()) / 64; }
-int lstm_counter_words(int B) { return 2 * 32 * ((B + 127) / 128); }
+int lstm_counter_words(int B) { return 2 * kGroupFlagWords * ((B + 127) / 128); }
 
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
@@ -785,8 +776,8 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.b0 = b0;
     P.nb = nb;
     P.n_btile = (nb + 127) / 128;
-    P.counters = a.counters + (b0 / 128) * 2 * 32;
-    DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * 32 * P.n_btile, stream));
+    P.counters = a.counters + (b0 / 128) * 2 * kGroupFlagWords;
+    DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * kGroupFlagWords * P.n_btile, stream));
     if (fwd)
       rc = fwd_units() == 16
                ? launch_coop((const void*)lstm_fwd_kernel<16>, 2 * fwd::Cfg<16>::kUb * P.n_btile, P, stream,

@@ -118,7 +118,7 @@ def test_lstm_recurrent_fwd_bwd(B, T):
     gates = G.clone()
     cstate = torch.zeros(N, 2 * H, device=DEV)
     yfull = torch.zeros((T + 2) * B, 2 * H, device=DEV, dtype=torch.bfloat16)
-    counters = torch.zeros(1024, device=DEV, dtype=torch.int32)
+    counters = torch.zeros(16384, device=DEV, dtype=torch.int32)
     rc = lib.ds_debug_lstm_fwd(B, T, gates.data_ptr(), cstate.data_ptr(), yfull.data_ptr(), W.data_ptr(),
                                counters.data_ptr(), None, _lib.stream_ptr())
     _lib.check(rc, "lstm_fwd")

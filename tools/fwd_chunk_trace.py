@@ -17,7 +17,7 @@ W = (torch.randn(8 * H, H, device="cuda") * 0.05).bfloat16()
 gates = G.clone()
 cstate = torch.zeros(N, 2 * H, device="cuda")
 yfull = torch.zeros((T + 2) * B, 2 * H, device="cuda", dtype=torch.bfloat16)
-counters = torch.zeros(4096, device="cuda", dtype=torch.int32)
+counters = torch.zeros(16384, device="cuda", dtype=torch.int32)
 grid = 128
 tr = torch.zeros(grid * T * 6 + T * 8 * 2, device="cuda", dtype=torch.int64)
 s = _lib.stream_ptr()

@@ -22,7 +22,7 @@ WT = torch.cat([W[:4 * H].t(), W[4 * H:].t()], 0).contiguous()
 gates = G.clone()
 cstate = torch.zeros(N, 2 * H, device=dev)
 yfull = torch.zeros((T + 2) * B, 2 * H, device=dev, dtype=torch.bfloat16)
-counters = torch.zeros(4096, device=dev, dtype=torch.int32)
+counters = torch.zeros(16384, device=dev, dtype=torch.int32)
 dY = torch.randn(N, 2 * H, device=dev).bfloat16()
 dg = torch.zeros(N, 8 * H, device=dev, dtype=torch.bfloat16)
 ntile = (B + 127) // 128
