@@ -268,7 +268,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
-    TRY(op_rowsum(h->biaspart, p.tiles_m * 4, C, grad + L.off_bo, s));
+    TRY(op_rowsum(h->biaspart, ((N + kGemmBM - 1) / kGemmBM) * 4, C, grad + L.off_bo, s));
     nl += 2;
     MARK(PH_GEMM);
   }

@@ -8,13 +8,20 @@
 // whose epilogue computes soft-max statistics (forward) or
 // (softmax - onehot)/N (backward) without ever materialising fp32 logits.
 //
-// Structure (one CTA per SM, 640 threads):
-//   warp 0      : TMA producer (one elected lane), 4-stage smem ring
-//   warp 1      : tcgen05.mma issuer (one elected lane)
-//   warp 2      : TMEM allocator (512 columns = 2 x 128x256 fp32 accumulators)
-//   warps 4..19 : epilogue, thread = accumulator row (TMEM lane); warp 4+e
-//                 takes lane quadrant e%4 and columns 64*(e/4) .. +64
-// Tiles are walked round-robin over the persistent grid; the two TMEM
+// Structure: CTA pairs (2-CTA clusters, tcgen05 cta_group::2), one CTA per
+// SM, 640 threads.  A pair owns a 256 x 256 output tile: CTA rank r stages
+// rows r*128.. of the A tile and rows r*128.. of the B tile (K-block 64), so
+// each SM streams 32 KB per k-block instead of 48 KB and the tensor cores of
+// both SMs read the B halves of both (M=256 N=256 K=16 pair MMA).
+//   warp 0      : TMA producer (one elected lane, both CTAs), 6-stage ring;
+//                 byte counts complete on the leader's (rank 0) barrier
+//   warp 1      : tcgen05.mma issuer (leader CTA only, one elected lane)
+//   warp 2      : TMEM allocator (512 columns = 2 x 128x256 fp32 accumulators
+//                 per CTA, mirrored in the pair)
+//   warps 4..19 : epilogue of the CTA's 128 rows, thread = accumulator row
+//                 (TMEM lane); warp 4+e takes lane quadrant e%4 and columns
+//                 64*(e/4) .. +64
+// Pair tiles are walked round-robin over the persistent grid; the two TMEM
 // accumulators let the epilogue of tile i overlap the main loop of tile i+1.
 #include "ds_internal.h"
 #include "ds_ptx.cuh"
@@ -24,9 +31,11 @@ namespace ds {
 namespace {
 
 constexpr int BM = kGemmBM, BN = kGemmBN, BK = kGemmBK;
-constexpr int kStages = 4;
-constexpr int kABytes = BM * BK * 2;  // 16 KB
-constexpr int kBBytes = BN * BK * 2;  // 32 KB
+constexpr int kStages = 6;
+constexpr int kPairM = 2 * BM;             // rows of a pair tile
+constexpr int kBHalf = BN / 2;             // B rows staged per CTA
+constexpr int kABytes = BM * BK * 2;       // 16 KB
+constexpr int kBBytes = kBHalf * BK * 2;   // 16 KB
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 640;  // warps 0-3 roles, 4-19 epilogue (4 lane quadrants x 4 column quarters)
 constexpr int kEpiWarp0 = 4;
@@ -112,6 +121,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  const uint32_t crank = cluster_ctarank();  // 0 = leader (issues the pair MMAs)
+  const bool leader = crank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < batch.nprob; ++i) {
@@ -126,13 +138,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 512);
+      mbar_init(&tempty[a], 2 * kEpiWarps);  // every epilogue warp of both CTAs drained it
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / complete_tx
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -140,32 +152,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   if (warp == 0) {
     if (elect_one()) {
-      // ---------------- TMA producer ----------------
+      // ---------------- TMA producer (both CTAs) ----------------
+      const uint32_t full_c = mapa_shared(smem_u32(full), 0);  // leader's full[0]
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      for (int tile = pair; tile < total; tile += npairs) {
         TileCoord tc = locate(batch, tile);
         const GemmProblem& P = batch.p[tc.prob];
-        const int m0 = tc.tm * BM, n0 = tc.tn * BN;
+        const int m0 = tc.tm * kPairM + (int)crank * BM, n0 = tc.tn * BN + (int)crank * kBHalf;
         int kb0, kb1;
         kb_range(P, tc.ks, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1);  // the pair MMA that read this stage (both CTAs) is done
           uint8_t* sA = smem + stage * kStageBytes;
           uint8_t* sB = sA + kABytes;
-          mbar_arrive_expect_tx(&full[stage], kStageBytes);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          const uint32_t bar = full_c + stage * 8;
           const int k0 = kb * BK;
           if (!P.a_mn) {
-            tma_load_2d(sA, &P.tmA, &full[stage], k0, m0);
+            tma_load_2d_pair(sA, &P.tmA, bar, k0, m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sA + j * 8192, &P.tmA, &full[stage], m0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sA + j * 8192, &P.tmA, bar, m0 + 64 * j, k0);
           }
           if (!P.b_mn) {
-            tma_load_2d(sB, &P.tmB, &full[stage], k0, n0);
+            tma_load_2d_pair(sB, &P.tmB, bar, k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, &P.tmB, &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < kBHalf / 64; ++j) tma_load_2d_pair(sB + j * 8192, &P.tmB, bar, n0 + 64 * j, k0);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -175,42 +189,44 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-      TileCoord tc = locate(batch, tile);
-      const GemmProblem& P = batch.p[tc.prob];
-      int kb0, kb1;
-      kb_range(P, tc.ks, kb0, kb1);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      const uint32_t idesc = idesc_bf16_f32(BM, BN, P.a_mn, P.b_mn);
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
+    // ---------------- MMA issuer (leader CTA) ----------------
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = pair; tile < total; tile += npairs, ++it) {
+        TileCoord tc = locate(batch, tile);
+        const GemmProblem& P = batch.p[tc.prob];
+        int kb0, kb1;
+        kb_range(P, tc.ks, kb0, kb1);
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        const uint32_t idesc = idesc_bf16_f32(kPairM, BN, P.a_mn, P.b_mn);
+        mbar_wait_acq_cluster(&tempty[acc], acc_phase ^ 1);  // both CTAs' epilogues drained it
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t aBase = smem_u32(smem + stage * kStageBytes);
-          const uint32_t bBase = aBase + kABytes;
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t aBase = smem_u32(smem + stage * kStageBytes);
+            const uint32_t bBase = aBase + kABytes;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t ad = P.a_mn ? smem_desc_sw128(aBase + k * 2048, 8192, 1024)
-                                 : smem_desc_sw128(aBase + k * 32, 16, 1024);
-            uint64_t bd = P.b_mn ? smem_desc_sw128(bBase + k * 2048, 8192, 1024)
-                                 : smem_desc_sw128(bBase + k * 32, 16, 1024);
-            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
+            for (int k = 0; k < BK / 16; ++k) {
+              uint64_t ad = P.a_mn ? smem_desc_sw128(aBase + k * 2048, 8192, 1024)
+                                   : smem_desc_sw128(aBase + k * 32, 16, 1024);
+              uint64_t bd = P.b_mn ? smem_desc_sw128(bBase + k * 2048, 8192, 1024)
+                                   : smem_desc_sw128(bBase + k * 32, 16, 1024);
+              mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
+            }
+            mma_commit_pair_mc(&empty[stage], 0x3);
+            if (kb == kb1 - 1) mma_commit_pair_mc(&tfull[acc], 0x3);
           }
-          mma_commit(&empty[stage]);
-          if (kb == kb1 - 1) mma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1;
+          __syncwarp();
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -221,10 +237,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const uint32_t part = e >> 2; // column quarter of the 256-wide tile
     constexpr int kCols = BN / 4; // 64 columns per thread
     constexpr float kLog2e = 1.4426950408889634f;
+    const uint32_t tempty_c = mapa_shared(smem_u32(tempty), 0);
     int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+    for (int tile = pair; tile < total; tile += npairs, ++it) {
       TileCoord tc = locate(batch, tile);
       const GemmProblem& P = batch.p[tc.prob];
+      const int rt = tc.tm * 2 + (int)crank;  // 128-row tile of this CTA
       // problem fields into registers once per tile (P is indexed dynamically)
       const int epi = P.epi, n_valid = P.n_valid;
       const float* __restrict__ bias = P.bias;
@@ -232,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const long long ldo = P.ldo;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int row = tc.tm * BM + q * 32 + lane;
+      const int row = rt * BM + q * 32 + lane;
       const int n0 = tc.tn * BN + part * kCols;
       const bool row_ok = row < P.m_valid;
       const bool full_cols = n0 + kCols <= n_valid;
@@ -331,14 +349,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] *= sc;
           if (P.c_tma) {
-            store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, tc.tm * BM + q * 32);
+            store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, rt * BM + q * 32);
           } else if (row_ok) {
             store_bf16x16(orow + nb, v);
             store_bf16x16(orow + nb + 16, v + 16);
           }
-          if (colpart) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
+          if (colpart && rt * BM < P.m_valid) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
             const float cs = warp_colsum32(v);
-            colpart[(size_t)(tc.tm * 4 + q) * n_valid + nb + lane] = cs;
+            colpart[(size_t)(rt * 4 + q) * n_valid + nb + lane] = cs;
           }
         }
       } else if (epi == EPI_BF16) {
@@ -361,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             }
           }
           if (P.c_tma) {
-            store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, tc.tm * BM + q * 32);
+            store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, rt * BM + q * 32);
           } else if (row_ok) {
             store_bf16x16(orow + nb, v);
             if (nb + 16 < n_valid) store_bf16x16(orow + nb + 16, v + 16);
@@ -397,15 +415,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tempty[acc]);
+        else
+          mbar_arrive_remote_release(tempty_c + acc * 8);
+      }
     }
     if (lane == 0) bulk_wait0();  // staged output stores complete before exit
   }
 
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // neither CTA leaves (or frees TMEM) while the pair is still working
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
+  if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
 }
 
 }  // namespace
@@ -421,7 +446,7 @@ int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const v
     rc = make_tmap_2d(&p->tmA, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, M, K, (uint64_t)lda * 2, 64, 64);
   if (rc) return rc;
   if (!b_mn)
-    rc = make_tmap_2d(&p->tmB, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, K, N, (uint64_t)ldb * 2, 64, BN);
+    rc = make_tmap_2d(&p->tmB, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, K, N, (uint64_t)ldb * 2, 64, kBHalf);
   else
     rc = make_tmap_2d(&p->tmB, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, N, K, (uint64_t)ldb * 2, 64, 64);
   if (rc) return rc;
@@ -430,7 +455,7 @@ int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const v
   p->K = K;
   p->a_mn = a_mn;
   p->b_mn = b_mn;
-  p->tiles_m = (M + BM - 1) / BM;
+  p->tiles_m = (M + kPairM - 1) / kPairM;  // pair tiles
   p->tiles_n = (N + BN - 1) / BN;
   p->n_valid = N;
   p->m_valid = M;
@@ -466,9 +491,21 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   }
   b->total_tiles = total;
   if (total == 0) return DS_OK;
-  int grid = total < num_sms() ? total : num_sms();
-  gemm_kernel<<<grid, kThreads, kSmemBytes, stream>>>(*b);
-  DS_CUDA_TRY(cudaGetLastError());
+  const int max_pairs = num_sms() / 2;
+  const int pairs = total < max_pairs ? total : max_pairs;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel, *b));
   return DS_OK;
 }
 
