@@ -126,12 +126,13 @@ int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, 
                        int64_t ldc, int32_t M, int32_t N, int32_t K, ds_stream_t stream);
 
 /* Recurrent-kernel self-test hooks (tests only): run one bidirectional layer's
- * forward / backward recurrence on caller buffers (layouts of lstm_rec.cu).
+ * forward / backward recurrence on caller buffers (layouts of lstm_rec.cu;
+ * whh = W_hh bf16 [4096, 512] for both directions of recurrence).
  * counters: >= 512*ceil(B/128) words; trace (nullable): [grid][T][4] u64
  * globaltimer marks (producer ready, loads issued, MMA done, step published). */
 int ds_debug_lstm_fwd(int32_t B, int32_t T, void* gates, float* cstate, void* y_full, const void* whh,
                       uint32_t* counters, uint64_t* trace, ds_stream_t stream);
-int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* cstate, const void* whhT, const void* dy,
+int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* cstate, const void* whh, const void* dy,
                       void* dg, uint32_t* counters, uint64_t* trace, ds_stream_t stream);
 
 const char* ds_last_error(void);

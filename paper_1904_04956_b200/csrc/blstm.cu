@@ -29,10 +29,8 @@ struct ds_blstm {
   void* arena = nullptr;
   // operand snapshot
   __nv_bfloat16* snap = nullptr;
-  __nv_bfloat16* whhT = nullptr;
   __nv_bfloat16* wih0pad = nullptr;
   float* bias_snap = nullptr;
-  int64_t* d_whh_offs = nullptr;
   // activations
   __nv_bfloat16* x0 = nullptr;
   int32_t* lab = nullptr;
@@ -88,6 +86,19 @@ int dz_split(int classes) {
   return (nkb % kDzSplit == 0 && nkb >= 4 * kDzSplit) ? kDzSplit : 1;
 }
 
+// dW_b = dZ^T Y is 256 x 1024 with K = frames: 4 pair tiles of 84 k-blocks at
+// B=256, so split K to spread it over the pairs that run the dY tiles.
+constexpr int kWbSplit = 12;
+// largest S <= target whose ceil-split leaves no split empty
+int ksplit_for(int K, int target) {
+  const int nkb = (K + kGemmBK - 1) / kGemmBK;
+  for (int S = target < nkb ? target : nkb; S > 1; --S) {
+    const int per = (nkb + S - 1) / S;
+    if ((S - 1) * per < nkb) return S;
+  }
+  return 1;
+}
+
 struct Arena {
   size_t off = 0;
   template <class T>
@@ -104,10 +115,8 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   const ModelLayout& L = h->L;
   const int64_t N = h->Nmax;
   h->snap = a.take<__nv_bfloat16>(base, L.total);
-  h->whhT = a.take<__nv_bfloat16>(base, (size_t)L.layers * kGates2 * kHidden);
   h->wih0pad = a.take<__nv_bfloat16>(base, (size_t)kGates2 * kInPad);
   h->bias_snap = a.take<float>(base, (size_t)L.layers * kGates2 + L.bottleneck + L.classes);
-  h->d_whh_offs = a.take<int64_t>(base, L.layers);
   h->x0 = a.take<__nv_bfloat16>(base, (size_t)N * kInPad);
   h->lab = a.take<int32_t>(base, N);
   h->gates.resize(L.layers);
@@ -126,15 +135,20 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   h->dz = a.take<__nv_bfloat16>(base, (size_t)N * L.bottleneck);
   h->dy = a.take<__nv_bfloat16>(base, (size_t)N * kLayerOut);
   h->dg = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
-  int64_t cp = op_colsum_scratch(L.classes > kGates2 ? L.classes : kGates2);
-  h->colpart = a.take<float>(base, cp);
+  {  // bottleneck bias colsum partials / CE loss partials
+    const int64_t c1 = op_colsum_scratch(N, L.bottleneck), c2 = (N + 31) / 32 + 64;
+    h->colpart = a.take<float>(base, c1 > c2 ? c1 : c2);
+  }
   {
     const int64_t tiles_m = (N + kGemmBM - 1) / kGemmBM;
     const int64_t a1 = tiles_m * 4 * L.classes;
     const int64_t a2 = (int64_t)((h->Bmax + 127) / 128) * 4 * kGates2;
     h->biaspart = a.take<float>(base, a1 > a2 ? a1 : a2);
   }
-  h->splitk = a.take<float>(base, (size_t)kDzSplit * N * L.bottleneck);
+  {  // split-K fp32 partials: dZ (K = classes) and dW_b (K = frames)
+    const int64_t s1 = (int64_t)kDzSplit * N * L.bottleneck, s2 = (int64_t)kWbSplit * L.bottleneck * kLayerOut;
+    h->splitk = a.take<float>(base, s1 > s2 ? s1 : s2);
+  }
   h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64);
   *total = a.off + 256;
   return DS_OK;
@@ -307,11 +321,14 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
     gb.nprob = 2;
-    GemmProblem& p0 = gb.p[0];  // dW_b = dZ^T Y
+    GemmProblem& p0 = gb.p[0];  // dW_b = dZ^T Y (split-K fp32 partials, reduced below in split order)
     TRY(gemm_problem(&p0, h->dz, bott, 1, Y(Lh - 1), kLayerOut, 1, bott, kLayerOut, N));
     p0.epi = EPI_F32;
-    p0.out = grad + L.off_wb;
+    const int Sb = ksplit_for(N, kWbSplit);
+    p0.out = Sb > 1 ? h->splitk : grad + L.off_wb;
     p0.ldo = kLayerOut;
+    p0.ksplit = Sb;
+    p0.split_stride = (long long)bott * kLayerOut;
     GemmProblem& p1 = gb.p[1];  // dY = dZ W_b
     TRY(gemm_problem(&p1, h->dz, bott, 0, h->snap + L.off_wb, kLayerOut, 1, N, kLayerOut, bott));
     p1.epi = EPI_BF16;
@@ -321,11 +338,12 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
+    if (Sb > 1) TRY(op_splitk_f32(h->splitk, Sb, (int64_t)bott * kLayerOut, grad + L.off_wb, s));
     TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, s));
-    nl += 3;
+    nl += Sb > 1 ? 4 : 3;
   }
   for (int l = Lh - 1; l >= 0; --l) {
-    LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->whhT + (size_t)l * kGates2 * kHidden, h->dy,
+    LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], h->dy,
                      h->dg, h->counters, nullptr, h->biaspart};
     MARK(PH_LSTM_BWD);
     TRY(lstm_backward(la, s));
@@ -461,10 +479,7 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
     return fail_cuda(e, "cudaMalloc(workspace)");
   }
   carve(h, reinterpret_cast<char*>(h->arena), &total);
-  std::vector<int64_t> offs(h->L.layers);
-  for (int l = 0; l < h->L.layers; ++l) offs[l] = h->L.off_whh[l];
-  e = cudaMemcpy(h->d_whh_offs, offs.data(), sizeof(int64_t) * offs.size(), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(h->counters, 0, sizeof(uint32_t) * 64);
+  e = cudaMemset(h->counters, 0, sizeof(uint32_t) * 64);
   if (e != cudaSuccess) {
     cudaFree(h->arena);
     delete h;
@@ -499,7 +514,7 @@ int ds_blstm_cast_snapshot(ds_blstm* h, const float* theta, ds_stream_t stream) 
   DS_CUDA_TRY(cudaSetDevice(h->device));
   int rc = op_cast(theta, h->L.total, h->snap, s);
   if (rc) return rc;
-  return op_snapshot_aux(theta, h->L, h->d_whh_offs, h->whhT, h->wih0pad, h->bias_snap, s);
+  return op_snapshot_aux(theta, h->L, h->wih0pad, h->bias_snap, s);
 }
 
 int ds_blstm_fwd_bwd(ds_blstm* h, const int64_t* idx, int32_t B, float* grad, float* loss_sum, int32_t* nonfinite,
@@ -522,8 +537,7 @@ int ds_sgd_momentum(float* theta, float* v, const float* g, float lr, float mu, 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int rc = op_sgd(theta, v, g, lr, mu, n, snap_owner ? snap_owner->snap : nullptr, nonfinite, s);
   if (rc || !snap_owner) return rc;
-  return op_snapshot_aux(theta, snap_owner->L, snap_owner->d_whh_offs, snap_owner->whhT, snap_owner->wih0pad,
-                         snap_owner->bias_snap, s);
+  return op_snapshot_aux(theta, snap_owner->L, snap_owner->wih0pad, snap_owner->bias_snap, s);
 }
 
 int ds_adpsgd_mix(float* a, float* b, int64_t n, ds_stream_t stream) {
@@ -620,14 +634,14 @@ int ds_debug_lstm_fwd(int32_t B, int32_t T, void* gates, float* cstate, void* y_
   return lstm_forward(a, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* cstate, const void* whhT, const void* dy,
+int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* cstate, const void* whh, const void* dy,
                       void* dg, uint32_t* counters, uint64_t* trace, ds_stream_t stream) {
   LstmLayerArgs a{B,
                   T,
                   const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(gates)),
                   const_cast<float*>(cstate),
                   nullptr,
-                  reinterpret_cast<const __nv_bfloat16*>(whhT),
+                  reinterpret_cast<const __nv_bfloat16*>(whh),
                   reinterpret_cast<const __nv_bfloat16*>(dy),
                   reinterpret_cast<__nv_bfloat16*>(dg),
                   counters,

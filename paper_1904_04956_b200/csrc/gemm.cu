@@ -484,8 +484,8 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
     GemmProblem& P = b->p[i];
     if (P.ksplit < 1) P.ksplit = 1;
     const int nkb = (P.K + BK - 1) / BK;
-    if (P.ksplit > 1 && (P.epi != EPI_F32 || P.accumulate || nkb % P.ksplit))
-      return fail_arg("split-K needs EPI_F32, no accumulate and an even k-block split");
+    if (P.ksplit > 1 && (P.epi != EPI_F32 || P.accumulate || (P.ksplit - 1) * ((nkb + P.ksplit - 1) / P.ksplit) >= nkb))
+      return fail_arg("split-K needs EPI_F32, no accumulate and no empty split");
     P.tile_begin = total;
     total += P.tiles_m * P.tiles_n * P.ksplit;
   }

@@ -21,7 +21,7 @@
 //   prefetched input projection, applies sigmoid/tanh (MUFU tanh.approx),
 //   updates c (registers) and h, then publishes a per-CTA step flag.
 // Backward CTA (dir, batch tile, unit block of 32):
-//   W_hh^T[dir][unit block] (32 x 2048 bf16, 128 KB) resident.
+//   W_hh[dir][K slice][unit block] resident (MN-major B operand: no transposed copy).
 //   step s: acc[128 batch, 32 units] = dG_prev[128, 2048] . W^T, epilogue adds
 //   dY, runs the cell backward, writes dG_t and publishes its flag.
 // Dataflow instead of a group barrier: the producer of every CTA waits only
@@ -381,7 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
 // ============================================================================
 // Backward: split-K over a 4-CTA cluster.
 //   cluster = (dir, batch tile, unit group ug of 64 units); CTA rank ks holds
-//   W_hh^T[64 units of ug][gate rows ks*512 .. +512] (64 KB) and streams the
+//   W_hh[gate rows ks*512 .. +512][64 units of ug] (64 KB, read as an
+//   MN-major operand straight from the bf16 snapshot) and streams the
 //   matching 512-row K slice of dG_prev (128 KB, all 8 chunks in flight).
 //   Partial dh[128 batch, 64 units] (TMEM) is exchanged through DSMEM: CTA ks
 //   finalises units ug*64 + ks*16 .. +16, runs their cell backward and writes
@@ -462,8 +463,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       tma_prefetch_desc(&P.tmA);
       tma_prefetch_desc(&P.tmW);
       mbar_arrive_expect_tx(wbar, kWBytesB);
-      for (int j = 0; j < kChunks; ++j)
-        tma_load_2d(sW + j * kGU * 128, &P.tmW, wbar, ks * kKSlice + j * 64, dir * kH + ug * kGU);
+      for (int j = 0; j < kChunks; ++j)  // W_hh rows (K) ks*512 + 64j.., units (N) ug*64..: MN-major boxes
+        tma_load_2d(sW + j * 8192, &P.tmW, wbar, ug * kGU, dir * 4 * kH + ks * kKSlice + j * 64);
       int stage = 0;
       uint32_t phase = 0;
       FlagCache fc;
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
     }
   } else if (warp == 1) {
     mbar_wait(wbar, 0);
-    const uint32_t idesc = idesc_bf16_f32(128, kGU, 0, 0);
+    const uint32_t idesc = idesc_bf16_f32(128, kGU, 0, 1);  // B = W_hh slice, MN-major (units contiguous)
     const uint32_t wbase = smem_u32(sW);
     int stage = 0;
     uint32_t phase = 0;
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             uint64_t ad = smem_desc_sw128(abase + k * 32, 16, 1024);
-            uint64_t bd = smem_desc_sw128(wbase + j * kGU * 128 + k * 32, 16, 1024);
+            uint64_t bd = smem_desc_sw128(wbase + j * 8192 + k * 2048, 8192, 1024);
             mma_bf16_ss(dacc, ad, bd, idesc, (j | k) != 0);
           }
           if (kMulticastB)
@@ -754,7 +755,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   } else {
     rc = make_tmap_2d(&P.tmA, a.dg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 8 * kH, (uint64_t)T * B, 8 * kH * 2, 64, 128);
     if (rc) return rc;
-    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4 * kH, 2 * kH, 4 * kH * 2, 64, bwd::kGU);
+    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, bwd::kGU, 64);
     if (rc) return rc;
   }
   P.gates = a.gates;

@@ -9,7 +9,7 @@ namespace ds {
 
 struct LstmParams {
   CUtensorMap tmA;  // forward: Y_full; backward: dG
-  CUtensorMap tmW;  // forward: W_hh [4096, 512]; backward: W_hh^T [1024, 2048]
+  CUtensorMap tmW;  // W_hh [4096, 512] bf16 (forward: K-major B; backward: MN-major B)
   __nv_bfloat16* gates;
   float* cstate;
   __nv_bfloat16* y;
@@ -27,7 +27,7 @@ struct LstmLayerArgs {
   __nv_bfloat16* gates;     // [T*B, 4096]
   float* cstate;            // [T*B, 1024]
   __nv_bfloat16* y_full;    // [(T+2)*B, 1024]
-  const __nv_bfloat16* w;   // forward: W_hh bf16 [4096, 512]; backward: W_hh^T bf16 [1024, 2048]
+  const __nv_bfloat16* w;   // W_hh bf16 [4096, 512] (rows dir*2048 + unit*4 + gate)
   const __nv_bfloat16* dy;  // backward: [T*B, 1024]
   __nv_bfloat16* dg;        // backward: [T*B, 4096]
   uint32_t* counters;       // >= lstm_counter_words(B)

@@ -6,6 +6,7 @@
 // engines/ssgd.py:85-87), column sums for bias gradients and the
 // soft-max/cross-entropy combine.
 #include <cmath>
+#include <cstring>
 
 #include "ds_internal.h"
 #include "ds_ptx.cuh"
@@ -40,32 +41,48 @@ __global__ void gather_kernel(const int64_t* __restrict__ idx, int B, int T, con
 }
 
 // --------------------------------------------------------------------------
-// column sums of a bf16 [rows, ld] matrix, deterministic two-stage.
-constexpr int kColSplit = 32;  // minimum split count (scratch is sized for 32 x the widest matrix)
-inline int colsum_splits(int ncols) {
-  const int cb = (ncols + 255) / 256;
-  int sp = 1024 / cb;
-  sp = sp < kColSplit ? kColSplit : sp;
-  const long long cap = (long long)kColSplit * (ncols > kGates2 ? ncols : kGates2) / ncols;
-  return (int)(sp > cap ? cap : sp);
-}
+// column sums of a bf16 [rows, ld] matrix, deterministic two-stage: block =
+// 128 rows x 256 columns, thread = 8 columns (one 16-byte load per row) x
+// every 8th row; the 8 row lanes are combined in smem in a fixed order.
+constexpr int kColRows = 128;
 __global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int ncols, int64_t ld,
                                       float* __restrict__ part) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  const int split = blockIdx.y;
-  if (col >= ncols) return;
-  const int64_t per = (rows + gridDim.y - 1) / gridDim.y;
-  const int64_t r0 = split * per, r1 = min(rows, r0 + per);
-  float s = 0.f;
-  for (int64_t r = r0; r < r1; ++r) s += __bfloat162float(x[r * ld + col]);
-  part[(int64_t)split * ncols + col] = s;
-}
-__global__ void colsum_final_kernel(const float* __restrict__ part, int ncols, int splits, float* __restrict__ out) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= ncols) return;
-  float s = 0.f;
-  for (int k = 0; k < splits; ++k) s += part[(int64_t)k * ncols + col];
-  out[col] = s;
+  __shared__ float red[8][256 + 8];
+  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;  // 32 column groups of 8, 8 row lanes
+  const int c0 = blockIdx.x * 256 + cg * 8;
+  const int64_t r0 = (int64_t)blockIdx.y * kColRows;
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  if (c0 < ncols) {
+#pragma unroll 4
+    for (int k = 0; k < kColRows / 8; ++k) {
+      const int64_t r = r0 + rl + 8 * k;
+      if (r < rows) {
+        float f[8];
+        const uint4 w = *reinterpret_cast<const uint4*>(x + r * ld + c0);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 t = __bfloat1622float2(h[i]);
+          f[2 * i] = t.x;
+          f[2 * i + 1] = t.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += f[i];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[rl][cg * 8 + i] = acc[i];
+  __syncthreads();
+  const int c = threadIdx.x;  // 256 threads = 256 columns
+  if (blockIdx.x * 256 + c < ncols) {
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += red[k][c];
+    part[(int64_t)blockIdx.y * ncols + blockIdx.x * 256 + c] = sum;
+  }
 }
 
 // out[c] = sum_r part[r][c], rows in order (deterministic)
@@ -94,11 +111,20 @@ __global__ void splitk_bf16_kernel(const float* __restrict__ part, int S, int64_
   }
 }
 
+// split-K finish: out(f32)[i] = sum_s part[s][i] in split order
+__global__ void splitk_f32_kernel(const float* __restrict__ part, int S, int64_t n, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = part[i];
+    for (int k = 1; k < S; ++k) s += part[(int64_t)k * n + i];
+    out[i] = s;
+  }
+}
+
 // --------------------------------------------------------------------------
 // soft-max / CE combine: lse[m] = logsumexp over column-tile (max, sumexp)
 // partials; per-block loss partials, then one ordered sum (deterministic).
-constexpr int kCeRows = 32;  // rows per block (lane = row: coalesced stats reads)
-constexpr int kCeGroups = 8;  // tile groups per block (warps)
+constexpr int kCeRows = 32;   // rows per block (lane = row: coalesced stats reads)
+constexpr int kCeGroups = 16;  // tile groups per block (warps)
 __global__ void ce_rows_kernel(const float2* __restrict__ stats, int ntiles, int64_t ld, const float* __restrict__ tgt,
                                int M, float* __restrict__ lse, float* __restrict__ part) {
   __shared__ float smx[kCeGroups][kCeRows], ssum[kCeGroups][kCeRows];
@@ -106,14 +132,22 @@ __global__ void ce_rows_kernel(const float2* __restrict__ stats, int ntiles, int
   const int m = blockIdx.x * kCeRows + lane;
   float mx = -INFINITY, s = 0.f;
   if (m < M) {
-    for (int j = g; j < ntiles; j += kCeGroups) {  // online combine of this group's tiles
-      const float2 st = stats[j * ld + m];
-      if (!(st.y > 0.f)) continue;  // fully masked column block
-      if (st.x > mx) {
-        s = s * __expf(mx - st.x) + st.y;
-        mx = st.x;
-      } else {
-        s += st.y * __expf(st.x - mx);
+    for (int j0 = g; j0 < ntiles; j0 += 4 * kCeGroups) {  // online combine, four loads in flight
+      float2 st[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * kCeGroups;
+        st[u] = j < ntiles ? stats[j * ld + m] : make_float2(-INFINITY, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (!(st[u].y > 0.f)) continue;  // fully masked column block / past the end
+        if (st[u].x > mx) {
+          s = s * __expf(mx - st[u].x) + st[u].y;
+          mx = st[u].x;
+        } else {
+          s += st[u].y * __expf(st[u].x - mx);
+        }
       }
     }
   }
@@ -201,35 +235,37 @@ __global__ void cast_kernel(const float* __restrict__ theta, int64_t n, __nv_bfl
     snap[i] = __float2bfloat16_rn(theta[i]);
 }
 
-// W_hh^T snapshot: out[l][d][u][r] = W_hh[l][d*2048 + r][u]  (32x32 smem tiles)
-__global__ void whh_transpose_kernel(const float* __restrict__ theta, const int64_t* __restrict__ offs, int layers,
-                                     __nv_bfloat16* __restrict__ out) {
-  __shared__ float tile[32][33];
-  const int l = blockIdx.z;
-  const float* src = theta + offs[l];  // [4096][512]
-  __nv_bfloat16* dst = out + (int64_t)l * kGates2 * kHidden;  // [2][512][2048]
-  const int r0 = blockIdx.y * 32;  // gate row (both dirs, 0..4095)
-  const int u0 = blockIdx.x * 32;  // unit
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) tile[i][threadIdx.x] = src[(int64_t)(r0 + i) * kHidden + u0 + threadIdx.x];
-  __syncthreads();
-  const int d = r0 / kGates, rr0 = r0 % kGates;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y)
-    dst[((int64_t)d * kHidden + u0 + i) * kGates + rr0 + threadIdx.x] = __float2bfloat16_rn(tile[threadIdx.x][i]);
-}
-
-// layer-0 W_ih padded to kInPad columns (TMA needs a 16-byte row pitch)
-__global__ void wih0_pad_kernel(const float* __restrict__ w, int din, __nv_bfloat16* __restrict__ out) {
-  const int64_t total = (int64_t)kGates2 * kInPad;
+// Operand-snapshot extras in one launch: layer-0 W_ih padded to kInPad
+// columns (TMA needs a 16-byte row pitch) followed by the fp32 bias copies
+// [layers][4096], b_b, b_o.  (W_hh is read straight from the bf16 snapshot by
+// both recurrent kernels: no transposed copy.)
+struct AuxOffs {
+  int64_t off_b[kMaxLayers];
+  int64_t off_wih0, off_bb, off_bo;
+  int layers, din, bott, classes;
+};
+__global__ void snapshot_aux_kernel(const float* __restrict__ theta, AuxOffs o, __nv_bfloat16* __restrict__ wpad,
+                                    float* __restrict__ bias) {
+  const int64_t npad = (int64_t)kGates2 * kInPad;
+  const int64_t nb = (int64_t)o.layers * kGates2;
+  const int64_t total = npad + nb + o.bott + o.classes;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / kInPad;
-    const int c = (int)(i % kInPad);
-    out[i] = __float2bfloat16_rn(c < din ? w[r * din + c] : 0.f);
+    if (i < npad) {
+      const int64_t r = i / kInPad;
+      const int c = (int)(i % kInPad);
+      wpad[i] = __float2bfloat16_rn(c < o.din ? theta[o.off_wih0 + r * o.din + c] : 0.f);
+      continue;
+    }
+    const int64_t j = i - npad;
+    int64_t src;
+    if (j < nb)
+      src = o.off_b[j / kGates2] + j % kGates2;
+    else if (j < nb + o.bott)
+      src = o.off_bb + (j - nb);
+    else
+      src = o.off_bo + (j - nb - o.bott);
+    bias[j] = theta[src];
   }
-}
-
-__global__ void copy_f32_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = src[i];
 }
 
 // --------------------------------------------------------------------------
@@ -322,14 +358,20 @@ int op_gather(const int64_t* idx, int B, int T, const __nv_bfloat16* feats, cons
 }
 
 int op_colsum(const __nv_bfloat16* x, int64_t rows, int ncols, int64_t ld, float* part, float* out, cudaStream_t s) {
-  const int sp = colsum_splits(ncols);
+  if ((ncols & 7) || (ld & 7)) return fail_arg("colsum: columns and pitch must be multiples of 8");
+  const int sp = (int)((rows + kColRows - 1) / kColRows);
   dim3 g1((ncols + 255) / 256, sp);
   colsum_partial_kernel<<<g1, 256, 0, s>>>(x, rows, ncols, ld, part);
-  colsum_final_kernel<<<(ncols + 255) / 256, 256, 0, s>>>(part, ncols, sp, out);
+  DS_CUDA_TRY(cudaGetLastError());
+  return op_rowsum(part, sp, ncols, out, s);
+}
+int64_t op_colsum_scratch(int64_t rows, int ncols) { return (rows + kColRows - 1) / kColRows * ncols; }
+
+int op_splitk_f32(const float* part, int S, int64_t n, float* out, cudaStream_t s) {
+  splitk_f32_kernel<<<ew_grid(n), kEW, 0, s>>>(part, S, n, out);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
-int64_t op_colsum_scratch(int ncols) { return (int64_t)kColSplit * ncols; }
 
 int op_splitk_bf16(const float* part, int S, int64_t n, __nv_bfloat16* out, cudaStream_t s) {
   splitk_bf16_kernel<<<ew_grid(n), kEW, 0, s>>>(part, S, n, out);
@@ -367,18 +409,20 @@ int op_cast(const float* theta, int64_t n, __nv_bfloat16* snap, cudaStream_t s) 
   return DS_OK;
 }
 
-int op_snapshot_aux(const float* theta, const ModelLayout& L, const int64_t* d_whh_offs, __nv_bfloat16* whhT,
-                    __nv_bfloat16* wih0pad, float* bias_snap, cudaStream_t s) {
-  dim3 grid(kHidden / 32, kGates2 / 32, L.layers);
-  whh_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(theta, d_whh_offs, L.layers, whhT);
-  wih0_pad_kernel<<<ew_grid((int64_t)kGates2 * kInPad), kEW, 0, s>>>(theta + L.off_wih[0], L.input_dim, wih0pad);
-  // bias snapshot: [layers][4096] then b_b, b_o
-  for (int l = 0; l < L.layers; ++l)
-    copy_f32_kernel<<<ew_grid(kGates2), kEW, 0, s>>>(theta + L.off_b[l], bias_snap + (int64_t)l * kGates2, kGates2);
-  copy_f32_kernel<<<ew_grid(L.bottleneck), kEW, 0, s>>>(theta + L.off_bb, bias_snap + (int64_t)L.layers * kGates2,
-                                                        L.bottleneck);
-  copy_f32_kernel<<<ew_grid(L.classes), kEW, 0, s>>>(
-      theta + L.off_bo, bias_snap + (int64_t)L.layers * kGates2 + L.bottleneck, L.classes);
+int op_snapshot_aux(const float* theta, const ModelLayout& L, __nv_bfloat16* wih0pad, float* bias_snap,
+                    cudaStream_t s) {
+  AuxOffs o;
+  memset(&o, 0, sizeof(o));
+  for (int l = 0; l < L.layers; ++l) o.off_b[l] = L.off_b[l];
+  o.off_wih0 = L.off_wih[0];
+  o.off_bb = L.off_bb;
+  o.off_bo = L.off_bo;
+  o.layers = L.layers;
+  o.din = L.input_dim;
+  o.bott = L.bottleneck;
+  o.classes = L.classes;
+  const int64_t total = (int64_t)kGates2 * kInPad + (int64_t)L.layers * kGates2 + L.bottleneck + L.classes;
+  snapshot_aux_kernel<<<ew_grid(total), kEW, 0, s>>>(theta, o, wih0pad, bias_snap);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }

@@ -12,16 +12,17 @@ constexpr int kMaxGroup = 16;
 int op_gather(const int64_t* idx, int B, int T, const __nv_bfloat16* feats, const int32_t* labels, int64_t n_seq,
               __nv_bfloat16* x0, int32_t* lab, int* flag, cudaStream_t s);
 int op_colsum(const __nv_bfloat16* x, int64_t rows, int ncols, int64_t ld, float* part, float* out, cudaStream_t s);
-int64_t op_colsum_scratch(int ncols);
+int64_t op_colsum_scratch(int64_t rows, int ncols);
 int op_splitk_bf16(const float* part, int S, int64_t n, __nv_bfloat16* out, cudaStream_t s);
+int op_splitk_f32(const float* part, int S, int64_t n, float* out, cudaStream_t s);
 int op_rowsum(const float* part, int nrows, int ncols, float* out, cudaStream_t s);
 int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt, int M, float* lse, float* scratch,
                   float* loss_sum, int* flag, cudaStream_t s);
 int op_sgd(float* theta, float* v, const float* g, float lr, float mu, int64_t n, __nv_bfloat16* snap, int* flag,
            cudaStream_t s);
 int op_cast(const float* theta, int64_t n, __nv_bfloat16* snap, cudaStream_t s);
-int op_snapshot_aux(const float* theta, const ModelLayout& L, const int64_t* d_whh_offs, __nv_bfloat16* whhT,
-                    __nv_bfloat16* wih0pad, float* bias_snap, cudaStream_t s);
+int op_snapshot_aux(const float* theta, const ModelLayout& L, __nv_bfloat16* wih0pad, float* bias_snap,
+                    cudaStream_t s);
 int op_mix(float* a, float* b, int64_t n, cudaStream_t s);
 int op_group_reduce(int world, int rank, float* const* g, float* const* theta, float* const* v,
                     __nv_bfloat16* const* snap, int64_t dim, int nchunks, float lr, float mu, int mode, float divisor,

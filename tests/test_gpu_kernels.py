@@ -133,7 +133,7 @@ def test_lstm_recurrent_fwd_bwd(B, T):
 
     dY = torch.randn(N, 2 * H, device=DEV, generator=g).bfloat16()
     dg = torch.zeros(N, 8 * H, device=DEV, dtype=torch.bfloat16)
-    rc = lib.ds_debug_lstm_bwd(B, T, gates.data_ptr(), cstate.data_ptr(), WT.data_ptr(), dY.data_ptr(),
+    rc = lib.ds_debug_lstm_bwd(B, T, gates.data_ptr(), cstate.data_ptr(), W.data_ptr(), dY.data_ptr(),
                                dg.data_ptr(), counters.data_ptr(), None, _lib.stream_ptr())
     _lib.check(rc, "lstm_bwd")
     torch.cuda.synchronize()

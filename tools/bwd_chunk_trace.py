@@ -23,7 +23,7 @@ grid = 128
 tr = torch.zeros(grid * T * 6 + T * 8 * 2, device="cuda", dtype=torch.int64)
 s = _lib.stream_ptr()
 for i in range(4):
-    _lib.check(lib.ds_debug_lstm_bwd(B, T, gates.data_ptr(), cstate.data_ptr(), WT.data_ptr(), dY.data_ptr(),
+    _lib.check(lib.ds_debug_lstm_bwd(B, T, gates.data_ptr(), cstate.data_ptr(), W.data_ptr(), dY.data_ptr(),
                                      dg.data_ptr(), counters.data_ptr(), tr.data_ptr() if i == 3 else None, s))
 torch.cuda.synchronize()
 a = tr.cpu().numpy().astype(np.float64)

@@ -37,7 +37,7 @@ def fwd(tr=None):
 
 
 def bwd(tr=None):
-    _lib.check(lib.ds_debug_lstm_bwd(B, T, gates.data_ptr(), cstate.data_ptr(), WT.data_ptr(), dY.data_ptr(),
+    _lib.check(lib.ds_debug_lstm_bwd(B, T, gates.data_ptr(), cstate.data_ptr(), W.data_ptr(), dY.data_ptr(),
                                      dg.data_ptr(), counters.data_ptr(), tr, s))
 
 
