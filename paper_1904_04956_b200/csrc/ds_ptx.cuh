@@ -125,6 +125,13 @@ DS_DEV uint4 ld_acquire_gpu_v4(const uint32_t* p) {
                : "memory");
   return v;
 }
+// 32-byte acquire load of eight consecutive flags (one L2 round trip, LDG.256)
+DS_DEV void ld_acquire_gpu_v8(const uint32_t* p, uint32_t* v) {
+  asm volatile("ld.acquire.gpu.global.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p)
+               : "memory");
+}
 DS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 DS_DEV void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

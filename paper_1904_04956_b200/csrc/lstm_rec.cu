@@ -79,11 +79,20 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target)
     }
   }
 }
-// Step flags: 32 per (dir, batch tile) group, four per 128-byte line so the
-// pollers of one line are few (a single hot line serialised ~128 pollers).
+// Step flags: 32 per (dir, batch tile) group in four 32-byte segments, one
+// per 128-byte line (a single hot line serialised ~128 pollers).  Every
+// issuer finds all the flags it needs for a step in ONE segment and polls it
+// with a single 32-byte acquire load per round trip:
+//   forward: flag f = unit block; chunk kb (produced by blocks 4kb..4kb+3
+//     at U=16) has a line of its own, polled with one 16-byte acquire load
+//     (packing chunks r and r+4 into one segment measured slower: 8 writers
+//     per line);
+//   backward: flag c = dG chunk (64 gate rows); K-slice ks streams chunks
+//     8ks..8ks+7 = segment ks.
 constexpr int kFlagLine = 32;                   // words per line
-constexpr int kGroupFlagWords = 8 * kFlagLine;  // 32 flags
-__device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int f) { return base + (f >> 2) * kFlagLine + (f & 3); }
+constexpr int kGroupFlagWords = 8 * kFlagLine;  // 8 lines per group (4 used)
+__device__ __forceinline__ uint32_t* fwd_flag(uint32_t* base, int f) { return base + (f >> 2) * kFlagLine + (f & 3); }
+__device__ __forceinline__ uint32_t* bwd_flag(uint32_t* base, int c) { return base + (c >> 3) * kFlagLine + (c & 7); }
 
 // wait until all four consecutive flags (16-byte aligned) reach `target`,
 // polling them with one acquire vector load per round trip
@@ -93,20 +102,19 @@ __device__ __forceinline__ void wait_flags4(const uint32_t* flags4, uint32_t tar
     if (min(min(v.x, v.y), min(v.z, v.w)) >= target) break;
   }
 }
-// chunk-flag cache for issuers walking consecutive chunk flags
-struct FlagCache {
-  uint4 v;
-  int base;
+// segment cache for an issuer walking the flags of one 32-byte segment
+struct FlagSeg {
+  uint32_t v[8];
 };
-__device__ __forceinline__ void wait_flag_cached(FlagCache& c, const uint32_t* flags, int idx, uint32_t target) {
-  const int base = idx & ~3;
+// wait until flags [pos, pos + n) of the segment reach `target` (n = 1 or 4)
+template <int n>
+__device__ __forceinline__ void wait_seg(FlagSeg& c, const uint32_t* seg, int pos, uint32_t target) {
   while (true) {
-    if (c.base == base) {
-      const uint32_t x = (idx & 3) == 0 ? c.v.x : (idx & 3) == 1 ? c.v.y : (idx & 3) == 2 ? c.v.z : c.v.w;
-      if (x >= target) return;
-    }
-    c.v = ld_acquire_gpu_v4(flags + (base >> 2) * kFlagLine);
-    c.base = base;
+    uint32_t m = c.v[pos];
+#pragma unroll
+    for (int i = 1; i < n; ++i) m = min(m, c.v[pos + i]);
+    if (m >= target) return;
+    ld_acquire_gpu_v8(seg, c.v);
   }
 }
 
@@ -228,12 +236,12 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
           if (kb % kCl == crank) {
             if (s > 0) {  // chunk kb = units kb*64 .. +64 <- unit blocks kb*64/kU ..
               constexpr int kPer = 64 / kU;
-              if (kPer == 4) {
-                wait_flags4(flag_at(flags, 4 * kb), (uint32_t)s);  // acquire included
+              if (kPer == 4) {  // blocks 4kb..4kb+3: one line
+                wait_flags4(fwd_flag(flags, 4 * kb), (uint32_t)s);  // acquire included
               } else {
 #pragma unroll
-                for (int u = 0; u < kPer; ++u) wait_flag(flag_at(flags, kPer * kb + u), (uint32_t)s);
-                (void)ld_acquire_gpu(flag_at(flags, kPer * kb + kPer - 1));
+                for (int u = 0; u < kPer; ++u) wait_flag(fwd_flag(flags, kPer * kb + u), (uint32_t)s);
+                (void)ld_acquire_gpu(fwd_flag(flags, kPer * kb + kPer - 1));
               }
               fence_proxy_async_global();
             }
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
       named_bar_sync(kPubBar, kEpiThreads + 32);
       if (lane == 0) {
         trace_mark(P.trace, T, s, 5);
-        st_release_gpu(flag_at(flags, ublk), (uint32_t)(s + 1));
+        st_release_gpu(fwd_flag(flags, ublk), (uint32_t)(s + 1));
         trace_mark(P.trace, T, s, 4);
       }
       __syncwarp();
@@ -467,8 +475,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         tma_load_2d(sW + j * 8192, &P.tmW, wbar, ug * kGU, dir * 4 * kH + ks * kKSlice + j * 64);
       int stage = 0;
       uint32_t phase = 0;
-      FlagCache fc;
-      fc.base = -1;
+      FlagSeg seg;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) seg.v[i] = 0;
+      const uint32_t* myseg = flags + ks * kFlagLine;  // chunks 8ks .. 8ks+7
       for (int s = 1; s < T; ++s) {
         const int t = dir == 0 ? T - 1 - s : s;
         const int tprev = dir == 0 ? t + 1 : t - 1;
@@ -479,13 +489,13 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
           mbar_arrive_expect_tx(&full[stage], kTileA);
           if (kMulticastB) {  // the pair alternates chunks; multicast to both
             if ((j & 1) == upair) {
-              wait_flag(flag_at(flags, chunk), (uint32_t)s);
-              acquire_for_tma(flag_at(flags, chunk), P.variant);
+              wait_flag(bwd_flag(flags, chunk), (uint32_t)s);
+              acquire_for_tma(bwd_flag(flags, chunk), P.variant);
               tma_load_2d_mc(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow,
                              pair_mask);
             }
           } else {
-            wait_flag_cached(fc, flags, chunk, (uint32_t)s);  // acquire vector poll
+            wait_seg<1>(seg, myseg, j, (uint32_t)s);  // one 32-byte acquire poll covers the step's 8 chunks
             if (!(P.variant & 128)) fence_proxy_async_global();
             tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
             if (P.trace && blockIdx.x == 0)
@@ -585,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       // the finalisers we feed must have consumed the previous exchange
       // (checked before the MMA wait so the L2 round trip overlaps it)
       if (s >= 2 && lane == 0) {  // the finalisers 4ug .. 4ug+3 (one vector poll)
-        wait_flags4(flag_at(flags, ug * kKS), (uint32_t)s);
+        wait_flags4(bwd_flag(flags, ug * kKS), (uint32_t)s);
       }
       __syncwarp();
       if (s > 0) {
@@ -668,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         }
       }
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
-      publish(flag_at(flags, my_chunk), (uint32_t)(s + 1), P.variant);
+      publish(bwd_flag(flags, my_chunk), (uint32_t)(s + 1), P.variant);
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 4);
     }
     if (threadIdx.x == kEpiWarp0 * 32) bulk_wait0();  // outgoing exchange copies complete
