@@ -7,11 +7,19 @@ N = 1 : config "paper BLSTM ... SSGD batch 256 on 1 B200" — the reference's
         single-learner path run_single (engines/single.py:49-55): gather ->
         fwd/bwd -> learning_rate -> sgd_step, per minibatch of 256 21-frame
         sequences drawn from epoch_minibatches.
-N > 1 : one rank per GPU (torchrun), SSGD with per-learner batch B (weak
-        scaling): each rank computes its gradient, the gradient is
-        allreduced (torch.distributed / NCCL — the comparison baseline
-        transport) and every rank applies the fused SGD+snapshot kernel.
-
+N > 1 : one rank per GPU (torchrun), per-learner batch B (weak scaling),
+        --strategy ssgd (default) | adpsgd | hadpsgd:
+          ssgd     every rank's gradient is reduced in the reference's
+                   canonical chunk order, /world, momentum SGD on the owned
+                   chunk and theta all-gathered (ds_shard_step);
+          adpsgd   local momentum SGD, then ADPSGD pairwise averaging with
+                   the ring Topology partner of this iteration (ds_pair_mix),
+                   lock-step: every learner updates once per step;
+          hadpsgd  --groups groups: SSGD inside a group, then member r of a
+                   group averages with member r of the partner group.
+        --transport p2p (default): libds kernels over CUDA-IPC-mapped peer
+        memory (NVLink P2P) with device barriers; --transport nccl: the same
+        schedule with torch.distributed/NCCL collectives (comparison only).
 `value` is device-timed (CUDA events on the learner stream, inputs resident
 in HBM, max over ranks); `e2e` goes through the public Learner API with the
 minibatch indices copied host->device and the loss read back every step.
@@ -162,12 +170,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                              training_flops_per_frame)
     from paper_1904_04956_b200.schedule import baseline_schedule, epoch_minibatches, learning_rate
 
+    if args.same_device:  # functional check of the multi-process path on a one-GPU box (time-sliced)
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dist = None
+    red_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.same_device:
+            dist.init_process_group("gloo")
+            red_dev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     obj = BlstmObjective()
     B = args.batch
     T = obj.frames
@@ -184,15 +199,60 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     idx_dev = torch.from_numpy(np.stack(mine)).to(torch.device("cuda", local_rank))
     stream = L.stream
     P = obj.param_dim
+    strategy = "single" if world == 1 else args.strategy
+    if strategy in ("adpsgd", "hadpsgd") and world % 2:
+        raise SystemExit("adpsgd / hadpsgd need an even number of learners")
+    group = None
+    if world > 1 and args.transport == "p2p":
+        from paper_1904_04956_b200.p2p import PeerGroup
+
+        group = PeerGroup(L, rank, world)
+    from paper_1904_04956_b200.p2p import adpsgd_partner, hadpsgd_layout
+
+    ngroups = args.groups if strategy == "hadpsgd" else 1
+    gsize = world // max(1, ngroups)
+    if strategy == "hadpsgd" and (ngroups < 2 or world % ngroups or ngroups % 2):
+        raise SystemExit("hadpsgd needs an even group count dividing the learner count")
+    peer_buf = torch.empty_like(L.theta) if (world > 1 and args.transport == "nccl" and strategy != "ssgd") else None
+
+    def nccl_mix(peer: int):
+        ops = [dist.P2POp(dist.isend, L.theta, peer), dist.P2POp(dist.irecv, peer_buf, peer)]
+        with torch.cuda.stream(stream):
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            L.theta.add_(peer_buf).mul_(0.5)
+        L.snapshot()
+
+    def sync(k: int, lr: float):
+        """the strategy's exchange after this rank's gradient of step k"""
+        if strategy == "single":
+            L.sgd_step(lr)
+        elif strategy == "ssgd":
+            if group is not None:
+                group.ssgd_step(lr)
+            else:
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(L.grad)
+                    L.grad.div_(world)
+                L.sgd_step(lr)
+        elif strategy == "adpsgd":
+            L.sgd_step(lr)
+            peer = adpsgd_partner(rank, world, k + 1)
+            group.mix(peer) if group is not None else nccl_mix(peer)
+        else:  # hadpsgd
+            gid, mi = hadpsgd_layout(rank, ngroups, gsize)
+            members = list(range(gid * gsize, (gid + 1) * gsize))
+            if group is not None:
+                group.ssgd_step(lr, members=members)
+            else:
+                raise SystemExit("hadpsgd is implemented on the p2p transport only")
+            peer = adpsgd_partner(gid, ngroups, k + 1) * gsize + mi
+            group.mix(peer)
 
     def step(k: int):
         j = k % q
         L.gradient_device(idx_dev[j], B)
-        if dist is not None:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(L.grad)
-                L.grad.div_(world)
-        L.sgd_step(learning_rate(sched, 1, j, q))
+        sync(k, learning_rate(sched, 1, j, q))
 
     for k in range(args.warmup):
         step(k)
@@ -210,14 +270,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
     L.check_finite()
+    if group is not None:
+        group.check()
     frames = args.steps * B * T * world
     value = frames / (ms / 1e3)
-    launches_per_step = L.kernel_count() + 4 + obj.layers  # + sgd, W_hh^T, W_ih0 pad, bias copies
+    # fwd/bwd kernels + the strategy's sync kernels (sgd+aux / barriers + shard step or mix + aux)
+    sync_launches = {"single": 2, "ssgd": 4 if group is not None else 2, "adpsgd": 6 if group is not None else 3,
+                     "hadpsgd": 10}[strategy]
+    launches_per_step = L.kernel_count() + sync_launches
 
     # ---- end to end through the public Learner API (host indices in, loss out)
     e2e_steps = max(3, min(args.steps, 20))
@@ -228,16 +293,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for k in range(e2e_steps):
         j = k % q
         L.gradient(mine[j])
-        if dist is not None:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(L.grad)
-                L.grad.div_(world)
-        L.sgd_step(learning_rate(sched, 1, j, q))
+        sync(args.warmup + args.steps + k, learning_rate(sched, 1, j, q))
         _ = L.mean_loss()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist is not None:
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": round(e2e_steps * B * T * world / e2e_s, 1), "unit": UNIT, "h2d_bytes_per_step": B * 8,
@@ -276,10 +337,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": ("paper BLSTM run_single step, batch 256 (config 2)" if world == 1 else
-                                f"paper BLSTM SSGD, {B}/learner, allreduce=nccl-baseline"),
+                                f"paper BLSTM {strategy.upper()}, {B}/learner, transport={args.transport}"
+                                + (f", {ngroups} groups x {gsize}" if strategy == "hadpsgd" else "")),
                    "layers": obj.layers, "cells": 1024, "bottleneck": obj.bottleneck, "classes": obj.classes,
                    "input_dim": obj.input_dim, "frames": T, "batch_per_learner": B, "global_batch": B * world,
-                   "strategy": "single" if world == 1 else "ssgd",
+                   "strategy": strategy, "transport": args.transport if world > 1 else None,
                    "l2_policy": "per-step working set ~1.2 GB (activations, 344 MB dlogits) >> 126 MB L2; no flush",
                    "parallelism": f"dp{world}"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
@@ -287,6 +349,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if group is not None:
+        group.close()
     L.close()
     if dist is not None:
         dist.destroy_process_group()
@@ -303,6 +367,11 @@ def main():
     ap.add_argument("--cpu-batch", type=int, default=32)
     ap.add_argument("--ref-max-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--strategy", default="ssgd", choices=["ssgd", "adpsgd", "hadpsgd"])
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--groups", type=int, default=2)
+    ap.add_argument("--same-device", action="store_true",
+                    help="all ranks on cuda:0 with gloo plumbing (functional check only; p2p transport)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -125,6 +125,57 @@ int32_t ds_blstm_kernel_count(ds_blstm* h);
 int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C,
                        int64_t ldc, int32_t M, int32_t N, int32_t K, ds_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Multi-process data parallelism (one process per GPU, NVLink P2P).
+ * These replace the reference's in-process transports for a learner group
+ * (RingAllreduceGroup, collective.py:81-163; the ADPSGD channels and
+ * adpsgd_mix, engines/adpsgd.py:36-43,184-207,280-286) when every learner is
+ * its own process: buffers are shared through CUDA IPC and the sync kernels
+ * read and write the peers' memory directly.  NCCL is only the comparison.
+ */
+#define DS_IPC_HANDLE_BYTES 64
+
+/* Export the allocation holding `ptr`: 64-byte IPC handle + byte offset. */
+int ds_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
+/* Map a peer's exported allocation into this process (current device);
+ * *base_out is what ds_ipc_close takes, *ptr_out = base + offset. */
+int ds_ipc_open(const void* handle, int64_t offset, void** base_out, void** ptr_out);
+int ds_ipc_close(void* base);
+/* Stream-ordered copy between any two device (or peer-mapped) pointers. */
+int ds_device_copy(void* dst, const void* src, int64_t bytes, ds_stream_t stream);
+/* Single-process multi-device groups: enable device -> peer access. */
+int ds_enable_peer_access(int32_t device, int32_t peer);
+
+/* bf16 operand snapshot buffer of a handle (param_dim elements) so a peer
+ * can refresh it together with theta, and the snapshot extras (padded layer-0
+ * W_ih, fp32 biases) a learner re-derives from its own theta afterwards. */
+void* ds_blstm_snapshot_ptr(ds_blstm* h);
+int ds_blstm_snapshot_aux(ds_blstm* h, const float* theta, ds_stream_t stream);
+
+/* Device-side barrier of n members: flag word member_flags[m][my_rank] is set
+ * to `epoch` for every member m, then the call waits on the stream until
+ * own_flags[member_ranks[m]] >= epoch for all m.  Epochs must increase
+ * monotonically per process (SPMD call order).  After timeout_s the wait
+ * gives up and sets *err (checked by the host): a lost peer never hangs. */
+int ds_peer_barrier(int32_t n, uint32_t* const* member_flags, const int32_t* member_ranks, int32_t my_rank,
+                    uint32_t* own_flags, uint32_t epoch, int32_t* err, double timeout_s, ds_stream_t stream);
+
+/* Sharded group step of rank `rank` (RingAllreduceGroup.allreduce + /world +
+ * sgd_step, engines/ssgd.py:84-87): for the chunks this rank owns
+ * (j % world == rank, make_chunk_plan) sum the members' gradients in the
+ * canonical ring order, divide, update this rank's velocity and theta, and
+ * store theta (+ bf16 snapshot) into every member.  mode 1 averages theta
+ * instead (Hybrid, engines/hybrid.py:97-99).  Call between two barriers. */
+int ds_shard_step(int32_t world, int32_t rank, const float* const* grads, float* const* thetas,
+                  void* const* snaps, float* v_own, int64_t n, int32_t nchunks, float lr, float mu, int32_t mode,
+                  float divisor, ds_stream_t stream);
+
+/* ADPSGD pairwise average (adpsgd_mix) over P2P: m = (self + peer) / 2 on
+ * half 0 ([0, n/2)), half 1 ([n/2, n)) or -1 (all), stored to both sides and
+ * to their bf16 snapshots (nullable). */
+int ds_pair_mix(float* self, float* peer, void* snap_self, void* snap_peer, int64_t n, int32_t half,
+                ds_stream_t stream);
+
 /* Recurrent-kernel self-test hooks (tests only): run one bidirectional layer's
  * forward / backward recurrence on caller buffers (layouts of lstm_rec.cu;
  * whh = W_hh bf16 [4096, 512] for both directions of recurrence).

@@ -44,6 +44,16 @@ SIGNATURES = {
     "ds_debug_gemm_bf16": (_I32, [_VP, _I64, _I32, _VP, _I64, _I32, _VP, _I64, _I32, _I32, _I32, _VP]),
     "ds_debug_lstm_fwd": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ds_debug_lstm_bwd": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ds_ipc_export": (_I32, [_VP, _VP, ctypes.POINTER(_I64)]),
+    "ds_ipc_open": (_I32, [_VP, _I64, ctypes.POINTER(_VP), ctypes.POINTER(_VP)]),
+    "ds_ipc_close": (_I32, [_VP]),
+    "ds_device_copy": (_I32, [_VP, _VP, _I64, _VP]),
+    "ds_enable_peer_access": (_I32, [_I32, _I32]),
+    "ds_blstm_snapshot_ptr": (_VP, [_VP]),
+    "ds_blstm_snapshot_aux": (_I32, [_VP, _VP, _VP]),
+    "ds_peer_barrier": (_I32, [_I32, _VP, _VP, _I32, _VP, ctypes.c_uint32, _VP, ctypes.c_double, _VP]),
+    "ds_shard_step": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _I64, _I32, _F32, _F32, _I32, _F32, _VP]),
+    "ds_pair_mix": (_I32, [_VP, _VP, _VP, _VP, _I64, _I32, _VP]),
     "ds_last_error": (ctypes.c_char_p, []),
 }
 

@@ -517,6 +517,14 @@ int ds_blstm_cast_snapshot(ds_blstm* h, const float* theta, ds_stream_t stream) 
   return op_snapshot_aux(theta, h->L, h->wih0pad, h->bias_snap, s);
 }
 
+int ds_blstm_snapshot_aux(ds_blstm* h, const float* theta, ds_stream_t stream) {
+  if (!h || !theta) return fail_arg("null argument");
+  DS_CUDA_TRY(cudaSetDevice(h->device));
+  return op_snapshot_aux(theta, h->L, h->wih0pad, h->bias_snap, reinterpret_cast<cudaStream_t>(stream));
+}
+
+void* ds_blstm_snapshot_ptr(ds_blstm* h) { return h ? h->snap : nullptr; }
+
 int ds_blstm_fwd_bwd(ds_blstm* h, const int64_t* idx, int32_t B, float* grad, float* loss_sum, int32_t* nonfinite,
                      ds_stream_t stream) {
   if (!h || !idx || !grad) return fail_arg("null argument");

@@ -1,0 +1,151 @@
+"""One-process-per-GPU P2P path (paper_1904_04956_b200/p2p.py, csrc/p2p.cu).
+
+CPU: the partner schedule is the reference Topology and a perfect matching
+every iteration (so lock-step ADPSGD pairs never overlap).
+GPU: two processes share cuda:0 through CUDA IPC (the same mechanism that maps
+a neighbour GPU's memory over NVLink); the sharded SSGD step and the pairwise
+mix must equal float32 restatements of the reference arithmetic bit for bit,
+and every replica must hold identical weights afterwards."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+from paper_1904_04956_b200.p2p import adpsgd_partner, hadpsgd_layout
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_partner_schedule_is_topology_matching(world):
+    from paper_1904_04956_b200.schedule import Topology
+
+    topo = Topology(world)
+    for it in range(1, 9):
+        p = [adpsgd_partner(r, world, it) for r in range(world)]
+        assert sorted(p) == list(range(world))            # a permutation ...
+        assert all(p[p[r]] == r and p[r] != r for r in range(world))  # ... of disjoint pairs
+        for s in topo.senders():
+            assert p[s - 1] == topo.partner(s, it) - 1
+
+
+def test_partner_schedule_matches_reference(ref):
+    from distsgd.engines.common import Topology as RefTopology
+
+    for world in (2, 4, 8):
+        t = RefTopology(world)
+        for it in range(1, 7):
+            for s in range(1, world + 1, 2):
+                assert adpsgd_partner(s - 1, world, it) == t.partner(s, it) - 1
+
+
+def test_hadpsgd_layout():
+    assert [hadpsgd_layout(r, 2, 4) for r in range(8)] == [(0, 0), (0, 1), (0, 2), (0, 3), (1, 0), (1, 1), (1, 2),
+                                                         (1, 3)]
+    with pytest.raises(ValueError):
+        hadpsgd_layout(8, 2, 4)
+
+
+# ---------------------------------------------------------------------------
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import blstm_ref as O
+    from paper_1904_04956_b200.blstm import BlstmObjective, DeviceDataset, Learner
+    from paper_1904_04956_b200.p2p import PeerGroup
+
+    torch.cuda.set_device(0)
+    obj = BlstmObjective(layers=1, bottleneck=64, classes=64, frames=3)
+    spec = O.BlstmSpec(layers=1, input_dim=260, hidden=512, bottleneck=64, classes=64, frames=3)
+    x, y, _, _ = O.make_dataset(spec, 32, seed=0)
+    w0 = O.initial_weights(spec, 0)
+    L = Learner(obj, DeviceDataset(x, y), max_batch=8, theta0=w0)
+    G = PeerGroup(L, rank, world, timeout_s=120.0)
+    out = {}
+    # --- SSGD: same weights, different batches -> identical replicas
+    L.gradient(np.arange(8) + 8 * rank)
+    L.stream.synchronize()
+    out["g"] = L.grad.cpu().numpy()
+    out["theta0"] = L.theta.cpu().numpy()
+    G.ssgd_step(0.05)
+    G.check()
+    out["theta_ssgd"] = L.theta.cpu().numpy()
+    from paper_1904_04956_b200 import _lib
+
+    snap = torch.empty(obj.param_dim, dtype=torch.bfloat16, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.ds_device_copy(snap.data_ptr(), lib.ds_blstm_snapshot_ptr(L.handle), obj.param_dim * 2,
+                                  L.stream.cuda_stream))
+    L.stream.synchronize()
+    out["snap_ssgd"] = snap.float().cpu().numpy()
+    # the step refreshed the bf16 operand snapshot: the loss on it equals the
+    # loss after an explicit re-cast of theta (and is the same on both ranks)
+    L.loss(np.arange(8))
+    L.stream.synchronize()
+    out["loss_step_snap"] = np.float32(L.loss_sum.item())
+    L.snapshot()
+    L.loss(np.arange(8))
+    L.stream.synchronize()
+    out["loss_recast"] = np.float32(L.loss_sum.item())
+    # --- ADPSGD mix: different weights -> both hold (a + b) / 2
+    with torch.cuda.stream(L.stream):
+        L.theta.mul_(1.0 + 0.25 * (rank + 1)).add_(0.001 * (rank + 1))
+    L.stream.synchronize()
+    out["theta_pre_mix"] = L.theta.cpu().numpy()
+    G.mix(1 - rank)
+    G.check()
+    out["theta_mix"] = L.theta.cpu().numpy()
+    G.close()
+    L.close()
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), **out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_process_ipc_ssgd_and_mix_bit_exact():
+    torch = pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_worker, args=(2, _free_port(), d), nprocs=2, join=True, start_method="spawn")
+        r = [dict(np.load(os.path.join(d, f"r{i}.npz"))) for i in range(2)]
+    # SSGD: canonical-order chunk sums (owner first), / world, v = 0*mu + g, theta - lr*v (float32)
+    P = r[0]["g"].shape[0]
+    chunk = -(-P // 2)
+    g0, g1 = r[0]["g"], r[1]["g"]
+    s = np.empty(P, np.float32)
+    s[:chunk] = g0[:chunk] + g1[:chunk]      # chunk 0: owner 0 then 1
+    s[chunk:] = g1[chunk:] + g0[chunk:]      # chunk 1: owner 1 then 0
+    gm = s / np.float32(2)
+    v = np.float32(0.9) * np.zeros(P, np.float32) + gm
+    want = r[0]["theta0"] - np.float32(0.05) * v
+    assert np.array_equal(r[0]["theta_ssgd"], r[1]["theta_ssgd"])
+    assert np.array_equal(r[0]["theta_ssgd"], want)
+    bf = torch.from_numpy(want).bfloat16().float().numpy()
+    for k in (0, 1):
+        bad = np.nonzero(r[k]["snap_ssgd"] != bf)[0]
+        assert bad.size == 0, (k, bad.size, bad[:3], bad[-3:], P)
+    for k in (0, 1):
+        assert r[k]["loss_step_snap"] == r[k]["loss_recast"]
+    assert r[0]["loss_step_snap"] == r[1]["loss_step_snap"]
+    # mix
+    m = (r[0]["theta_pre_mix"] + r[1]["theta_pre_mix"]) * np.float32(0.5)
+    assert np.array_equal(r[0]["theta_mix"], m) and np.array_equal(r[1]["theta_mix"], m)
