@@ -84,10 +84,20 @@ struct GemmProblem {
   long long split_stride;
 };
 
+// Pair-tile schedule: when the tiles of a launch differ in length the host
+// assigns them to the persistent CTA pairs longest-first onto the least
+// loaded pair (LPT) and passes the per-pair lists here; otherwise pairs walk
+// the tiles round-robin.
+constexpr int kMaxSched = 2048;
+constexpr int kMaxPairs = 80;
+
 struct GemmBatch {
   GemmProblem p[kMaxProblems];
   int nprob;
   int total_tiles;
+  int sched;                            // 1: use order/pstart
+  uint16_t pstart[kMaxPairs + 1];       // pair p runs order[pstart[p] .. pstart[p+1])
+  uint16_t order[kMaxSched];
 };
 
 // Host helpers -------------------------------------------------------------

@@ -173,6 +173,9 @@ DS_DEV void bulk_copy_s2cluster(uint32_t dst_caddr, const void* src, uint32_t by
       "r"(smem_u32(src)), "r"(bytes), "r"(mbar_caddr)
       : "memory");
 }
+DS_DEV void mbar_arrive_remote(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
 DS_DEV void mbar_arrive_remote_release(uint32_t caddr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }

@@ -23,6 +23,10 @@
 //                 64*(e/4) .. +64
 // Pair tiles are walked round-robin over the persistent grid; the two TMEM
 // accumulators let the epilogue of tile i overlap the main loop of tile i+1.
+#include <algorithm>
+#include <utility>
+#include <vector>
+
 #include "ds_internal.h"
 #include "ds_ptx.cuh"
 
@@ -61,6 +65,15 @@ __device__ __forceinline__ TileCoord locate(const GemmBatch& b, int tile) {
   c.tn = rest % b.p[p].tiles_n;
   c.ks = rest / b.p[p].tiles_n;
   return c;
+}
+
+// the i-th tile of pair `pair` (i < pair_tile_count)
+__device__ __forceinline__ int pair_tile_count(const GemmBatch& b, int pair, int npairs) {
+  if (b.sched) return b.pstart[pair + 1] - b.pstart[pair];
+  return pair < b.total_tiles ? (b.total_tiles - 1 - pair) / npairs + 1 : 0;
+}
+__device__ __forceinline__ int pair_tile(const GemmBatch& b, int pair, int npairs, int i) {
+  return b.sched ? (int)b.order[b.pstart[pair] + i] : pair + i * npairs;
 }
 
 // k-block range of split `ks`
@@ -148,7 +161,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int total = batch.total_tiles;
 
   if (warp == 0) {
     if (elect_one()) {
@@ -156,8 +168,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const uint32_t full_c = mapa_shared(smem_u32(full), 0);  // leader's full[0]
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < total; tile += npairs) {
-        TileCoord tc = locate(batch, tile);
+      const int ntl = pair_tile_count(batch, pair, npairs);
+      for (int ti = 0; ti < ntl; ++ti) {
+        TileCoord tc = locate(batch, pair_tile(batch, pair, npairs, ti));
         const GemmProblem& P = batch.p[tc.prob];
         const int m0 = tc.tm * kPairM + (int)crank * BM, n0 = tc.tn * BN + (int)crank * kBHalf;
         int kb0, kb1;
@@ -194,8 +207,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = pair; tile < total; tile += npairs, ++it) {
-        TileCoord tc = locate(batch, tile);
+      const int ntl = pair_tile_count(batch, pair, npairs);
+      for (int ti = 0; ti < ntl; ++ti, ++it) {
+        TileCoord tc = locate(batch, pair_tile(batch, pair, npairs, ti));
         const GemmProblem& P = batch.p[tc.prob];
         int kb0, kb1;
         kb_range(P, tc.ks, kb0, kb1);
@@ -239,8 +253,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     constexpr float kLog2e = 1.4426950408889634f;
     const uint32_t tempty_c = mapa_shared(smem_u32(tempty), 0);
     int it = 0;
-    for (int tile = pair; tile < total; tile += npairs, ++it) {
-      TileCoord tc = locate(batch, tile);
+    const int ntl = pair_tile_count(batch, pair, npairs);
+    for (int ti = 0; ti < ntl; ++ti, ++it) {
+      TileCoord tc = locate(batch, pair_tile(batch, pair, npairs, ti));
       const GemmProblem& P = batch.p[tc.prob];
       const int rt = tc.tm * 2 + (int)crank;  // 128-row tile of this CTA
       // problem fields into registers once per tile (P is indexed dynamically)
@@ -269,11 +284,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         // online (max, sum exp) over this thread's 64 columns, log2 domain
         float mx = -INFINITY, se = 0.f, tg = 0.f;
         bool have_t = false;
-#pragma unroll 1
+        float vbuf[2][32];
+        tmem_ld32(t_row, vbuf[0]);
+        tmem_ld_wait();
+#pragma unroll
         for (int c = 0; c < kCols; c += 32) {
-          float v[32];
-          tmem_ld32(t_row + c, v);
-          tmem_ld_wait();
+          float* v = vbuf[(c >> 5) & 1];
+          if (c + 32 < kCols) tmem_ld32(t_row + c + 32, vbuf[((c >> 5) + 1) & 1]);  // in flight meanwhile
           const int nb = n0 + c;
           float cm = -INFINITY;
           if (full_cols) {
@@ -314,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             se = se * ex2_fast(mx - nm) + ((s0 + s1) + (s2 + s3));
             mx = nm;
           }
+          if (c + 32 < kCols) tmem_ld_wait();
         }
         if (row_ok) {
           // stats in natural-log units: max, sum exp(x - max)
@@ -419,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       if (lane == 0) {
         if (leader)
           mbar_arrive(&tempty[acc]);
-        else
-          mbar_arrive_remote_release(tempty_c + acc * 8);
+        else  // TMEM reads are complete (wait::ld + fence): no memory release needed
+          mbar_arrive_remote(tempty_c + acc * 8);
       }
     }
     if (lane == 0) bulk_wait0();  // staged output stores complete before exit
@@ -473,6 +491,49 @@ int gemm_bf16_output(GemmProblem* p) {
   return DS_OK;
 }
 
+// Tile cost in k-block units (mainloop) plus the epilogue's weight, for the
+// host-side LPT assignment.  Uniform batches keep the round-robin walk.
+static void schedule_tiles(GemmBatch* b, int pairs) {
+  b->sched = 0;
+  const int total = b->total_tiles;
+  if (total > kMaxSched || total <= pairs) return;
+  std::vector<std::pair<int, int>> cost(total);  // (cost, tile)
+  bool uniform = true;
+  for (int i = 0; i < b->nprob; ++i) {
+    const GemmProblem& P = b->p[i];
+    const int nkb = (P.K + BK - 1) / BK;
+    const int per = (nkb + P.ksplit - 1) / P.ksplit;
+    const int epi = P.epi == EPI_CE_STATS || P.epi == EPI_CE_GRAD ? 8 : (P.epi == EPI_F32 ? 3 : 2);
+    const int n = P.tiles_m * P.tiles_n * P.ksplit;
+    for (int t = 0; t < n; ++t) {
+      const int ks = t / (P.tiles_m * P.tiles_n);
+      const int len = (ks == P.ksplit - 1) ? nkb - per * (P.ksplit - 1) : per;
+      cost[P.tile_begin + t] = {len + epi, P.tile_begin + t};
+    }
+  }
+  for (int t = 1; t < total; ++t) uniform &= cost[t].first == cost[0].first;
+  if (uniform) return;
+  std::stable_sort(cost.begin(), cost.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+    return x.first > y.first;
+  });
+  std::vector<long long> load(pairs, 0);
+  std::vector<std::vector<int>> lists(pairs);
+  for (const auto& c : cost) {  // longest remaining tile onto the least loaded pair
+    int best = 0;
+    for (int p = 1; p < pairs; ++p)
+      if (load[p] < load[best]) best = p;
+    load[best] += c.first;
+    lists[best].push_back(c.second);
+  }
+  int pos = 0;
+  for (int p = 0; p < pairs; ++p) {
+    b->pstart[p] = (uint16_t)pos;
+    for (int t : lists[p]) b->order[pos++] = (uint16_t)t;
+  }
+  b->pstart[pairs] = (uint16_t)pos;
+  b->sched = 1;
+}
+
 int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -491,8 +552,9 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   }
   b->total_tiles = total;
   if (total == 0) return DS_OK;
-  const int max_pairs = num_sms() / 2;
+  const int max_pairs = num_sms() / 2 < kMaxPairs ? num_sms() / 2 : kMaxPairs;
   const int pairs = total < max_pairs ? total : max_pairs;
+  schedule_tiles(b, pairs);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kThreads);
