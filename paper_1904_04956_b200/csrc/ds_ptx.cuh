@@ -132,6 +132,12 @@ DS_DEV void ld_acquire_gpu_v8(const uint32_t* p, uint32_t* v) {
                : "l"(p)
                : "memory");
 }
+DS_DEV void ld_relaxed_gpu_v8(const uint32_t* p, uint32_t* v) {
+  asm volatile("ld.relaxed.gpu.global.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p)
+               : "memory");
+}
 DS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 DS_DEV void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -387,6 +387,249 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_cons
 }
 
 // ============================================================================
+// Forward, batch-as-N (default): weights stationary as the MMA's M operand.
+//   CTA pair (tcgen05 cta_group::2) = (dir, batch block of 64, 64 units =
+//   256 gate rows).  Rank r keeps W_hh rows [r*128, +128) of the pair's 256
+//   (32 units, 128 KB smem, A operand) and stages batch rows [r*32, +32) of
+//   every h_{t-1} chunk (B operand, N split across the pair), so one SM pulls
+//   8 x 4 KB = 32 KB of h per step instead of the whole 128 KB tile.
+//   acc[128 gate rows (TMEM lanes), 64 batch] per CTA; the epilogue
+//   transposes gate quads with two shuffle stages so a thread owns one unit
+//   x 8 batch columns (i,f,g,o together), keeps c in registers, stages h_t in
+//   smem for coalesced 16-byte stores and publishes one flag per CTA.
+//   16 CTAs per (dir, batch block): chunk k of h (64 units) = pair k.
+namespace fwd2 {
+constexpr int kNB = 64;                 // batch columns per pair (MMA N)
+constexpr int kNH = kNB / 2;            // batch rows staged per CTA
+constexpr int kPairs = kH / 64;         // 8 pairs per (dir, batch block)
+constexpr int kCtas = 2 * kPairs;       // 16
+constexpr int kWB = 128 * kH * 2;       // 128 KB resident W slice
+constexpr int kChunkB = kNH * 128;      // 4 KB: 32 batch rows x 64 units bf16
+constexpr int kBufB = 8 * kChunkB;      // one step's B operand (32 KB)
+constexpr int kHst = kNB * 64;          // h staging: 64 batch rows x 32 units bf16 (4 KB)
+constexpr size_t kSmem = 1024 + kWB + 2 * kBufB + kHst + 512;
+constexpr int kEpiWarps = 8;
+constexpr int kEpiT = kEpiWarps * 32;
+constexpr int kPub = 2;                 // named barriers 2/3: epilogue <-> publisher
+}  // namespace fwd2
+
+__global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_constant__ LstmParams P) {
+  using namespace fwd2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = sm;
+  uint8_t* sB = sW + kWB;                 // [2 steps][8 chunks][32 rows x 128 B]
+  uint8_t* sH = sB + 2 * kBufB;           // [64 rows][32 units] bf16
+  uint64_t* full = reinterpret_cast<uint64_t*>(sH + kHst);  // [2][8], leader only
+  uint64_t* wbar = full + 16;
+  uint64_t* tfull = wbar + 1;   // [2]
+  uint64_t* tempty = tfull + 2;  // [2], leader: every epilogue warp of both CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();  // 0 = leader
+  const bool leader = rank == 0;
+  const int pg = blockIdx.x >> 1;
+  const int pr = pg % kPairs;
+  const int bb = (pg / kPairs) % P.n_btile;  // batch block of 64 (n_btile counts blocks here)
+  const int dir = pg / (kPairs * P.n_btile);
+  uint32_t* flags = P.counters + (dir * P.n_btile + bb) * kFlagLine;  // 16 flags: CTA = 2*pair + rank
+  const int T = P.T, B = P.B;
+  const int b0 = P.b0 + bb * kNB;
+
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < 16; ++i) mbar_init(&full[i], 1);
+    mbar_init(wbar, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 128);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&P.tmA);
+      tma_prefetch_desc(&P.tmW);
+      mbar_arrive_expect_tx(wbar, kWB);
+      const int wrow = dir * 4 * kH + pr * 256 + (int)rank * 128;
+      for (int kb = 0; kb < kH / 64; ++kb) tma_load_2d(sW + kb * 16384, &P.tmW, wbar, kb * 64, wrow);
+      const uint32_t full_c = mapa_shared(smem_u32(full), 0);
+      FlagSeg seg[2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) seg[0].v[i] = seg[1].v[i] = 0;
+      for (int s = 0; s < T; ++s) {
+        const int t = dir == 0 ? s : T - 1 - s;
+        const int tprev = dir == 0 ? t - 1 : t + 1;
+        const int arow = (tprev + 1) * B + b0 + (int)rank * kNH;
+        const int buf = s & 1;
+        for (int k = 0; k < kPairs; ++k) {
+          uint64_t* fb = &full[buf * 8 + k];
+          if (leader) mbar_arrive_expect_tx(fb, 2 * kChunkB);
+          if (s > 0) {  // chunk k of h_{t-1} = both CTAs of pair k (flags 2k, 2k+1)
+            wait_seg<2>(seg[k >> 2], flags + (k >> 2) * 8, (k & 3) * 2, (uint32_t)s);
+            fence_proxy_async_global();
+          }
+          tma_load_2d_pair(sB + buf * kBufB + k * kChunkB, &P.tmA, full_c + (uint32_t)(buf * 8 + k) * 8,
+                           dir * kH + k * 64, arow);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      mbar_wait(wbar, 0);
+      const uint32_t idesc = idesc_bf16_f32(256, kNB, 0, 0);
+      const uint32_t wbase = smem_u32(sW), bbase = smem_u32(sB);
+      for (int s = 0; s < T; ++s) {
+        const int acc = s & 1, buf = s & 1;
+        mbar_wait_acq_cluster(&tempty[acc], ((s >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem + acc * kNB;
+        for (int k = 0; k < kPairs; ++k) {
+          mbar_wait(&full[buf * 8 + k], (s >> 1) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint64_t ad = smem_desc_sw128(wbase + k * 16384 + kk * 32, 16, 1024);
+              uint64_t bd = smem_desc_sw128(bbase + buf * kBufB + k * kChunkB + kk * 32, 16, 1024);
+              mma_bf16_ss_pair(dacc, ad, bd, idesc, (k | kk) != 0);
+            }
+            if (k == kPairs - 1) mma_commit_pair_mc(&tfull[acc], 0x3);
+          }
+          __syncwarp();
+        }
+      }
+    } else {
+      mbar_wait(wbar, 0);  // keep the W load's barrier alive until it lands
+    }
+  } else if (warp == 3) {
+    // publisher: h_t of this CTA stored -> release the step flag
+    uint32_t* myflag = flags + (pr >> 2) * 8 + (pr & 3) * 2 + (int)rank;  // flag 2*pr + rank: segment /8, pos %8
+    for (int s = 0; s < T; ++s) {
+      named_bar_sync(kPub, kEpiT + 32);
+      if (lane == 0) st_release_gpu(myflag, (uint32_t)(s + 1));
+      __syncwarp();
+      asm volatile("bar.arrive %0, %1;" ::"n"(kPub + 1), "n"(kEpiT + 32) : "memory");
+    }
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
+    const uint32_t e = warp - kEpiWarp0;
+    const uint32_t q = e & 3, hc = e >> 2;      // TMEM lane quadrant, batch-column half
+    const uint32_t g = lane & 3;                 // gate of this thread's TMEM row (unit-interleaved rows)
+    const uint32_t b0b = g & 1, b1b = g >> 1;
+    const int uq = (int)(q * 8 + (lane >> 2));   // unit within the CTA's 32
+    const int unit = pr * 64 + (int)rank * 32 + uq;  // unit within the direction
+    const int col0 = (int)(hc * 32 + g * 8);     // after the transpose: batch columns col0 .. +8
+    const uint32_t tcol = tmem + ((q * 32) << 16) + hc * 32;
+    const uint32_t tempty_c = mapa_shared(smem_u32(tempty), 0);
+    const size_t gcol = (size_t)dir * 4 * kH + (size_t)unit * 4;
+    float c[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = 0.f;
+    for (int s = 0; s < T; ++s) {
+      const int t = dir == 0 ? s : T - 1 - s;
+      // prefetch the input projection (i,f,g,o of this unit) for my 8 batch rows
+      uint2 gp[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = b0 + col0 + i;
+        gp[i] = b < B ? *reinterpret_cast<const uint2*>(P.gates + ((size_t)t * B + b) * (8 * kH) + gcol)
+                      : make_uint2(0u, 0u);
+      }
+      mbar_wait(&tfull[s & 1], (s >> 1) & 1);
+      tc_fence_after();
+      float v[32];
+      tmem_ld32(tcol + (s & 1) * kNB, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tempty[s & 1]);
+        else
+          mbar_arrive_remote(tempty_c + (s & 1) * 8);
+      }
+      // quad transpose: stage 1 (lane ^ 2) splits the 32 columns in halves,
+      // stage 2 (lane ^ 1) in quarters -> 4 gates x 8 columns per lane
+      float a1[16], a2[16];  // a1: gate g, a2: gate g^2 (columns of my half)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float send = b1b ? v[i] : v[16 + i];
+        a1[i] = b1b ? v[16 + i] : v[i];
+        a2[i] = __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      float k1[8], k2[8], r1[8], r2[8];  // gates g, g^2 (kept), g^1, g^3 (received)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float s1 = b0b ? a1[i] : a1[8 + i];
+        const float s2 = b0b ? a2[i] : a2[8 + i];
+        k1[i] = b0b ? a1[8 + i] : a1[i];
+        k2[i] = b0b ? a2[8 + i] : a2[i];
+        r1[i] = __shfl_xor_sync(0xffffffffu, s1, 1);
+        r2[i] = __shfl_xor_sync(0xffffffffu, s2, 1);
+      }
+      float hv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        // gate x lives in: d = g ^ x -> d0 ? (d1 ? r2 : r1) : (d1 ? k2 : k1)
+        const float x0 = b0b ? (b1b ? r2[i] : r1[i]) : (b1b ? k2[i] : k1[i]);   // i gate (x = 0)
+        const float x1 = b0b ? (b1b ? k2[i] : k1[i]) : (b1b ? r2[i] : r1[i]);   // f gate (x = 1)
+        const float x2 = b0b ? (b1b ? r1[i] : r2[i]) : (b1b ? k1[i] : k2[i]);   // g gate (x = 2)
+        const float x3 = b0b ? (b1b ? k1[i] : k2[i]) : (b1b ? r1[i] : r2[i]);   // o gate (x = 3)
+        const __nv_bfloat162* gg = reinterpret_cast<const __nv_bfloat162*>(&gp[i]);
+        const float2 g01 = __bfloat1622float2(gg[0]), g23 = __bfloat1622float2(gg[1]);
+        const float ig = sigmoid_fast(x0 + g01.x);
+        const float fg = sigmoid_fast(x1 + g01.y);
+        const float gt = tanh_fast(x2 + g23.x);
+        const float og = sigmoid_fast(x3 + g23.y);
+        c[i] = fmaf(fg, c[i], ig * gt);
+        hv[i] = og * tanh_fast(c[i]);
+        // keep the activations for the BPTT state (written after the release)
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(ig, fg), p1 = __floats2bfloat162_rn(gt, og);
+        gp[i].x = *reinterpret_cast<uint32_t*>(&p0);
+        gp[i].y = *reinterpret_cast<uint32_t*>(&p1);
+      }
+      // h_t -> smem [64 rows][32 units] -> coalesced 16-byte stores
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<__nv_bfloat16*>(sH)[(col0 + i) * 32 + uq] = __float2bfloat16_rn(hv[i]);
+      named_bar_sync(1, kEpiT);
+      {
+        const int tid = (int)(e * 32 + lane);  // 256 threads = 64 rows x 4 segments of 8 units
+        const int row = tid >> 2, sg = tid & 3;
+        const int b = b0 + row;
+        const uint4 w = reinterpret_cast<const uint4*>(sH)[tid];
+        if (b < B && row < P.nb - bb * kNB)
+          *reinterpret_cast<uint4*>(P.y + ((size_t)(t + 1) * B + b) * (2 * kH) + dir * kH + pr * 64 + rank * 32 +
+                                    sg * 8) = w;
+      }
+      asm volatile("bar.arrive %0, %1;" ::"n"(kPub), "n"(kEpiT + 32) : "memory");
+      named_bar_sync(kPub + 1, kEpiT + 32);  // the release is out: BPTT state, then reuse sH
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = b0 + col0 + i;
+        if (b < B && col0 + i < P.nb - bb * kNB) {
+          const size_t n = (size_t)t * B + b;
+          *reinterpret_cast<uint2*>(P.gates + n * (8 * kH) + gcol) = gp[i];
+          P.cstate[n * (2 * kH) + dir * kH + unit] = c[i];
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair(tmem, 128);
+}
+
+// ============================================================================
 // Backward: split-K over a 4-CTA cluster.
 //   cluster = (dir, batch tile, unit group ug of 64 units); CTA rank ks holds
 //   W_hh[gate rows ks*512 .. +512][64 units of ug] (64 KB, read as an
@@ -431,7 +674,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   uint64_t* tfull = wbar + 1;    // [2] double-buffered accumulators: MMA iteration i = s-1 uses i & 1
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;  // recv buffer complete (all 4 sources)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 1);
+  uint64_t* rfree = rfull + 1;   // my last partials were consumed by the 3 peer finalisers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfree + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int crank = (int)cluster_ctarank();
@@ -458,6 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       mbar_init(&tempty[i], kEpiThreads);
     }
     mbar_init(rfull, 1);  // local expect_tx arrive; peers complete 3 x 8 KB of tx
+    mbar_init(rfree, kKS - 1);  // remote arrives of the 3 finalisers fed by this CTA
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 128);
@@ -495,7 +740,15 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
                              pair_mask);
             }
           } else {
-            wait_seg<1>(seg, myseg, j, (uint32_t)s);  // one 32-byte acquire poll covers the step's 8 chunks
+            if (P.variant & 256) {  // experiment: relaxed polls, one acquire load once satisfied
+              if (seg.v[j] < (uint32_t)s) {
+                do ld_relaxed_gpu_v8(myseg, seg.v);
+                while (seg.v[j] < (uint32_t)s);
+                ld_acquire_gpu_v8(myseg, seg.v);
+              }
+            } else {
+              wait_seg<1>(seg, myseg, j, (uint32_t)s);  // one 32-byte acquire poll covers the step's 8 chunks
+            }
             if (!(P.variant & 128)) fence_proxy_async_global();
             tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
             if (P.trace && blockIdx.x == 0)
@@ -592,12 +845,6 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       float dh[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) dh[u] = 0.f;
-      // the finalisers we feed must have consumed the previous exchange
-      // (checked before the MMA wait so the L2 round trip overlaps it)
-      if (s >= 2 && lane == 0) {  // the finalisers 4ug .. 4ug+3 (one vector poll)
-        wait_flags4(bwd_flag(flags, ug * kKS), (uint32_t)s);
-      }
-      __syncwarp();
       if (s > 0) {
         const int it = s - 1;
         mbar_wait(&tfull[it & 1], (it >> 1) & 1);
@@ -626,6 +873,9 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         fence_proxy_async_smem();
         named_bar_sync(3, kEpiThreads);
         if (issuer) {
+          // the finalisers we feed consumed our previous partials (cluster
+          // mbarrier: no global-memory polling next to the chunk flags)
+          if (s >= 2) mbar_wait_acq_cluster(rfree, (uint32_t)(s - 2) & 1);
           for (int f = 0; f < kKS; ++f) {
             if (f == ks) continue;
             const uint32_t peer = rbase + (uint32_t)f;
@@ -645,6 +895,11 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
           const float4 x1 = *reinterpret_cast<const float4*>(rb + src * kRecvSlot + slot_off(r, 2 * hf + 1));
           dh[0] += x0.x; dh[1] += x0.y; dh[2] += x0.z; dh[3] += x0.w;
           dh[4] += x1.x; dh[5] += x1.y; dh[6] += x1.z; dh[7] += x1.w;
+        }
+        named_bar_sync(3, kEpiThreads);  // every thread has read this exchange
+        if (issuer) {
+          for (int f = 0; f < kKS; ++f)
+            if (f != ks) mbar_arrive_remote(mapa_shared(smem_u32(rfree), rbase + (uint32_t)f));  // CTA-scope release: no GPU membar
         }
       }
       if (ok) {
@@ -738,9 +993,22 @@ int lstm_max_tiles() { return num_sms() / (2 * (kH / fwd_units())); }
 static int lstm_bwd_max_tiles() { return (num_sms() >= 132 ? 128 : num_sms()) / 64; }
 int lstm_counter_words(int B) { return 2 * kGroupFlagWords * ((B + 127) / 128); }
 
+// forward implementation: batch-as-N CTA pairs (default) or the batch-as-M
+// kernels above (DS_FWD_IMPL=m, with DS_FWD_UNITS=16|32)
+static bool fwd_nb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_FWD_IMPL");
+    v = (e && e[0] == 'm') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
+    DS_CUDA_TRY(
+        cudaFuncSetAttribute(lstm_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd2::kSmem));
     DS_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)fwd::Cfg<32>::kSmem));
     DS_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -751,6 +1019,36 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     attr_set = true;
   }
   const int B = a.B, T = a.T;
+  if (fwd && fwd_nb()) {
+    // 32 CTAs (2 directions x 8 pairs x 2) per 64-row batch block
+    const int max_blocks = num_sms() / (2 * fwd2::kCtas);
+    if (max_blocks < 1) return fail_arg("device too small for the recurrent kernel");
+    LstmParams P;
+    memset(&P, 0, sizeof(P));
+    int rc = make_tmap_2d(&P.tmA, a.y_full, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2 * kH, (uint64_t)(T + 2) * B,
+                          2 * kH * 2, 64, fwd2::kNH);
+    if (rc) return rc;
+    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, 64, 128);
+    if (rc) return rc;
+    P.gates = a.gates;
+    P.cstate = a.cstate;
+    P.y = a.y_full;
+    P.trace = nullptr;
+    P.B = B;
+    P.T = T;
+    const int chunk_rows = max_blocks * fwd2::kNB;
+    for (int b0 = 0; b0 < B; b0 += chunk_rows) {
+      const int nb = (B - b0) < chunk_rows ? (B - b0) : chunk_rows;
+      P.b0 = b0;
+      P.nb = nb;
+      P.n_btile = (nb + fwd2::kNB - 1) / fwd2::kNB;  // 64-row blocks
+      P.counters = a.counters + (b0 / fwd2::kNB) * 2 * kFlagLine;
+      DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * kFlagLine * P.n_btile, stream));
+      rc = launch_coop((const void*)lstm_fwd2_kernel, 2 * fwd2::kCtas * P.n_btile, P, stream, fwd2::kSmem, 2);
+      if (rc) return rc;
+    }
+    return DS_OK;
+  }
   const int max_tiles = fwd ? lstm_max_tiles() : lstm_bwd_max_tiles();
   if (max_tiles < 1) return fail_arg("device too small for the recurrent kernel");
   LstmParams P;
