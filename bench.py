@@ -251,8 +251,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     def step(k: int):
         j = k % q
+        lr = learning_rate(sched, 1, j, q)
+        if strategy in ("single", "adpsgd"):  # gradient + local momentum SGD fused in one graph
+            L.train_step(idx_dev[j], lr, device_idx=True)
+            if strategy == "adpsgd":
+                peer = adpsgd_partner(rank, world, k + 1)
+                group.mix(peer) if group is not None else nccl_mix(peer)
+            return
         L.gradient_device(idx_dev[j], B)
-        sync(k, learning_rate(sched, 1, j, q))
+        sync(k, lr)
 
     for k in range(args.warmup):
         step(k)
@@ -280,8 +287,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     frames = args.steps * B * T * world
     value = frames / (ms / 1e3)
     # fwd/bwd kernels + the strategy's sync kernels (sgd+aux / barriers + shard step or mix + aux)
-    sync_launches = {"single": 2, "ssgd": 4 if group is not None else 2, "adpsgd": 6 if group is not None else 3,
-                     "hadpsgd": 10}[strategy]
+    sync_launches = {"single": 0, "ssgd": 4 if group is not None else 2, "adpsgd": 4 if group is not None else 2,
+                     "hadpsgd": 10}[strategy]  # fused train steps count their SGD launches in kernel_count()
     launches_per_step = L.kernel_count() + sync_launches
 
     # ---- end to end through the public Learner API (host indices in, loss out)
@@ -292,8 +299,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     t0 = time.perf_counter()
     for k in range(e2e_steps):
         j = k % q
-        L.gradient(mine[j])
-        sync(args.warmup + args.steps + k, learning_rate(sched, 1, j, q))
+        lr = learning_rate(sched, 1, j, q)
+        if strategy in ("single", "adpsgd"):
+            L.train_step(mine[j], lr)
+            if strategy == "adpsgd":
+                peer = adpsgd_partner(rank, world, args.warmup + args.steps + k + 1)
+                group.mix(peer) if group is not None else nccl_mix(peer)
+        else:
+            L.gradient(mine[j])
+            sync(args.warmup + args.steps + k, lr)
         _ = L.mean_loss()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0

@@ -67,6 +67,16 @@ int ds_blstm_fwd_bwd(ds_blstm* h, const int64_t* idx, int32_t B, float* grad, fl
                      ds_stream_t stream);
 
 /* K13: evaluate/heldout_loss forward only (objectives.py:223-233, 286-291). */
+/* One run_single / ADPSGD-local training step in a single call (the
+ * reference's gradient(...) followed by sgd_step(...), engines/single.py:
+ * 49-55, optim.py:109-121): forward, backward into `grad`, and the momentum
+ * update v <- mu v + g, theta <- theta - lr v with the bf16 operand snapshot
+ * refreshed.  Each layer's update starts as soon as its gradient is final and
+ * runs beside the next layer's BPTT; arithmetic is identical to
+ * ds_blstm_fwd_bwd + ds_sgd_momentum. */
+int ds_blstm_train_step(ds_blstm* h, const int64_t* idx, int32_t B, float* theta, float* vel, float* grad, float lr,
+                        float mu, float* loss_sum, int32_t* nonfinite, ds_stream_t stream);
+
 int ds_blstm_loss(ds_blstm* h, const int64_t* idx, int32_t B, float* loss_sum, int32_t* nonfinite,
                   ds_stream_t stream);
 

@@ -32,6 +32,7 @@ SIGNATURES = {
     "ds_blstm_cast_snapshot": (_I32, [_VP, _VP, _VP]),
     "ds_blstm_fwd_bwd": (_I32, [_VP, _VP, _I32, _VP, _VP, _VP, _VP]),
     "ds_blstm_loss": (_I32, [_VP, _VP, _I32, _VP, _VP, _VP]),
+    "ds_blstm_train_step": (_I32, [_VP, _VP, _I32, _VP, _VP, _VP, _F32, _F32, _VP, _VP, _VP]),
     "ds_sgd_momentum": (_I32, [_VP, _VP, _VP, _F32, _F32, _I64, _VP, _VP, _VP]),
     "ds_adpsgd_mix": (_I32, [_VP, _VP, _I64, _VP]),
     "ds_group_reduce": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _I64, _I32, _F32, _F32, _I32, _F32, _VP]),

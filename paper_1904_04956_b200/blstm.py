@@ -232,6 +232,30 @@ class Learner:
                                         self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
                    "ds_blstm_fwd_bwd")
 
+    def train_step(self, batch, lr: float, device_idx: bool = False) -> None:
+        """gradient(...) then sgd_step(...) in one fused graph (engines/single.py:
+        49-55): each layer's momentum update starts as soon as its gradient is
+        final and runs beside the next layer's BPTT.  `batch` is a host index
+        array, or (device_idx=True) a device int64 tensor of indices."""
+        if lr <= 0:
+            raise ValueError(f"learning rate must be > 0, got {lr}")
+        if device_idx:
+            import torch
+
+            B = int(batch.shape[0])
+            if not 1 <= B <= self.max_batch:
+                raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
+            with torch.cuda.stream(self.stream):
+                self.idx[:B].copy_(batch, non_blocking=True)
+        else:
+            B = self._upload_batch(batch)
+        self.batch = B
+        lib = _lib.load()
+        _lib.check(lib.ds_blstm_train_step(self.handle, self.idx.data_ptr(), B, self.theta.data_ptr(),
+                                           self.vel.data_ptr(), self.grad.data_ptr(), float(lr), self.mu,
+                                           self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
+                   "ds_blstm_train_step")
+
     def set_grad_scale(self, frames_total: float) -> None:
         """CE gradient divisor for the next gradients (0 = this batch's frames)."""
         _lib.check(_lib.load().ds_blstm_set_grad_scale(self.handle, float(frames_total)), "ds_blstm_set_grad_scale")

@@ -48,6 +48,10 @@ struct ds_blstm {
   float* biaspart = nullptr;  // fused bias-gradient partials (CE grad epilogue / BPTT kernel)
   float* splitk = nullptr;    // split-K fp32 partials of dZ
   uint32_t* counters = nullptr;
+  float* d_lr = nullptr;  // fused training step: learning rate read by the SGD kernels
+  // fused training step: per-layer SGD on a side stream while the next BPTT runs
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork[kMaxLayers + 2] = {}, ev_join[kMaxLayers + 2] = {};
   // graph cache
   struct Key {
     int B;
@@ -57,9 +61,12 @@ struct ds_blstm {
     int* flag;
     int bwd;
     float gscale;
+    float* theta;
+    float* vel;
+    float mu;
     bool operator==(const Key& o) const {
       return B == o.B && idx == o.idx && grad == o.grad && loss == o.loss && flag == o.flag && bwd == o.bwd &&
-             gscale == o.gscale;
+             gscale == o.gscale && theta == o.theta && vel == o.vel && mu == o.mu;
     }
   };
   struct Entry {
@@ -150,6 +157,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
     h->splitk = a.take<float>(base, s1 > s2 ? s1 : s2);
   }
   h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64);
+  h->d_lr = a.take<float>(base, 4);
   *total = a.off + 256;
   return DS_OK;
 }
@@ -180,7 +188,30 @@ int mark(ds_blstm* h, int kind, cudaStream_t s) {
 
 // ---------------------------------------------------------------------------
 // The step schedule.  Forward always runs; backward when `grad` != nullptr.
-int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, int* flag, cudaStream_t s) {
+// Fused momentum SGD (K9+K2) of the parameter block [off, off + n) once its
+// gradient is final.  side: on the handle's side stream (<= 16 SMs, the ones
+// a recurrence leaves free), forked from / joined back into `s`.
+struct SgdCtx {
+  float* theta = nullptr;
+  float* vel = nullptr;
+  float mu = 0.f;
+  int nfork = 0;
+};
+int sgd_segment(ds_blstm* h, SgdCtx& c, float* grad, int* flag, int64_t off, int64_t n, bool side, cudaStream_t s) {
+  if (!c.theta) return DS_OK;
+  if (!side)
+    return op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, 0, s);
+  const int k = c.nfork++;
+  DS_CUDA_TRY(cudaEventRecord(h->ev_fork[k], s));
+  DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork[k], 0));
+  int rc = op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, 16, h->side);
+  if (rc) return rc;
+  DS_CUDA_TRY(cudaEventRecord(h->ev_join[k], h->side));
+  return DS_OK;
+}
+
+int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, int* flag, cudaStream_t s,
+               SgdCtx sg = SgdCtx()) {
   const ModelLayout& L = h->L;
   const int T = h->T;
   const int N = T * B;
@@ -341,6 +372,8 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     if (Sb > 1) TRY(op_splitk_f32(h->splitk, Sb, (int64_t)bott * kLayerOut, grad + L.off_wb, s));
     TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, s));
     nl += Sb > 1 ? 4 : 3;
+    // bottleneck + output layer gradients are final: update them beside BPTT_{L-1}
+    TRY(sgd_segment(h, sg, grad, flag, L.off_wb, L.total - L.off_wb, true, s));
   }
   for (int l = Lh - 1; l >= 0; --l) {
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], h->dy,
@@ -384,6 +417,14 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     nl += 2;
+    // layer l's gradients are final: update them beside BPTT_{l-1} (layer 0 on the critical path)
+    TRY(sgd_segment(h, sg, grad, flag, L.off_wih[l], L.off_b[l] + kGates2 - L.off_wih[l], l > 0, s));
+  }
+  if (sg.theta) {
+    MARK(PH_OTHER);
+    for (int k = 0; k < sg.nfork; ++k) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_join[k], 0));
+    TRY(op_snapshot_aux(sg.theta, L, h->wih0pad, h->bias_snap, s));
+    nl += L.layers + 2;
   }
   MARK(PH_END);
 #undef MARK
@@ -400,7 +441,8 @@ bool use_graphs() {
   return v == 1;
 }
 
-int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, int* flag, cudaStream_t s) {
+int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, int* flag, cudaStream_t s,
+             SgdCtx sg = SgdCtx()) {
   if (B < 1 || B > h->Bmax) return fail_arg("batch size out of range 1..max_batch");
   if (!h->feats) return fail_arg("dataset not bound (ds_blstm_set_dataset)");
   if (!loss) return fail_arg("loss_sum pointer is required");
@@ -416,8 +458,8 @@ int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, i
   cudaStreamCaptureStatus cs;
   DS_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
   if (!use_graphs() || h->profile || cs != cudaStreamCaptureStatusNone)
-    return issue_step(h, idx, B, grad, loss, flag, s);
-  ds_blstm::Key key{B, idx, grad, loss, flag, grad != nullptr, h->grad_frames};
+    return issue_step(h, idx, B, grad, loss, flag, s, sg);
+  ds_blstm::Key key{B, idx, grad, loss, flag, grad != nullptr, h->grad_frames, sg.theta, sg.vel, sg.mu};
   for (auto& e : h->graphs)
     if (e.key == key) {
       DS_CUDA_TRY(cudaGraphLaunch(e.exec, s));
@@ -426,7 +468,7 @@ int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, i
   cudaStream_t cap;
   DS_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   DS_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-  int rc = issue_step(h, idx, B, grad, loss, flag, cap);
+  int rc = issue_step(h, idx, B, grad, loss, flag, cap, sg);
   cudaGraph_t g = nullptr;
   cudaError_t ce = cudaStreamEndCapture(cap, &g);
   cudaStreamDestroy(cap);
@@ -480,6 +522,11 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
   }
   carve(h, reinterpret_cast<char*>(h->arena), &total);
   e = cudaMemset(h->counters, 0, sizeof(uint32_t) * 64);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+  for (int k = 0; k < kMaxLayers + 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&h->ev_fork[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join[k], cudaEventDisableTiming);
+  }
   if (e != cudaSuccess) {
     cudaFree(h->arena);
     delete h;
@@ -493,6 +540,11 @@ int ds_blstm_destroy(ds_blstm* h) {
   if (!h) return DS_OK;
   cudaSetDevice(h->device);
   for (auto& e : h->graphs) cudaGraphExecDestroy(e.exec);
+  for (int k = 0; k < kMaxLayers + 2; ++k) {
+    if (h->ev_fork[k]) cudaEventDestroy(h->ev_fork[k]);
+    if (h->ev_join[k]) cudaEventDestroy(h->ev_join[k]);
+  }
+  if (h->side) cudaStreamDestroy(h->side);
   if (h->arena) cudaFree(h->arena);
   delete h;
   return DS_OK;
@@ -529,6 +581,24 @@ int ds_blstm_fwd_bwd(ds_blstm* h, const int64_t* idx, int32_t B, float* grad, fl
                      ds_stream_t stream) {
   if (!h || !idx || !grad) return fail_arg("null argument");
   return run_step(h, idx, B, grad, loss_sum, nonfinite, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ds_blstm_train_step(ds_blstm* h, const int64_t* idx, int32_t B, float* theta, float* vel, float* grad, float lr,
+                        float mu, float* loss_sum, int32_t* nonfinite, ds_stream_t stream) {
+  if (!h || !idx || !grad || !theta || !vel) return fail_arg("null argument");
+  if (!(lr > 0.f)) return fail_arg("learning rate must be > 0");
+  if (((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(vel) | reinterpret_cast<uintptr_t>(grad)) &
+       15))
+    return fail_arg("sgd: buffers must be 16-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DS_CUDA_TRY(cudaSetDevice(h->device));
+  // pageable source: staged by the driver before the call returns
+  DS_CUDA_TRY(cudaMemcpyAsync(h->d_lr, &lr, sizeof(float), cudaMemcpyHostToDevice, s));
+  SgdCtx sg;
+  sg.theta = theta;
+  sg.vel = vel;
+  sg.mu = mu;
+  return run_step(h, idx, B, grad, loss_sum, nonfinite, s, sg);
 }
 
 int ds_blstm_loss(ds_blstm* h, const int64_t* idx, int32_t B, float* loss_sum, int32_t* nonfinite,

@@ -230,6 +230,62 @@ __global__ void sgd_kernel(float* __restrict__ theta, float* __restrict__ v, con
   if (bad && flag) atomicOr(flag, 1);
 }
 
+// K9 for the fused training step: lr read from device memory (the captured
+// step graph is reused while the schedule changes lr), two float4 per thread
+// per iteration so a small grid (the SMs a recurrence leaves free) still
+// keeps enough bytes in flight.  Same rounding order as sgd_kernel.
+__global__ void sgd_lr_kernel(float* __restrict__ theta, float* __restrict__ v, const float* __restrict__ g,
+                              const float* __restrict__ lr_dev, float mu, int64_t n, __nv_bfloat16* __restrict__ snap,
+                              int* __restrict__ flag) {
+  const float lr = *lr_dev;
+  const int64_t n4 = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n4; i0 += 2 * stride) {
+    float4 w[2], vv[2], gg[2];
+    const int64_t idx[2] = {i0, i0 + stride};
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (idx[u] < n4) {
+        w[u] = reinterpret_cast<float4*>(theta)[idx[u]];
+        vv[u] = reinterpret_cast<float4*>(v)[idx[u]];
+        gg[u] = reinterpret_cast<const float4*>(g)[idx[u]];
+      }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (idx[u] >= n4) continue;
+      bad |= !(isfinite(gg[u].x) && isfinite(gg[u].y) && isfinite(gg[u].z) && isfinite(gg[u].w));
+      vv[u].x = __fadd_rn(__fmul_rn(vv[u].x, mu), gg[u].x);
+      vv[u].y = __fadd_rn(__fmul_rn(vv[u].y, mu), gg[u].y);
+      vv[u].z = __fadd_rn(__fmul_rn(vv[u].z, mu), gg[u].z);
+      vv[u].w = __fadd_rn(__fmul_rn(vv[u].w, mu), gg[u].w);
+      w[u].x = __fsub_rn(w[u].x, __fmul_rn(lr, vv[u].x));
+      w[u].y = __fsub_rn(w[u].y, __fmul_rn(lr, vv[u].y));
+      w[u].z = __fsub_rn(w[u].z, __fmul_rn(lr, vv[u].z));
+      w[u].w = __fsub_rn(w[u].w, __fmul_rn(lr, vv[u].w));
+      reinterpret_cast<float4*>(theta)[idx[u]] = w[u];
+      reinterpret_cast<float4*>(v)[idx[u]] = vv[u];
+      if (snap) {
+        __nv_bfloat162 a = __floats2bfloat162_rn(w[u].x, w[u].y), b = __floats2bfloat162_rn(w[u].z, w[u].w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&a);
+        pk.y = *reinterpret_cast<uint32_t*>(&b);
+        reinterpret_cast<uint2*>(snap)[idx[u]] = pk;
+      }
+    }
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float gv = g[i];
+    bad |= !isfinite(gv);
+    float vn = __fadd_rn(__fmul_rn(v[i], mu), gv);
+    float w = __fsub_rn(theta[i], __fmul_rn(lr, vn));
+    v[i] = vn;
+    theta[i] = w;
+    if (snap) snap[i] = __float2bfloat16_rn(w);
+  }
+  if (bad && flag) atomicOr(flag, 1);
+}
+
 __global__ void cast_kernel(const float* __restrict__ theta, int64_t n, __nv_bfloat16* __restrict__ snap) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     snap[i] = __float2bfloat16_rn(theta[i]);
@@ -399,6 +455,19 @@ int op_sgd(float* theta, float* v, const float* g, float lr, float mu, int64_t n
   if (((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(g)) & 15))
     return fail_arg("sgd: buffers must be 16-byte aligned");
   sgd_kernel<<<ew_grid(n / 4 + 1), kEW, 0, s>>>(theta, v, g, lr, mu, n, snap, flag);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+int op_sgd_lr(float* theta, float* v, const float* g, const float* lr_dev, float mu, int64_t n, __nv_bfloat16* snap,
+              int* flag, int max_blocks, cudaStream_t s) {
+  if (((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(g)) & 15))
+    return fail_arg("sgd: buffers must be 16-byte aligned");
+  const int threads = max_blocks > 0 ? 1024 : kEW;
+  int64_t blocks = (n / 8 + threads - 1) / threads;
+  const int64_t cap = max_blocks > 0 ? max_blocks : (int64_t)num_sms() * 8;
+  blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
+  sgd_lr_kernel<<<(int)blocks, threads, 0, s>>>(theta, v, g, lr_dev, mu, n, snap, flag);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }

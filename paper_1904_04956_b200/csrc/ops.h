@@ -20,6 +20,9 @@ int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt,
                   float* loss_sum, int* flag, cudaStream_t s);
 int op_sgd(float* theta, float* v, const float* g, float lr, float mu, int64_t n, __nv_bfloat16* snap, int* flag,
            cudaStream_t s);
+// lr from device memory; max_blocks > 0: at most that many 1024-thread blocks
+int op_sgd_lr(float* theta, float* v, const float* g, const float* lr_dev, float mu, int64_t n, __nv_bfloat16* snap,
+              int* flag, int max_blocks, cudaStream_t s);
 int op_cast(const float* theta, int64_t n, __nv_bfloat16* snap, cudaStream_t s);
 int op_snapshot_aux(const float* theta, const ModelLayout& L, __nv_bfloat16* wih0pad, float* bias_snap,
                     cudaStream_t s);

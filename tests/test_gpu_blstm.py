@@ -142,3 +142,31 @@ def ctypes_arr(ts):
     import ctypes
 
     return (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+
+
+@pytest.mark.parametrize("layers,B,T,classes", [(3, 32, 5, 512), (2, 256, 21, 1024)])
+def test_fused_train_step_equals_gradient_then_sgd(layers, B, T, classes):
+    """ds_blstm_train_step (per-layer SGD beside the next BPTT) is bit-identical
+    to ds_blstm_fwd_bwd followed by ds_sgd_momentum, over several steps (so the
+    refreshed snapshot, padded W_ih0 and bias copies are exercised too)."""
+    obj = BlstmObjective(layers=layers, classes=classes, frames=T)
+    spec = _spec(obj)
+    x, y, _, _ = O.make_dataset(spec, 3 * B, seed=7)
+    w = O.initial_weights(spec, 7)
+    data = DeviceDataset(x, y)
+    A = Learner(obj, data, max_batch=B, theta0=w)
+    R = Learner(obj, data, max_batch=B, theta0=w)
+    rng = np.random.default_rng(1)
+    for step, lr in enumerate((0.05, 0.02, 0.08)):
+        batch = rng.permutation(len(x))[:B]
+        A.train_step(batch, lr)
+        R.gradient(batch)
+        R.sgd_step(lr)
+        A.check_finite()
+        R.check_finite()
+        assert A.mean_loss() == R.mean_loss(), step
+        for name in ("grad", "vel", "theta"):
+            a, r = getattr(A, name), getattr(R, name)
+            assert torch.equal(a, r), (step, name, (a - r).abs().max().item())
+    A.close()
+    R.close()
