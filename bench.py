@@ -334,9 +334,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     rec_flops = 2 * obj.layers * 2.0 * N * (8 * 512) * 512  # forward h W_hh^T + backward dh = dG W_hh
     gemm_flops = flops_frame * N - rec_flops
     gemm_tfs = gemm_flops / (ph["gemm"] * 1e-3) / 1e12 if ph["gemm"] > 0 else 0.0
+    traffic = None  # DRAM bytes of the same GEMM launches of one step, from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1c_gemm_traffic.json")) as f:
+            tj = json.load(f)
+        if B == 256 and obj.layers == 6:
+            traffic = {"bytes_per_step": tj["gemm_dram_bytes_per_step"], "launches": tj["gemm_launches_per_step"],
+                       "source": "profiles/r1c_gemm_traffic.json (ncu dram__bytes_read+write)"}
+    except Exception:
+        pass
     roof = {"bound": "tensor", "kernel": "gemm_kernel (tcgen05 bf16, all GEMM launches of one step)",
             "achieved": round(gemm_tfs, 1), "peak": burst, "unit": "TFLOP/s", "frac": round(gemm_tfs / burst, 4),
-            "peak_kind": f"{peak_kind} burst bf16", "traffic": None,
+            "peak_kind": f"{peak_kind} burst bf16", "traffic": traffic,
+            "algorithmic_flop_per_step": gemm_flops,
             "step_tensor_frac": round(value / world * flops_frame / 1e12 / sustained, 4),
             "phase_ms": {k: round(v, 3) for k, v in ph.items()}}
 
