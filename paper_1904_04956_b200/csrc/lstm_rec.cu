@@ -13,22 +13,15 @@
 // so a CTA that owns 32 hidden units owns 128 contiguous gate rows and the
 // cell update is thread-local (one thread = one batch row).
 //
-// Forward CTA (dir, batch tile of 128, unit block of 32):
-//   W_hh[dir][unit block] (128 x 512 bf16, 128 KB) stays resident in smem.
-//   step s: acc[128 batch, 128 gate rows] = h_prev[128, 512] . W^T (tcgen05,
-//   M=128 N=128 K=512, A streamed by TMA from L2 in 64-unit chunks); the
-//   epilogue (8 warps: 4 TMEM lane quadrants x 2 column halves) adds the
-//   prefetched input projection, applies sigmoid/tanh (MUFU tanh.approx),
-//   updates c (registers) and h, then publishes a per-CTA step flag.
-// Backward CTA (dir, batch tile, unit block of 32):
-//   W_hh[dir][K slice][unit block] resident (MN-major B operand: no transposed copy).
-//   step s: acc[128 batch, 32 units] = dG_prev[128, 2048] . W^T, epilogue adds
-//   dY, runs the cell backward, writes dG_t and publishes its flag.
+// Forward (lstm_fwd2_kernel): CTA pairs with the batch as the MMA's N
+//   operand and W_hh rows stationary as M (see the kernel's comment).
+// Backward (lstm_bwd_kernel): CTA = (dir, 128-row batch tile, 64 units, K
+//   slice of 512 gate rows) in 4-CTA clusters; W_hh[dir][K slice][units]
+//   resident as an MN-major operand; partial dh exchanged through DSMEM.
 // Dataflow instead of a group barrier: the producer of every CTA waits only
-// for the (one or two) CTAs that produced the 64-column chunk it is about to
-// load, so chunk k's MMA overlaps the epilogues still running elsewhere.
-// The grid (<= #SMs, one CTA per SM) is launched cooperatively so every CTA
-// of a group is co-resident.
+// for the CTAs that produced the chunk it is about to load, so chunk k's MMA
+// overlaps the epilogues still running elsewhere.  Every CTA of a (direction,
+// batch tile) group must be co-resident: grids stay <= 128 CTAs, one per SM.
 #include "ds_internal.h"
 #include "ds_ptx.cuh"
 #include "lstm_rec.h"
@@ -42,14 +35,8 @@ namespace {
 constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 256;
-constexpr int kUnits = 32;            // hidden units per CTA
-constexpr int kRows = 4 * kUnits;     // gate rows per CTA
 constexpr int kH = 512;               // hidden units per direction
-constexpr int kUblk = kH / kUnits;    // 16 unit blocks per direction
-constexpr int kStages = 6;
 constexpr int kTileA = 128 * 64 * 2;  // one 128x64 bf16 A box (16 KB)
-constexpr int kWBytes = 128 * 1024;   // resident weight slice
-constexpr size_t kSmemBytes = 1024 + kWBytes + kStages * kTileA + 256;
 
 __device__ __forceinline__ void bf16x8_to_f32(uint4 w, float* out) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
@@ -143,247 +130,6 @@ __device__ __forceinline__ void publish(uint32_t* flag, uint32_t value, int vari
 constexpr int kTraceSlots = 6;
 __device__ __forceinline__ void trace_mark(uint64_t* trace, int T, int s, int k) {
   if (trace) trace[((size_t)blockIdx.x * T + s) * kTraceSlots + k] = globaltimer();
-}
-
-// ============================================================================
-// Forward: CTA = (dir, batch tile, unit block of 32 units = 128 gate rows),
-// clusters of 8 unit blocks.  W_hh slice 128 x 512 bf16 (128 KB) resident.
-// The h_prev tile (128 rows x 512) is shared by all CTAs of a group, so each
-// of its eight 64-unit chunks is fetched from L2 ONCE per cluster: cluster
-// rank k waits for the flags of the two unit blocks that produce chunk k and
-// multicasts it into all eight CTAs; every CTA's MMA completion is multicast
-// back to the issuers' stage-empty barriers.  Warp 3 publishes the step flag
-// after the epilogue warps stored h_t; the BPTT state (gates, c) is written
-// after that hand-off so its stores are not drained on the critical path.
-namespace fwd {
-template <int U>
-struct Cfg {
-  static constexpr int kU = U;                        // units per CTA (16 or 32)
-  static constexpr int kR = 4 * U;                    // gate rows per CTA
-  static constexpr int kUb = kH / U;                  // unit blocks per direction
-  // cluster size: 8-CTA clusters cannot all be co-resident at 128 CTAs (only
-  // ~15 fit), so the 128-CTA U=16 grid uses clusters of 4
-  static constexpr int kCl = U == 32 ? 8 : 4;
-  static constexpr int kWB = kR * kH * 2;             // resident W slice bytes
-  static constexpr int kStagesF = U == 32 ? 6 : 8;    // U=16: the whole h tile in flight
-  static constexpr size_t kSmem = 1024 + kWB + kStagesF * kTileA + 256;
-  static constexpr int kUT = U / 2;                   // units per epilogue thread
-};
-constexpr int kPubBar = 2;  // named barriers 2/3: epilogue <-> publisher warp hand-offs
-}  // namespace fwd
-
-template <int U>
-__global__ void __launch_bounds__(kThreads, 1) lstm_fwd_kernel(const __grid_constant__ LstmParams P) {
-  using C = fwd::Cfg<U>;
-  constexpr int kU = C::kU, kR = C::kR, kUb = C::kUb, kCl = C::kCl, kWB = C::kWB, kStagesF = C::kStagesF;
-  constexpr int kUT = C::kUT;
-  using fwd::kPubBar;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sW = sm;
-  uint8_t* sA = sW + kWB;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sA + kStagesF * kTileA);
-  uint64_t* empty = full + kStagesF;
-  uint64_t* wbar = empty + kStagesF;
-  uint64_t* tfull = wbar + 1;    // [2] double-buffered accumulators: step s uses buffer s & 1
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const int ublk = blockIdx.x % kUb;
-  const int btile = (blockIdx.x / kUb) % P.n_btile;
-  const int dir = blockIdx.x / (kUb * P.n_btile);
-  const int crank = (int)cluster_ctarank();  // == ublk % kCl
-  const uint16_t all = (uint16_t)((1u << kCl) - 1);
-  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kGroupFlagWords;
-  const int T = P.T, B = P.B;
-  const int brow0 = P.b0 + btile * 128;
-
-  if (warp == 1 && lane == 0) {
-    for (int i = 0; i < kStagesF; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kCl);  // one multicast commit per cluster CTA
-    }
-    mbar_init(wbar, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiThreads);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 2 * kR);
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&P.tmA);
-      tma_prefetch_desc(&P.tmW);
-      mbar_arrive_expect_tx(wbar, kWB);
-      for (int kb = 0; kb < kH / 64; ++kb)
-        tma_load_2d(sW + kb * kR * 128, &P.tmW, wbar, kb * 64, dir * 4 * kH + ublk * kR);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int s = 0; s < T; ++s) {
-        const int t = dir == 0 ? s : T - 1 - s;
-        const int tprev = dir == 0 ? t - 1 : t + 1;
-        const int arow = (tprev + 1) * B + brow0;
-        for (int kb = 0; kb < kH / 64; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);  // every cluster CTA freed this stage
-          mbar_arrive_expect_tx(&full[stage], kTileA);
-          if (kb % kCl == crank) {
-            if (s > 0) {  // chunk kb = units kb*64 .. +64 <- unit blocks kb*64/kU ..
-              constexpr int kPer = 64 / kU;
-              if (kPer == 4) {  // blocks 4kb..4kb+3: one line
-                wait_flags4(fwd_flag(flags, 4 * kb), (uint32_t)s);  // acquire included
-              } else {
-#pragma unroll
-                for (int u = 0; u < kPer; ++u) wait_flag(fwd_flag(flags, kPer * kb + u), (uint32_t)s);
-                (void)ld_acquire_gpu(fwd_flag(flags, kPer * kb + kPer - 1));
-              }
-              fence_proxy_async_global();
-            }
-            tma_load_2d_mc(sA + stage * kTileA, &P.tmA, &full[stage], dir * kH + kb * 64, arow, all);
-            if (P.trace && blockIdx.x < kCl)  // debug: chunk issue times of cluster 0
-              P.trace[(size_t)gridDim.x * T * kTraceSlots + ((size_t)s * 8 + kb) * 2] = globaltimer();
-          }
-          if (kb == 0) trace_mark(P.trace, T, s, 0);
-          if (++stage == kStagesF) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        trace_mark(P.trace, T, s, 1);
-      }
-    }
-  } else if (warp == 1) {
-    mbar_wait(wbar, 0);
-    const uint32_t idesc = idesc_bf16_f32(128, kR, 0, 0);
-    const uint32_t wbase = smem_u32(sW);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int s = 0; s < T; ++s) {
-      const int acc = s & 1;
-      mbar_wait(&tempty[acc], ((s >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t dacc = tmem + acc * kR;
-      for (int kb = 0; kb < kH / 64; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (P.trace && blockIdx.x == 0 && lane == 0)  // debug: chunk arrival times at CTA 0
-          P.trace[(size_t)gridDim.x * T * kTraceSlots + ((size_t)s * 8 + kb) * 2 + 1] = globaltimer();
-        if (elect_one()) {
-          const uint32_t abase = smem_u32(sA + stage * kTileA);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint64_t ad = smem_desc_sw128(abase + k * 32, 16, 1024);
-            uint64_t bd = smem_desc_sw128(wbase + kb * kR * 128 + k * 32, 16, 1024);
-            mma_bf16_ss(dacc, ad, bd, idesc, (kb | k) != 0);
-          }
-          mma_commit_mc(&empty[stage], all);
-          if (kb == kH / 64 - 1) mma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-        if (++stage == kStagesF) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else if (warp == 3) {
-    // publisher: h_t of all 256 epilogue threads stored -> release the flag
-    for (int s = 0; s < T; ++s) {
-      named_bar_sync(kPubBar, kEpiThreads + 32);
-      if (lane == 0) {
-        trace_mark(P.trace, T, s, 5);
-        st_release_gpu(fwd_flag(flags, ublk), (uint32_t)(s + 1));
-        trace_mark(P.trace, T, s, 4);
-      }
-      __syncwarp();
-      // let the epilogue write the BPTT state only once the release is out
-      asm volatile("bar.arrive %0, %1;" ::"n"(kPubBar + 1), "n"(kEpiThreads + 32) : "memory");
-    }
-  } else if (warp >= kEpiWarp0) {
-    const uint32_t e = warp - kEpiWarp0;
-    const uint32_t q = e & 3;
-    const uint32_t hf = e >> 2;  // gate rows hf*4kUT .. = units hf*kUT .. +kUT of the block
-    const int r = q * 32 + lane;
-    const int b = brow0 + r;
-    const bool ok = (r + btile * 128 < P.nb) && b < B;
-    const uint32_t tcol = tmem + ((q * 32) << 16) + hf * 4 * kUT;
-    const int col_g = dir * 4 * kH + ublk * kR + hf * 4 * kUT;
-    const int col_u = dir * kH + ublk * kU + hf * kUT;
-    float creg[kUT];
-#pragma unroll
-    for (int u = 0; u < kUT; ++u) creg[u] = 0.f;
-    for (int s = 0; s < T; ++s) {
-      const int t = dir == 0 ? s : T - 1 - s;
-      const size_t n = (size_t)t * B + b;
-      __nv_bfloat16* grow = P.gates + n * (8 * kH) + col_g;
-      uint4 gpre[kUT / 2];
-      if (ok) {
-#pragma unroll
-        for (int j = 0; j < kUT / 2; ++j) gpre[j] = reinterpret_cast<const uint4*>(grow)[j];
-      }
-      mbar_wait(&tfull[s & 1], (s >> 1) & 1);
-      tc_fence_after();
-      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
-      float v[4 * kUT];
-#pragma unroll
-      for (int c = 0; c < 4 * kUT; c += 32) tmem_ld32(tcol + (s & 1) * kR + c, v + c);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&tempty[s & 1]);
-      float hv[kUT], cv[kUT];
-      uint4 actp[kUT / 2];
-#pragma unroll
-      for (int j = 0; j < kUT / 2; ++j) {
-        float gi[8];
-        bf16x8_to_f32(gpre[j], gi);
-        float act[8];
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int u = 2 * j + h2;
-          const float ig = sigmoid_fast(v[4 * u + 0] + gi[4 * h2 + 0]);
-          const float fg = sigmoid_fast(v[4 * u + 1] + gi[4 * h2 + 1]);
-          const float gg = tanh_fast(v[4 * u + 2] + gi[4 * h2 + 2]);
-          const float og = sigmoid_fast(v[4 * u + 3] + gi[4 * h2 + 3]);
-          const float cn = fmaf(fg, creg[u], ig * gg);
-          creg[u] = cn;
-          cv[u] = cn;
-          hv[u] = og * tanh_fast(cn);
-          act[4 * h2 + 0] = ig;
-          act[4 * h2 + 1] = fg;
-          act[4 * h2 + 2] = gg;
-          act[4 * h2 + 3] = og;
-        }
-        actp[j] = f32_to_bf16x8(act);
-      }
-      if (ok) {
-        uint4* h4 = reinterpret_cast<uint4*>(P.y + ((size_t)(t + 1) * B + b) * (2 * kH) + col_u);
-#pragma unroll
-        for (int j = 0; j < kUT / 8; ++j) h4[j] = f32_to_bf16x8(hv + 8 * j);
-      }
-      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
-      asm volatile("bar.arrive %0, %1;" ::"n"(kPubBar), "n"(kEpiThreads + 32) : "memory");
-      named_bar_sync(kPubBar + 1, kEpiThreads + 32);
-      if (ok) {  // BPTT state, after the flag release (not drained by it)
-#pragma unroll
-        for (int j = 0; j < kUT / 2; ++j) reinterpret_cast<uint4*>(grow)[j] = actp[j];
-        float4* c4 = reinterpret_cast<float4*>(P.cstate + n * (2 * kH) + col_u);
-#pragma unroll
-        for (int j = 0; j < kUT / 4; ++j) c4[j] = make_float4(cv[4 * j], cv[4 * j + 1], cv[4 * j + 2], cv[4 * j + 3]);
-      }
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();  // no CTA exits while peers may still multicast into it
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 2 * kR);
 }
 
 // ============================================================================
@@ -639,273 +385,6 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
   cluster_sync_all();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair(tmem, 128);
-}
-
-// ============================================================================
-// Forward, batch-as-N with data-as-flag (experiment, DS_FWD_IMPL=d).
-//   CTA = (dir, batch block of 64, 32 units = 128 gate rows); W_hh slice
-//   (128 x 512, 128 KB) resident as the M operand; acc[128 gate rows x 64
-//   batch] (tcgen05 cta_group::1, N = 64).
-//   Y_full's step rows are prefilled with the bf16 pattern 0xFFFF (a NaN no
-//   arithmetic produces: converted NaNs are 0x7FFF), so h itself is the
-//   step flag: producers store h_t with relaxed 16-byte stores and no fence,
-//   and the 8 epilogue warps, once done with step s, poll-load the next
-//   step's 8 chunks straight from L2 (warp k loads chunk k = units k*64..,
-//   64 batch rows x 128 B), swizzle them into the SW128 K-major operand and
-//   hand each chunk to the MMA warp.  No flag round trip and no release
-//   fence sit on the recurrence's critical path.
-namespace fwd3 {
-constexpr int kNB = 64;                 // batch columns (MMA N)
-constexpr int kCtas = kH / 32;          // 16 CTAs per (dir, batch block)
-constexpr int kWB = 128 * kH * 2;       // 128 KB resident W slice
-constexpr int kChunkB = kNB * 128;      // 8 KB: 64 batch rows x 64 units bf16
-constexpr int kBufB = 8 * kChunkB;      // 64 KB: one step's B operand
-constexpr int kHst = kNB * 64;          // h staging: 64 rows x 32 units bf16
-constexpr size_t kSmem = 1024 + kWB + kBufB + kHst + 512;
-constexpr int kEpiWarps = 8;
-constexpr int kEpiT = kEpiWarps * 32;
-constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // two bf16 0xFFFF
-}  // namespace fwd3
-
-__device__ __forceinline__ bool has_sentinel(uint4 w) {
-  // any 16-bit half == 0xFFFF
-  const uint32_t x[4] = {w.x, w.y, w.z, w.w};
-  bool bad = false;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) bad |= ((x[i] & 0xFFFFu) == 0xFFFFu) | ((x[i] >> 16) == 0xFFFFu);
-  return bad;
-}
-__device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
-  uint4 v;
-  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_v4(void* p, uint4 v) {
-  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
-}
-
-__global__ void __launch_bounds__(kThreads, 1) lstm_fwd3_kernel(const __grid_constant__ LstmParams P) {
-  using namespace fwd3;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sW = sm;
-  uint8_t* sB = sW + kWB;                 // [8 chunks][64 rows x 128 B], SW128
-  uint8_t* sH = sB + kBufB;               // [64 rows][32 units] bf16
-  uint64_t* full = reinterpret_cast<uint64_t*>(sH + kHst);  // [8]: chunk k staged for this step
-  uint64_t* wbar = full + 8;
-  uint64_t* tfull = wbar + 1;   // [2]
-  uint64_t* tempty = tfull + 2;  // [2]
-  uint64_t* lbar = tempty + 2;   // [8]: chunk k's TMA landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lbar + 8);
-
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const int cb = blockIdx.x % kCtas;               // unit block of 32
-  const int bb = (blockIdx.x / kCtas) % P.n_btile;  // batch block of 64
-  const int dir = blockIdx.x / (kCtas * P.n_btile);
-  const int T = P.T, B = P.B;
-  const int b0 = P.b0 + bb * kNB;
-  const int rows = min(kNB, P.nb - bb * kNB);      // valid batch rows of this block
-
-  if (warp == 1 && lane == 0) {
-    for (int i = 0; i < 8; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&lbar[i], 1);
-    }
-    mbar_init(wbar, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiT);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 128);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&P.tmW);
-      tma_prefetch_desc(&P.tmA);
-      mbar_arrive_expect_tx(wbar, kWB);
-      const int wrow = dir * 4 * kH + cb * 128;
-      for (int kb = 0; kb < kH / 64; ++kb) tma_load_2d(sW + kb * 16384, &P.tmW, wbar, kb * 64, wrow);
-    }
-  } else if (warp == 1) {
-    mbar_wait(wbar, 0);
-    const uint32_t idesc = idesc_bf16_f32(128, kNB, 0, 0);
-    const uint32_t wbase = smem_u32(sW), bbase = smem_u32(sB);
-    for (int s = 0; s < T; ++s) {
-      const int acc = s & 1;
-      mbar_wait(&tempty[acc], ((s >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t dacc = tmem + acc * kNB;
-      for (int k = 0; k < 8; ++k) {
-        mbar_wait(&full[k], s & 1);
-        tc_fence_after();
-        if (k == 7 && lane == 0) trace_mark(P.trace, T, s, 4);
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            uint64_t ad = smem_desc_sw128(wbase + k * 16384 + kk * 32, 16, 1024);
-            uint64_t bd = smem_desc_sw128(bbase + k * kChunkB + kk * 32, 16, 1024);
-            mma_bf16_ss(dacc, ad, bd, idesc, (k | kk) != 0);
-          }
-          if (k == 7) mma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-      }
-    }
-  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
-    const uint32_t e = warp - kEpiWarp0;
-    const uint32_t q = e & 3, hc = e >> 2;
-    const uint32_t g = lane & 3;
-    const uint32_t b0b = g & 1, b1b = g >> 1;
-    const int uq = (int)(q * 8 + (lane >> 2));
-    const int unit = cb * 32 + uq;
-    const int col0 = (int)(hc * 32 + g * 8);
-    const uint32_t tcol = tmem + ((q * 32) << 16) + hc * 32;
-    const size_t gcol = (size_t)dir * 4 * kH + (size_t)unit * 4;
-    uint8_t* mychunk = sB + e * kChunkB;  // this warp stages chunk k = e (units e*64 ..)
-    float c[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) c[i] = 0.f;
-    unsigned long long spins = 0;
-    for (int s = 0; s < T; ++s) {
-      const int t = dir == 0 ? s : T - 1 - s;
-      const int tprev = dir == 0 ? t - 1 : t + 1;
-      // ---- stage h_{t-1} chunk e (64 rows x 128 B): lane = rows lane, lane+32
-      {
-        const __nv_bfloat16* src = P.y + ((size_t)(tprev + 1) * B + b0) * (2 * kH) + dir * kH + e * 64;
-        if (s > 0 && lane < 2) {
-          // cheap watch: one 16-byte piece of each of the chunk's two producers
-          // (last valid row) -- polling the whole 8 KB would flood L2
-          const __nv_bfloat16* pp = src + (size_t)(rows - 1) * (2 * kH) + lane * 32;
-          uint4 x = ld_relaxed_v4(pp);
-          while (has_sentinel(x) && ++spins < (1ull << 24)) {
-            __nanosleep(32);
-            x = ld_relaxed_v4(pp);
-          }
-        }
-        __syncwarp();
-        if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 0);
-        // optimistic TMA of the whole chunk, then validate it in smem: any
-        // piece still holding the 0xFFFF pattern is re-polled from L2 (rare)
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&lbar[e], kChunkB);
-          tma_load_2d(mychunk, &P.tmA, &lbar[e], dir * kH + e * 64, (tprev + 1) * B + b0);
-        }
-        mbar_wait(&lbar[e], s & 1);
-        if (s > 0) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = lane + 32 * h;
-#pragma unroll
-            for (int c16 = 0; c16 < 8; ++c16) {
-              uint4* dst = reinterpret_cast<uint4*>(mychunk + r * 128 + ((c16 ^ (r & 7)) << 4));
-              uint4 w = *dst;
-              if (r < rows && has_sentinel(w)) {
-                do {
-                  __nanosleep(32);
-                  w = ld_relaxed_v4(src + (size_t)r * (2 * kH) + c16 * 8);
-                } while (has_sentinel(w) && ++spins < (1ull << 24));
-                *dst = w;
-              }
-            }
-          }
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[e]);
-        if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 1);
-      }
-      // ---- prefetch the input projection of my 8 batch rows
-      uint2 gp[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int b = b0 + col0 + i;
-        gp[i] = col0 + i < rows ? *reinterpret_cast<const uint2*>(P.gates + ((size_t)t * B + b) * (8 * kH) + gcol)
-                                : make_uint2(0u, 0u);
-      }
-      mbar_wait(&tfull[s & 1], (s >> 1) & 1);
-      tc_fence_after();
-      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
-      float v[32];
-      tmem_ld32(tcol + (s & 1) * kNB, v);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&tempty[s & 1]);
-      float a1[16], a2[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float send = b1b ? v[i] : v[16 + i];
-        a1[i] = b1b ? v[16 + i] : v[i];
-        a2[i] = __shfl_xor_sync(0xffffffffu, send, 2);
-      }
-      float k1[8], k2[8], r1[8], r2[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float s1 = b0b ? a1[i] : a1[8 + i];
-        const float s2 = b0b ? a2[i] : a2[8 + i];
-        k1[i] = b0b ? a1[8 + i] : a1[i];
-        k2[i] = b0b ? a2[8 + i] : a2[i];
-        r1[i] = __shfl_xor_sync(0xffffffffu, s1, 1);
-        r2[i] = __shfl_xor_sync(0xffffffffu, s2, 1);
-      }
-      float hv[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float x0 = b0b ? (b1b ? r2[i] : r1[i]) : (b1b ? k2[i] : k1[i]);
-        const float x1 = b0b ? (b1b ? k2[i] : k1[i]) : (b1b ? r2[i] : r1[i]);
-        const float x2 = b0b ? (b1b ? r1[i] : r2[i]) : (b1b ? k1[i] : k2[i]);
-        const float x3 = b0b ? (b1b ? k1[i] : k2[i]) : (b1b ? r1[i] : r2[i]);
-        const __nv_bfloat162* gg = reinterpret_cast<const __nv_bfloat162*>(&gp[i]);
-        const float2 g01 = __bfloat1622float2(gg[0]), g23 = __bfloat1622float2(gg[1]);
-        const float ig = sigmoid_fast(x0 + g01.x);
-        const float fg = sigmoid_fast(x1 + g01.y);
-        const float gt = tanh_fast(x2 + g23.x);
-        const float og = sigmoid_fast(x3 + g23.y);
-        c[i] = fmaf(fg, c[i], ig * gt);
-        hv[i] = og * tanh_fast(c[i]);
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(ig, fg), p1 = __floats2bfloat162_rn(gt, og);
-        gp[i].x = *reinterpret_cast<uint32_t*>(&p0);
-        gp[i].y = *reinterpret_cast<uint32_t*>(&p1);
-      }
-      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 5);
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        reinterpret_cast<__nv_bfloat16*>(sH)[(col0 + i) * 32 + uq] = __float2bfloat16_rn(hv[i]);
-      named_bar_sync(1, kEpiT);
-      {
-        const int tid = (int)(e * 32 + lane);  // 64 rows x 4 segments of 8 units
-        const int row = tid >> 2, sg = tid & 3;
-        const uint4 w = reinterpret_cast<const uint4*>(sH)[tid];
-        if (row < rows)  // h_t is the consumers' step flag: relaxed store, no fence
-          st_relaxed_v4(P.y + ((size_t)(t + 1) * B + b0 + row) * (2 * kH) + dir * kH + cb * 32 + sg * 8, w);
-      }
-      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {  // BPTT state
-        if (col0 + i < rows) {
-          const size_t n = (size_t)t * B + b0 + col0 + i;
-          *reinterpret_cast<uint2*>(P.gates + n * (8 * kH) + gcol) = gp[i];
-          P.cstate[n * (2 * kH) + dir * kH + unit] = c[i];
-        }
-      }
-      named_bar_sync(1, kEpiT);  // sH is free again
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 128);
 }
 
 // ============================================================================
@@ -1260,31 +739,11 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
 
 // batch tiles per launch: forward 32 CTAs / tile; backward 64 CTAs / tile in
 // clusters of 4 (cluster placement leaves some SMs unusable: keep <= 128)
-static int fwd_units() {
-  static int u = 0;
-  if (!u) {
-    const char* e = getenv("DS_FWD_UNITS");
-    u = (e && atoi(e) == 32) ? 32 : 16;  // default U=16 (measured 6.8 vs 8.0 us per step)
-  }
-  return u;
-}
-int lstm_max_tiles() { return num_sms() / (2 * (kH / fwd_units())); }
-static int lstm_bwd_max_tiles() { return (num_sms() >= 132 ? 128 : num_sms()) / 64; }
+// <= 128 CTAs per launch: forward 32 CTAs per 64-row batch block, backward
+// 64 CTAs per 128-row batch tile in clusters of 4
+int lstm_max_tiles() { return (num_sms() >= 132 ? 128 : num_sms()) / 64; }
+static int lstm_bwd_max_tiles() { return lstm_max_tiles(); }
 int lstm_counter_words(int B) { return 2 * kGroupFlagWords * ((B + 127) / 128); }
-
-// forward implementation, DS_FWD_IMPL: 'p' batch-as-N CTA pairs with step
-// flags (default, 4.6 us/step at B=256), 'd' batch-as-N with data-as-flag
-// (no release fence, but validation re-polls and producer skew leave it at
-// ~4.6-5.0 us/step), 'm' the batch-as-M kernels (DS_FWD_UNITS=16|32, 5.1)
-static char fwd_impl() {
-  static char v = 0;
-  if (!v) {
-    const char* e = getenv("DS_FWD_IMPL");
-    v = (e && (e[0] == 'm' || e[0] == 'd')) ? e[0] : 'p';
-  }
-  return v;
-}
-static bool fwd_nb() { return fwd_impl() == 'p'; }
 
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
@@ -1292,48 +751,12 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     DS_CUDA_TRY(
         cudaFuncSetAttribute(lstm_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd2::kSmem));
     DS_CUDA_TRY(
-        cudaFuncSetAttribute(lstm_fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd3::kSmem));
-    DS_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)fwd::Cfg<32>::kSmem));
-    DS_CUDA_TRY(cudaFuncSetAttribute(lstm_fwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)fwd::Cfg<16>::kSmem));
-    DS_CUDA_TRY(
         cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmem));
 
     attr_set = true;
   }
   const int B = a.B, T = a.T;
-  if (fwd && fwd_impl() == 'd') {
-    const int max_blocks = num_sms() / (2 * fwd3::kCtas);
-    if (max_blocks < 1) return fail_arg("device too small for the recurrent kernel");
-    LstmParams P;
-    memset(&P, 0, sizeof(P));
-    int rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, 64, 128);
-    if (rc) return rc;
-    rc = make_tmap_2d(&P.tmA, a.y_full, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2 * kH, (uint64_t)(T + 2) * B, 2 * kH * 2,
-                      64, fwd3::kNB);
-    if (rc) return rc;
-    P.gates = a.gates;
-    P.cstate = a.cstate;
-    P.y = a.y_full;
-    P.trace = a.trace;
-    P.B = B;
-    P.T = T;
-    // every step row of Y_full reads "not yet written" until its producer stores it
-    DS_CUDA_TRY(cudaMemsetAsync(a.y_full + (size_t)B * 2 * kH, 0xFF, (size_t)T * B * 2 * kH * 2, stream));
-    const int chunk_rows = max_blocks * fwd3::kNB;
-    for (int b0 = 0; b0 < B; b0 += chunk_rows) {
-      const int nb = (B - b0) < chunk_rows ? (B - b0) : chunk_rows;
-      P.b0 = b0;
-      P.nb = nb;
-      P.n_btile = (nb + fwd3::kNB - 1) / fwd3::kNB;
-      rc = launch_coop((const void*)lstm_fwd3_kernel, 2 * fwd3::kCtas * P.n_btile, P, stream, fwd3::kSmem, 1);
-      if (rc) return rc;
-      P.trace = nullptr;
-    }
-    return DS_OK;
-  }
-  if (fwd && fwd_nb()) {
+  if (fwd) {
     // 32 CTAs (2 directions x 8 pairs x 2) per 64-row batch block
     const int max_blocks = num_sms() / (2 * fwd2::kCtas);
     if (max_blocks < 1) return fail_arg("device too small for the recurrent kernel");
@@ -1364,23 +787,14 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     }
     return DS_OK;
   }
-  const int max_tiles = fwd ? lstm_max_tiles() : lstm_bwd_max_tiles();
+  const int max_tiles = lstm_bwd_max_tiles();
   if (max_tiles < 1) return fail_arg("device too small for the recurrent kernel");
   LstmParams P;
   memset(&P, 0, sizeof(P));
-  int rc;
-  if (fwd) {
-    rc = make_tmap_2d(&P.tmA, a.y_full, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2 * kH, (uint64_t)(T + 2) * B,
-                      2 * kH * 2, 64, 128);
-    if (rc) return rc;
-    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, 64, 4 * fwd_units());
-    if (rc) return rc;
-  } else {
-    rc = make_tmap_2d(&P.tmA, a.dg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 8 * kH, (uint64_t)T * B, 8 * kH * 2, 64, 128);
-    if (rc) return rc;
-    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, bwd::kGU, 64);
-    if (rc) return rc;
-  }
+  int rc = make_tmap_2d(&P.tmA, a.dg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 8 * kH, (uint64_t)T * B, 8 * kH * 2, 64, 128);
+  if (rc) return rc;
+  rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, bwd::kGU, 64);
+  if (rc) return rc;
   P.gates = a.gates;
   P.cstate = a.cstate;
   P.y = a.y_full;
@@ -1388,10 +802,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   P.dg = a.dg;
   P.trace = a.trace;
   P.dbpart = a.dbpart;
-  {
-    const char* v = getenv("DS_LSTM_VARIANT");
-    P.variant = v ? atoi(v) : 7;  // 7: acquire by ld.acquire, no writer-side fences
-  }
+  P.variant = 7;  // acquire by ld.acquire, no writer-side fences
   P.B = B;
   P.T = T;
   const int chunk_rows = max_tiles * 128;
@@ -1402,14 +813,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.n_btile = (nb + 127) / 128;
     P.counters = a.counters + (b0 / 128) * 2 * kGroupFlagWords;
     DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * kGroupFlagWords * P.n_btile, stream));
-    if (fwd)
-      rc = fwd_units() == 16
-               ? launch_coop((const void*)lstm_fwd_kernel<16>, 2 * fwd::Cfg<16>::kUb * P.n_btile, P, stream,
-                             fwd::Cfg<16>::kSmem, fwd::Cfg<16>::kCl)
-               : launch_coop((const void*)lstm_fwd_kernel<32>, 2 * fwd::Cfg<32>::kUb * P.n_btile, P, stream,
-                             fwd::Cfg<32>::kSmem, fwd::Cfg<32>::kCl);
-    else
-      rc = launch_coop((const void*)lstm_bwd_kernel, 64 * P.n_btile, P, stream, bwd::kSmem, bwd::kClB);
+    rc = launch_coop((const void*)lstm_bwd_kernel, 64 * P.n_btile, P, stream, bwd::kSmem, bwd::kClB);
     if (rc) return rc;
     P.trace = nullptr;  // trace only the first chunk
   }
