@@ -179,6 +179,14 @@ DS_DEV void bulk_copy_s2cluster(uint32_t dst_caddr, const void* src, uint32_t by
       "r"(smem_u32(src)), "r"(bytes), "r"(mbar_caddr)
       : "memory");
 }
+// 16-byte store into a peer CTA's shared memory whose bytes complete on the
+// peer's mbarrier (both shared::cluster addresses from mapa).
+DS_DEV void st_async_v4(uint32_t caddr, float4 v, uint32_t bar_caddr) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   caddr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(bar_caddr)
+               : "memory");
+}
 DS_DEV void mbar_arrive_remote(uint32_t caddr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }
