@@ -106,6 +106,18 @@ int ksplit_for(int K, int target) {
   return 1;
 }
 
+// dlogits in 64x64 blocks: the dW_o (MN-major) and dZ (K-major) operand
+// boxes become contiguous 8 KB reads instead of 128-byte pieces of rows 64 KB
+// apart (DS_DLOGITS_ROWMAJOR=1 keeps the row-major layout)
+bool blocked_dlogits(const ds_blstm* h) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("DS_DLOGITS_ROWMAJOR");
+    off = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !off && h->L.classes % 64 == 0;
+}
+
 struct Arena {
   size_t off = 0;
   template <class T>
@@ -138,7 +150,10 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   h->stats = a.take<float2>(base, (size_t)4 * h->ntiles_c * N);  // four column quarters per tile
   h->tgt = a.take<float>(base, N);
   h->lse = a.take<float>(base, N);
-  h->dlogits = a.take<__nv_bfloat16>(base, (size_t)N * L.classes);
+  {  // row-major [N][C], or 64x64-blocked when C % 64 == 0
+    const int64_t e1 = (int64_t)N * L.classes, e2 = gemm_blocked_elems(N, L.classes);
+    h->dlogits = a.take<__nv_bfloat16>(base, e1 > e2 ? e1 : e2);
+  }
   h->dz = a.take<__nv_bfloat16>(base, (size_t)N * L.bottleneck);
   h->dy = a.take<__nv_bfloat16>(base, (size_t)N * kLayerOut);
   h->dg = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
@@ -309,7 +324,10 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.ldo = C;
     p.scale = 1.0f / (h->grad_frames > 0.f ? h->grad_frames : (float)N);
     p.colpart = getenv("DS_NO_COLSUM") ? nullptr : h->biaspart;
-    TRY(gemm_bf16_output(&p));
+    if (blocked_dlogits(h))  // 64x64 blocks: the two readers below fetch contiguous 8 KB boxes
+      TRY(gemm_blocked_output(&p, N, C));
+    else
+      TRY(gemm_bf16_output(&p));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
@@ -323,11 +341,13 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     gb.nprob = 2;
     GemmProblem& p0 = gb.p[0];  // dW_o = dlogits^T Z
     TRY(gemm_problem(&p0, h->dlogits, C, 1, h->z, bott, 1, C, bott, N));
+    if (blocked_dlogits(h)) TRY(gemm_blocked_a(&p0, h->dlogits, N, C));
     p0.epi = EPI_F32;
     p0.out = grad + L.off_wo;
     p0.ldo = bott;
     GemmProblem& p1 = gb.p[1];  // dZ = dlogits W_o (split-K, fp32 partials)
     TRY(gemm_problem(&p1, h->dlogits, C, 0, h->snap + L.off_wo, bott, 1, N, bott, C));
+    if (blocked_dlogits(h)) TRY(gemm_blocked_a(&p1, h->dlogits, N, C));
     const int S = dz_split(C);
     if (S > 1) {
       p1.epi = EPI_F32;

@@ -69,6 +69,27 @@ int make_tmap_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, 
   return DS_OK;
 }
 
+int make_tmap_4d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, const uint64_t dims[4],
+                 const uint64_t strides_bytes[3], const uint32_t box[4], CUtensorMapSwizzle swizzle) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail_arg("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (strides_bytes[0] & 15) || (strides_bytes[1] & 15) ||
+      (strides_bytes[2] & 15))
+    return fail_arg("TMA operand must be 16-byte aligned with 16-byte multiple strides");
+  cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t st[3] = {strides_bytes[0], strides_bytes[1], strides_bytes[2]};
+  cuuint32_t bx[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(out, dtype, 4, const_cast<void*>(base), d, st, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (4d) failed (%d)", (int)r);
+    return fail_arg(buf);
+  }
+  return DS_OK;
+}
+
 }  // namespace ds
 
 extern "C" const char* ds_last_error(void) { return ds::g_last_error.c_str(); }

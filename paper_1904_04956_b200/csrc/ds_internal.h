@@ -38,6 +38,11 @@ int make_tmap_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, 
                  uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
                  CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B);
 
+// 4D tensor [d3][d2][d1][d0] (d0 contiguous); strides of d1..d3 in bytes.
+int make_tmap_4d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, const uint64_t dims[4],
+                 const uint64_t strides_bytes[3], const uint32_t box[4],
+                 CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B);
+
 // ---------------------------------------------------------------------------
 // GEMM: C[m, n] = sum_k A[m, k] * B[n, k], bf16 operands, fp32 accumulate in
 // TMEM (tcgen05), persistent tile loop, up to kMaxProblems per launch.
@@ -80,6 +85,10 @@ struct GemmProblem {
   int stats_ld;
   float* colpart;         // EPI_CE_GRAD: optional [tiles_m*4][n_valid] column-sum partials
   int c_tma;              // bf16 output stored through smem staging + TMA (tmC valid)
+  // 64x64-blocked [row/64][col/64][64][64] bf16 operand / output (dlogits):
+  // tmA / tmC are then 4D maps over (col%64, row%64, col/64, row/64)
+  int a_blk;
+  int c_blk;
   int ksplit;             // split-K factor (EPI_F32 only): split s writes out + s*split_stride
   long long split_stride;
 };
@@ -108,5 +117,11 @@ int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const v
 int gemm_launch(GemmBatch* batch, cudaStream_t stream);
 // Attach the TMA store map for a bf16 output (call after setting out/ldo/n_valid/m_valid).
 int gemm_bf16_output(GemmProblem* p);
+// 64x64-blocked bf16 matrices (rows x cols, see GemmProblem::a_blk): element
+// count of the buffer, A operand view (call after gemm_problem, sets tmA), and
+// TMA-stored bf16 output view (call after setting out/epi).
+int64_t gemm_blocked_elems(int64_t rows, int64_t cols);
+int gemm_blocked_a(GemmProblem* p, const void* A, int64_t rows, int64_t cols);
+int gemm_blocked_output(GemmProblem* p, int64_t rows, int64_t cols);
 
 }  // namespace ds

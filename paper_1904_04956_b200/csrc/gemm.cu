@@ -24,6 +24,7 @@
 // Pair tiles are walked round-robin over the persistent grid; the two TMEM
 // accumulators let the epilogue of tile i overlap the main loop of tile i+1.
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -99,7 +100,8 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v
 // Stage this warp's 32 rows x 32 bf16 columns (lane = row) in smem with the
 // 64-byte swizzle and TMA-store the box at (col, row0): full 64 B row
 // segments reach L2 instead of 16 B pieces of 32 different rows.
-__device__ __forceinline__ void store_box_tma(const CUtensorMap* map, uint8_t* stg, const float* v, int col, int row0) {
+__device__ __forceinline__ void store_box_tma(const CUtensorMap* map, uint8_t* stg, const float* v, int col, int row0,
+                                              int blk = 0) {
   const uint32_t lane = lane_id();
   if (lane == 0) bulk_wait_read0();  // the previous box has left this buffer
   __syncwarp();
@@ -117,7 +119,10 @@ __device__ __forceinline__ void store_box_tma(const CUtensorMap* map, uint8_t* s
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
-    tma_store_2d(map, stg, col, row0);
+    if (blk)
+      tma_store_4d(map, stg, col & 63, row0 & 63, col >> 6, row0 >> 6);
+    else
+      tma_store_2d(map, stg, col, row0);
     bulk_commit();
   }
 }
@@ -182,7 +187,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
           const uint32_t bar = full_c + stage * 8;
           const int k0 = kb * BK;
-          if (!P.a_mn) {
+          if (P.a_blk) {  // 64x64-blocked A: whole 8 KB blocks (box spans 2 row blocks when K-major)
+            if (!P.a_mn) {
+              tma_load_4d_pair(sA, &P.tmA, bar, 0, 0, k0 >> 6, m0 >> 6);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_4d_pair(sA + j * 8192, &P.tmA, bar, 0, 0, (m0 >> 6) + j, k0 >> 6);
+            }
+          } else if (!P.a_mn) {
             tma_load_2d_pair(sA, &P.tmA, bar, k0, m0);
           } else {
 #pragma unroll
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] *= sc;
           if (P.c_tma) {
-            store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, rt * BM + q * 32);
+            store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, rt * BM + q * 32, P.c_blk);
           } else if (row_ok) {
             store_bf16x16(orow + nb, v);
             store_bf16x16(orow + nb + 16, v + 16);
@@ -479,6 +492,44 @@ int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const v
   p->m_valid = M;
   p->scale = 1.f;
   p->ksplit = 1;
+  return DS_OK;
+}
+
+// 64x64-blocked bf16 matrix [ceil(rows/64)][ceil(cols/64)][64][64] (dlogits)
+static void blk_dims(int64_t rows, int64_t cols, uint64_t dims[4], uint64_t strides[3]) {
+  const uint64_t nrb = (rows + 63) / 64, ncb = (cols + 63) / 64;
+  dims[0] = 64;
+  dims[1] = 64;
+  dims[2] = ncb;
+  dims[3] = nrb;
+  strides[0] = 128;
+  strides[1] = 8192;
+  strides[2] = ncb * 8192;
+}
+int64_t gemm_blocked_elems(int64_t rows, int64_t cols) { return ((rows + 63) / 64) * ((cols + 63) / 64) * 4096; }
+
+int gemm_blocked_a(GemmProblem* p, const void* A, int64_t rows, int64_t cols) {
+  uint64_t dims[4], strides[3];
+  blk_dims(rows, cols, dims, strides);
+  // K-major (rows = M): one box = 2 row blocks x 1 column block = 128 x 64;
+  // MN-major (rows = K): one box = 1 x 1 block (64 x 64), two per k-block
+  const uint32_t box[4] = {64, 64, 1, p->a_mn ? 1u : 2u};
+  int rc = make_tmap_4d(&p->tmA, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dims, strides, box);
+  if (rc) return rc;
+  p->a_blk = 1;
+  return DS_OK;
+}
+
+int gemm_blocked_output(GemmProblem* p, int64_t rows, int64_t cols) {
+  if (p->epi != EPI_BF16 && p->epi != EPI_CE_GRAD) return fail_arg("TMA store only for bf16 epilogues");
+  uint64_t dims[4], strides[3];
+  blk_dims(rows, cols, dims, strides);
+  const uint32_t box[4] = {32, 32, 1, 1};
+  int rc = make_tmap_4d(&p->tmC, p->out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dims, strides, box,
+                        CU_TENSOR_MAP_SWIZZLE_64B);
+  if (rc) return rc;
+  p->c_tma = 1;
+  p->c_blk = 1;
   return DS_OK;
 }
 
