@@ -22,6 +22,8 @@
 // for the CTAs that produced the chunk it is about to load, so chunk k's MMA
 // overlaps the epilogues still running elsewhere.  Every CTA of a (direction,
 // batch tile) group must be co-resident: grids stay <= 128 CTAs, one per SM.
+#include <cuda_fp16.h>
+
 #include "ds_internal.h"
 #include "ds_ptx.cuh"
 #include "lstm_rec.h"
@@ -407,14 +409,26 @@ constexpr int kGU = 64;                      // units per cluster
 constexpr int kFU = kGU / kKS;               // 16 units finalised per CTA
 constexpr int kKSlice = 4 * kH / kKS;        // 512 gate rows per CTA
 constexpr int kChunks = kKSlice / 64;        // 8 A chunks per step
-constexpr int kStagesB = 6;
+constexpr int kStagesB = 8;                 // the whole step's dG slice in flight
 constexpr int kWBytesB = kGU * kKSlice * 2;  // 64 KB
-constexpr int kRecvSlot = 128 * kFU * 4;     // 8 KB: one source's [128 rows x 16 units] fp32
+// partial dh travels as fp16 scaled by P.xscale (a power of two ~ frames/2,
+// so the mean-loss gradients sit in fp16's normal range; 11-bit mantissa)
+constexpr int kRecvSlot = 128 * kFU * 2;     // 4 KB: one source's [128 rows x 16 units] fp16
 constexpr int kRecvBytes = kKS * kRecvSlot;  // 4 sources
 constexpr int kSendBytes = (kKS - 1) * kRecvSlot;  // staged partials for the 3 peers
 constexpr size_t kSmem = 1024 + kWBytesB + kStagesB * kTileA + kRecvBytes + kSendBytes + 512;
-// [128 rows][16 fp32] slots, 16-byte chunk c of row r stored at chunk c ^ ((r >> 1) & 3)
-__device__ __forceinline__ uint32_t slot_off(int r, int c) { return (uint32_t)(r * 64 + 16 * (c ^ ((r >> 1) & 3))); }
+// [128 rows][16 fp16] slots, 16-byte chunk c of row r stored at chunk c ^ ((r >> 2) & 1)
+__device__ __forceinline__ uint32_t slot_off(int r, int c) { return (uint32_t)(r * 32 + 16 * (c ^ ((r >> 2) & 1))); }
+__device__ __forceinline__ uint4 pack_h8(const float* v, float sc) {
+  uint4 w;
+  uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __half2 h = __floats2half2_rn(v[2 * i] * sc, v[2 * i + 1] * sc);
+    u[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return w;
+}
 }  // namespace bwd
 
 __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_constant__ LstmParams P) {
@@ -423,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = sm;
   uint8_t* sA = sW + kWBytesB;
-  float* recv = reinterpret_cast<float*>(sA + kStagesB * kTileA);  // [kKS][128][16] (swizzled rows)
-  uint8_t* send = reinterpret_cast<uint8_t*>(recv) + kRecvBytes;    // [kKS-1][128][16]
+  uint8_t* recv = sA + kStagesB * kTileA;  // [kKS][128][16] fp16 (swizzled rows)
+  uint8_t* send = recv + kRecvBytes;      // [kKS-1][128][16] fp16
   uint64_t* bars = reinterpret_cast<uint64_t*>(send + kSendBytes);
   uint64_t* full = bars;
   uint64_t* empty = full + kStagesB;
@@ -623,10 +637,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
           uint8_t* slot = f == ks ? reinterpret_cast<uint8_t*>(recv) + ks * kRecvSlot
                                   : send + (f < ks ? f : f - 1) * kRecvSlot;
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<float4*>(slot + slot_off(r, c)) =
-                make_float4(v[f2 * kFU + 4 * c], v[f2 * kFU + 4 * c + 1], v[f2 * kFU + 4 * c + 2],
-                            v[f2 * kFU + 4 * c + 3]);
+          for (int c = 0; c < 2; ++c)
+            *reinterpret_cast<uint4*>(slot + slot_off(r, c)) = pack_h8(v + f2 * kFU + 8 * c, P.xscale);
         }
         fence_proxy_async_smem();
         named_bar_sync(3, kEpiThreads);
@@ -649,11 +661,18 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         const uint8_t* rb = reinterpret_cast<const uint8_t*>(recv);
 #pragma unroll
         for (int src = 0; src < kKS; ++src) {
-          const float4 x0 = *reinterpret_cast<const float4*>(rb + src * kRecvSlot + slot_off(r, 2 * hf));
-          const float4 x1 = *reinterpret_cast<const float4*>(rb + src * kRecvSlot + slot_off(r, 2 * hf + 1));
-          dh[0] += x0.x; dh[1] += x0.y; dh[2] += x0.z; dh[3] += x0.w;
-          dh[4] += x1.x; dh[5] += x1.y; dh[6] += x1.z; dh[7] += x1.w;
+          const uint4 w = *reinterpret_cast<const uint4*>(rb + src * kRecvSlot + slot_off(r, hf));
+          const __half2* hx = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(hx[i]);
+            dh[2 * i] += f.x;
+            dh[2 * i + 1] += f.y;
+          }
         }
+        const float inv = 1.f / P.xscale;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dh[i] *= inv;
         named_bar_sync(3, kEpiThreads);  // every thread has read this exchange
         if (issuer) {
           for (int f = 0; f < kKS; ++f)
@@ -803,6 +822,11 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   P.trace = a.trace;
   P.dbpart = a.dbpart;
   P.variant = 7;  // acquire by ld.acquire, no writer-side fences
+  {  // fp16 exchange scale: power of two ~ frames / 2 (dh ~ 1/frames for a mean loss)
+    float sc = 1.f;
+    while (sc * 4.f <= (float)T * B && sc < 16384.f) sc *= 2.f;
+    P.xscale = sc;
+  }
   P.B = B;
   P.T = T;
   const int chunk_rows = max_tiles * 128;

@@ -20,6 +20,7 @@ struct LstmParams {
   float* dbpart;    // backward: optional [(B/128)*4][4096] bias-gradient partials
   int B, T, b0, nb, n_btile;
   int variant;  // debug: bit0 skip writer proxy fence, bit1 skip release fence
+  float xscale; // BPTT: fp16 scale of the exchanged partial dh (power of two)
 };
 
 struct LstmLayerArgs {
