@@ -11,6 +11,7 @@
 #include "layout.h"
 #include "lstm_rec.h"
 #include "ops.h"
+#include "softmax_dz.h"
 
 using namespace ds;
 
@@ -116,6 +117,24 @@ bool blocked_dlogits(const ds_blstm* h) {
     off = (e && e[0] == '1') ? 1 : 0;
   }
   return !off && h->L.classes % 64 == 0;
+}
+
+// fused soft-max gradient + dZ (softmax_dz.cu) when dlogits is blocked and
+// the shape fits (DS_NO_FUSED_CE=1 keeps the separate GEMMs)
+bool fused_ce_dz(const ds_blstm* h) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("DS_NO_FUSED_CE");
+    off = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !off && blocked_dlogits(h) && ce_grad_dz_supported(h->L.classes, h->L.bottleneck);
+}
+int fused_dz_splits(const ds_blstm* h, int N) {
+  int S = ce_grad_dz_splits(N);
+  const int n_ct = h->L.classes / 128;
+  if (S > kDzSplit) S = kDzSplit;  // h->splitk holds kDzSplit x N x bottleneck floats
+  if (S > n_ct) S = n_ct;
+  return S < 1 ? 1 : S;
 }
 
 struct Arena {
@@ -310,6 +329,41 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   }
 
   // ---- backward ----
+  if (fused_ce_dz(h)) {
+    // soft-max gradient + dZ in one pass (softmax_dz.cu), then dW_o alone
+    const int S = fused_dz_splits(h, N);
+    CeGradDzArgs ca;
+    ca.z = h->z;
+    ca.w = h->snap + L.off_wo;
+    ca.bias = bias_o;
+    ca.labels = h->lab;
+    ca.lse = h->lse;
+    ca.dlogits = h->dlogits;
+    ca.colpart = getenv("DS_NO_COLSUM") ? nullptr : h->biaspart;
+    ca.dzpart = h->splitk;
+    ca.scale = 1.0f / (h->grad_frames > 0.f ? h->grad_frames : (float)N);
+    ca.rows = N;
+    ca.classes = C;
+    ca.bott = bott;
+    ca.splits = S;
+    MARK(PH_GEMM);
+    TRY(ce_grad_dz_launch(ca, s));
+    MARK(PH_OTHER);
+    if (ca.colpart) TRY(op_rowsum(h->biaspart, ((N + kGemmBM - 1) / kGemmBM) * 4, C, grad + L.off_bo, s));
+    TRY(op_splitk_bf16(h->splitk, S, (int64_t)N * bott, h->dz, s));
+    GemmBatch gb;
+    memset(&gb, 0, sizeof(gb));
+    gb.nprob = 1;
+    GemmProblem& p0 = gb.p[0];  // dW_o = dlogits^T Z
+    TRY(gemm_problem(&p0, h->dlogits, C, 1, h->z, bott, 1, C, bott, N));
+    TRY(gemm_blocked_a(&p0, h->dlogits, N, C));
+    p0.epi = EPI_F32;
+    p0.out = grad + L.off_wo;
+    p0.ldo = bott;
+    MARK(PH_GEMM);
+    TRY(gemm_launch(&gb, s));
+    nl += 4;
+  } else {
   {
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
@@ -367,6 +421,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     TRY(gemm_launch(&gb, s));
     if (S > 1) TRY(op_splitk_bf16(h->splitk, S, (int64_t)N * bott, h->dz, s));
     nl += S > 1 ? 2 : 1;
+  }
   }
   {
     GemmBatch gb;

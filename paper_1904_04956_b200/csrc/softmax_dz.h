@@ -1,0 +1,41 @@
+// softmax_dz.h — fused soft-max gradient + dZ of the output layer (softmax_dz.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "ds_internal.h"
+
+namespace ds {
+
+struct CeGradDzParams {
+  CUtensorMap tmZ;  // Z [rows][bott] bf16, box 64 x 128
+  CUtensorMap tmW;  // W_o [classes][bott] bf16 (operand snapshot), box 64 x 128
+  CUtensorMap tmP;  // dlogits, 64x64-blocked 4D, box 64 x 64 (TMA store)
+  const float* bias;    // b_o [classes]
+  const int* labels;    // [rows], -1 = no target
+  const float* lse;     // [rows]
+  float* colpart;       // [ceil(rows/128)*4][classes] bias-gradient partials (nullable)
+  float* dzpart;        // [n_cs][rows][bott] fp32 dZ partials
+  float scale;          // 1 / frames
+  int bott, classes, m_valid, dz_rows;
+  int n_rb, n_ct, n_cs, ct_per;
+};
+
+struct CeGradDzArgs {
+  const __nv_bfloat16* z;
+  const __nv_bfloat16* w;
+  const float* bias;
+  const int* labels;
+  const float* lse;
+  __nv_bfloat16* dlogits;  // blocked, gemm_blocked_elems(rows, classes)
+  float* colpart;
+  float* dzpart;           // [splits][rows][bott]
+  float scale;
+  int rows, classes, bott, splits;
+};
+
+bool ce_grad_dz_supported(int classes, int bott);
+int ce_grad_dz_splits(int rows);  // class ranges per row block that fill the SMs
+int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream);
+
+}  // namespace ds
