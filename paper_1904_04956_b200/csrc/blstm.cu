@@ -89,6 +89,7 @@ namespace {
 // dZ = dlogits . W_o has K = classes (500 k-blocks at 32000): split it so its
 // tiles match the length of the concurrent dW_o tiles (K = frames).
 constexpr int kDzSplit = 5;
+constexpr int kDzPartMax = 8;  // dZ partial slices of the fused soft-max kernel
 int dz_split(int classes) {
   const int nkb = (classes + kGemmBK - 1) / kGemmBK;
   return (nkb % kDzSplit == 0 && nkb >= 4 * kDzSplit) ? kDzSplit : 1;
@@ -130,11 +131,8 @@ bool fused_ce_dz(const ds_blstm* h) {
   return !off && blocked_dlogits(h) && ce_grad_dz_supported(h->L.classes, h->L.bottleneck);
 }
 int fused_dz_splits(const ds_blstm* h, int N) {
-  int S = ce_grad_dz_splits(N);
-  const int n_ct = h->L.classes / 128;
-  if (S > kDzSplit) S = kDzSplit;  // h->splitk holds kDzSplit x N x bottleneck floats
-  if (S > n_ct) S = n_ct;
-  return S < 1 ? 1 : S;
+  // h->splitk holds kDzPartMax x N x bottleneck floats
+  return ce_grad_dz_splits(N, h->L.classes, kDzPartMax);
 }
 
 struct Arena {
@@ -187,7 +185,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
     h->biaspart = a.take<float>(base, a1 > a2 ? a1 : a2);
   }
   {  // split-K fp32 partials: dZ (K = classes) and dW_b (K = frames)
-    const int64_t s1 = (int64_t)kDzSplit * N * L.bottleneck, s2 = (int64_t)kWbSplit * L.bottleneck * kLayerOut;
+    const int64_t s1 = (int64_t)kDzPartMax * N * L.bottleneck, s2 = (int64_t)kWbSplit * L.bottleneck * kLayerOut;
     h->splitk = a.take<float>(base, s1 > s2 ? s1 : s2);
   }
   h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64);

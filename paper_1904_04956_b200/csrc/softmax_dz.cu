@@ -257,10 +257,16 @@ bool ce_grad_dz_supported(int classes, int bott) {
   return classes % kCT == 0 && bott % 64 == 0 && bott >= 64 && bott <= kMaxBott;
 }
 
-int ce_grad_dz_splits(int rows) {
-  const int n_rb = (rows + kRows - 1) / kRows;
-  int s = num_sms() / n_rb;
-  return s < 1 ? 1 : s;
+// class ranges per row block: about two work items per SM, so the persistent
+// CTAs finish together (one item per row block and split leaves SMs idle when
+// the row-block count does not divide the SM count)
+int ce_grad_dz_splits(int rows, int classes, int max_splits) {
+  const int n_rb = (rows + kRows - 1) / kRows, n_ct = classes / kCT;
+  int s = (2 * num_sms()) / n_rb;
+  s = s < 1 ? 1 : (s > max_splits ? max_splits : s);
+  s = s > n_ct ? n_ct : s;
+  const int per = (n_ct + s - 1) / s;
+  return (n_ct + per - 1) / per;  // no empty class range
 }
 
 int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream) {
@@ -298,6 +304,7 @@ int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream) {
   P.n_ct = a.classes / kCT;
   P.n_cs = a.splits;
   P.ct_per = (P.n_ct + a.splits - 1) / a.splits;
+  if ((a.splits - 1) * P.ct_per >= P.n_ct) return fail_arg("fused soft-max/dZ: empty class range");
   const int items = P.n_rb * P.n_cs;
   const int grid = items < num_sms() ? items : num_sms();
   ce_grad_dz_kernel<<<grid, kThreads, kSmem, stream>>>(P);

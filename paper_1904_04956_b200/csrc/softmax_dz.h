@@ -35,7 +35,7 @@ struct CeGradDzArgs {
 };
 
 bool ce_grad_dz_supported(int classes, int bott);
-int ce_grad_dz_splits(int rows);  // class ranges per row block that fill the SMs
+int ce_grad_dz_splits(int rows, int classes, int max_splits);  // class ranges per row block (none empty)
 int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream);
 
 }  // namespace ds
