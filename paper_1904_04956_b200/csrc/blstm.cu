@@ -152,7 +152,8 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   const int64_t N = h->Nmax;
   h->snap = a.take<__nv_bfloat16>(base, L.total);
   h->wih0pad = a.take<__nv_bfloat16>(base, (size_t)kGates2 * kInPad);
-  h->bias_snap = a.take<float>(base, (size_t)L.layers * kGates2 + L.bottleneck + L.classes);
+  // [layers][4096] b, b_b, b_o, b_o * log2(e) (CE-stats epilogue: one FFMA per logit)
+  h->bias_snap = a.take<float>(base, (size_t)L.layers * kGates2 + L.bottleneck + 2 * (size_t)L.classes);
   h->x0 = a.take<__nv_bfloat16>(base, (size_t)N * kInPad);
   h->lab = a.take<int32_t>(base, N);
   h->gates.resize(L.layers);
@@ -311,7 +312,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     GemmProblem& p = gb.p[0];
     TRY(gemm_problem(&p, h->z, bott, 0, h->snap + L.off_wo, bott, 0, N, C, bott));
     p.epi = EPI_CE_STATS;
-    p.bias = bias_o;
+    p.bias = bias_o + C;  // pre-scaled by log2(e)
     p.labels = h->lab;
     p.stats = h->stats;
     p.stats_ld = (int)h->Nmax;

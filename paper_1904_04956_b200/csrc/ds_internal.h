@@ -53,7 +53,8 @@ int make_tmap_4d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, 
 enum Epilogue : int {
   EPI_BF16 = 0,      // out bf16 [M, ldo] = acc (+ bias[n])
   EPI_F32 = 1,       // out f32  [M, ldo] = acc*scale (+ out if accumulate)
-  EPI_CE_STATS = 2,  // per-row partial (max, sumexp) of acc+bias[n] over n < n_valid, target logit
+  EPI_CE_STATS = 2,  // per-row partial (max, sumexp) of acc + b[n] over n < n_valid, target logit;
+                     // bias holds b * log2(e)
   EPI_CE_GRAD = 3,   // out bf16 = (exp(acc+bias-lse[m]) - [n==label[m]]) * scale
 };
 

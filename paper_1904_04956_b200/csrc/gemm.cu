@@ -305,23 +305,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           float* v = vbuf[(c >> 5) & 1];
           if (c + 32 < kCols) tmem_ld32(t_row + c + 32, vbuf[((c >> 5) + 1) & 1]);  // in flight meanwhile
           const int nb = n0 + c;
+          // logits in the log2 domain: one FFMA with the log2(e)-scaled bias
           float cm = -INFINITY;
           if (full_cols) {
+            float m8[8];
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 bb = bias ? __ldg(reinterpret_cast<const float4*>(bias + nb + i))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-              v[i] = (v[i] + bb.x) * kLog2e;
-              v[i + 1] = (v[i + 1] + bb.y) * kLog2e;
-              v[i + 2] = (v[i + 2] + bb.z) * kLog2e;
-              v[i + 3] = (v[i + 3] + bb.w) * kLog2e;
-              cm = fmaxf(cm, fmaxf(fmaxf(v[i], v[i + 1]), fmaxf(v[i + 2], v[i + 3])));
+              v[i] = fmaf(v[i], kLog2e, bb.x);
+              v[i + 1] = fmaf(v[i + 1], kLog2e, bb.y);
+              v[i + 2] = fmaf(v[i + 2], kLog2e, bb.z);
+              v[i + 3] = fmaf(v[i + 3], kLog2e, bb.w);
+              m8[i >> 2] = fmaxf(fmaxf(v[i], v[i + 1]), fmaxf(v[i + 2], v[i + 3]));
             }
+            // max as a tree (independent FMNMX) instead of a 32-long chain
+            cm = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const bool in = nb + i < n_valid;
-              v[i] = in ? (v[i] + (bias ? __ldg(bias + nb + i) : 0.f)) * kLog2e : -INFINITY;
+              v[i] = in ? fmaf(v[i], kLog2e, bias ? __ldg(bias + nb + i) : 0.f) : -INFINITY;
               cm = fmaxf(cm, v[i]);
             }
           }

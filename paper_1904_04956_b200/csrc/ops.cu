@@ -304,7 +304,7 @@ __global__ void snapshot_aux_kernel(const float* __restrict__ theta, AuxOffs o, 
                                     float* __restrict__ bias) {
   const int64_t npad = (int64_t)kGates2 * kInPad;
   const int64_t nb = (int64_t)o.layers * kGates2;
-  const int64_t total = npad + nb + o.bott + o.classes;
+  const int64_t total = npad + nb + o.bott + 2 * (int64_t)o.classes;  // + b_o * log2(e) for the CE-stats pass
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < npad) {
       const int64_t r = i / kInPad;
@@ -318,8 +318,12 @@ __global__ void snapshot_aux_kernel(const float* __restrict__ theta, AuxOffs o, 
       src = o.off_b[j / kGates2] + j % kGates2;
     else if (j < nb + o.bott)
       src = o.off_bb + (j - nb);
-    else
+    else if (j < nb + o.bott + o.classes)
       src = o.off_bo + (j - nb - o.bott);
+    else {
+      bias[j] = theta[o.off_bo + (j - nb - o.bott - o.classes)] * 1.4426950408889634f;
+      continue;
+    }
     bias[j] = theta[src];
   }
 }
@@ -490,7 +494,7 @@ int op_snapshot_aux(const float* theta, const ModelLayout& L, __nv_bfloat16* wih
   o.din = L.input_dim;
   o.bott = L.bottleneck;
   o.classes = L.classes;
-  const int64_t total = (int64_t)kGates2 * kInPad + (int64_t)L.layers * kGates2 + L.bottleneck + L.classes;
+  const int64_t total = (int64_t)kGates2 * kInPad + (int64_t)L.layers * kGates2 + L.bottleneck + 2 * (int64_t)L.classes;
   snapshot_aux_kernel<<<ew_grid(total), kEW, 0, s>>>(theta, o, wih0pad, bias_snap);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
