@@ -149,3 +149,30 @@ def test_two_process_ipc_ssgd_and_mix_bit_exact():
     # mix
     m = (r[0]["theta_pre_mix"] + r[1]["theta_pre_mix"]) * np.float32(0.5)
     assert np.array_equal(r[0]["theta_mix"], m) and np.array_equal(r[1]["theta_mix"], m)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["ssgd", "adpsgd"])
+def test_bench_multiprocess_p2p_same_device(strategy):
+    """bench.py's one-process-per-GPU path (torchrun, P2P transport) runs end
+    to end with both ranks on cuda:0 and prints one JSON line (functional
+    check: ranks time-slice one GPU, the value is not a scaling number)."""
+    import json
+    import subprocess
+    import sys
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2", "--steps",
+           "3", "--warmup", "3", "--no-cpu", "--n-seq", "1024", "--batch", "64", "--same-device", "--strategy",
+           strategy]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["config"]["strategy"] == strategy and rec["config"]["transport"] == "p2p"
+    assert rec["value"] > 0 and rec["e2e"]["value"] > 0
