@@ -338,7 +338,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     ca.labels = h->lab;
     ca.lse = h->lse;
     ca.dlogits = h->dlogits;
-    ca.colpart = getenv("DS_NO_COLSUM") ? nullptr : h->biaspart;
+    ca.colpart = h->biaspart;
     ca.dzpart = h->splitk;
     ca.scale = 1.0f / (h->grad_frames > 0.f ? h->grad_frames : (float)N);
     ca.rows = N;
@@ -348,7 +348,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     TRY(ce_grad_dz_launch(ca, s));
     MARK(PH_OTHER);
-    if (ca.colpart) TRY(op_rowsum(h->biaspart, ((N + kGemmBM - 1) / kGemmBM) * 4, C, grad + L.off_bo, s));
+    TRY(op_rowsum(h->biaspart, ((N + kGemmBM - 1) / kGemmBM) * 4, C, grad + L.off_bo, s));
     TRY(op_splitk_bf16(h->splitk, S, (int64_t)N * bott, h->dz, s));
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
@@ -376,7 +376,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.out = h->dlogits;
     p.ldo = C;
     p.scale = 1.0f / (h->grad_frames > 0.f ? h->grad_frames : (float)N);
-    p.colpart = getenv("DS_NO_COLSUM") ? nullptr : h->biaspart;
+    p.colpart = h->biaspart;
     if (blocked_dlogits(h))  // 64x64 blocks: the two readers below fetch contiguous 8 KB boxes
       TRY(gemm_blocked_output(&p, N, C));
     else

@@ -35,9 +35,7 @@ ch = a[grid * T * 6:].reshape(T, 8, 2)
 base = a[a > 0].min()
 main = np.where(main > 0, main - base, np.nan) / 1e3
 ch = np.where(ch > 0, ch - base, np.nan) / 1e3
-import os
-names = (["chunk0 issued", "last issued", "acc ready", "cell done", "h stored", "published"] if os.environ.get("DS_FWD_IMPL") == "p" else
-         ["watch done", "staged", "acc ready", "cell done", "h stored", "mma saw chunk 7"])
+names = ["chunk0 issued", "last issued", "acc ready", "cell done", "h stored", "published"]
 order = [0, 1, 2, 5, 3, 4]
 for st in (6, 10, 14):
     med = np.nanmedian(main[:, st, :], axis=0)
