@@ -363,29 +363,70 @@ struct GroupPtrs {
   __nv_bfloat16* snap[kMaxGroup];
 };
 
+__device__ __forceinline__ float4 f4_step(float4 v, float4 gm, float4& w, float lr, float mu) {
+  v.x = __fadd_rn(__fmul_rn(v.x, mu), gm.x);
+  v.y = __fadd_rn(__fmul_rn(v.y, mu), gm.y);
+  v.z = __fadd_rn(__fmul_rn(v.z, mu), gm.z);
+  v.w = __fadd_rn(__fmul_rn(v.w, mu), gm.w);
+  w.x = __fsub_rn(w.x, __fmul_rn(lr, v.x));
+  w.y = __fsub_rn(w.y, __fmul_rn(lr, v.y));
+  w.z = __fsub_rn(w.z, __fmul_rn(lr, v.z));
+  w.w = __fsub_rn(w.w, __fmul_rn(lr, v.w));
+  return v;
+}
+__device__ __forceinline__ uint2 f4_bf16(float4 w) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(w.x, w.y), b = __floats2bfloat162_rn(w.z, w.w);
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&a);
+  pk.y = *reinterpret_cast<uint32_t*>(&b);
+  return pk;
+}
+
+// float4 vectors inside each owned chunk, scalar at its ragged edges
 __global__ void group_reduce_kernel(GroupPtrs p, int world, int rank, int64_t dim, int64_t chunk, int nchunks,
                                     float lr, float mu, int mode, float divisor) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  const float* const* src = mode == 0 ? p.g : p.theta;
   for (int j = rank; j < nchunks; j += world) {
     const int64_t lo = min(dim, (int64_t)j * chunk), hi = min(dim, (int64_t)(j + 1) * chunk);
     const int owner = j % world;
-    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
-      const float* const* src = mode == 0 ? p.g : p.theta;
+    const int64_t lo4 = (lo + 3) / 4, hi4 = hi / 4;
+    for (int64_t i4 = lo4 + tid; i4 < hi4; i4 += nth) {
+      float4 sum = reinterpret_cast<const float4*>(src[owner])[i4];
+      for (int k = 1; k < world; ++k) {
+        const float4 x = reinterpret_cast<const float4*>(src[(owner + k) % world])[i4];
+        sum.x = __fadd_rn(sum.x, x.x);
+        sum.y = __fadd_rn(sum.y, x.y);
+        sum.z = __fadd_rn(sum.z, x.z);
+        sum.w = __fadd_rn(sum.w, x.w);
+      }
+      const float4 mean = make_float4(__fdiv_rn(sum.x, divisor), __fdiv_rn(sum.y, divisor), __fdiv_rn(sum.z, divisor),
+                                      __fdiv_rn(sum.w, divisor));
+      for (int r = 0; r < world; ++r) {
+        float4 w = mean;
+        if (mode == 0) {
+          w = reinterpret_cast<const float4*>(p.theta[r])[i4];
+          reinterpret_cast<float4*>(p.v[r])[i4] = f4_step(reinterpret_cast<const float4*>(p.v[r])[i4], mean, w, lr, mu);
+        }
+        reinterpret_cast<float4*>(p.theta[r])[i4] = w;
+        if (p.snap[r]) reinterpret_cast<uint2*>(p.snap[r])[i4] = f4_bf16(w);
+      }
+    }
+    const int64_t e0 = lo, e1 = min(hi, lo4 * 4), f0 = max(lo, hi4 * 4), f1 = hi;
+    for (int64_t t = tid; t < (e1 - e0) + (f1 - f0); t += nth) {
+      const int64_t i = t < (e1 - e0) ? e0 + t : f0 + (t - (e1 - e0));
       float s = src[owner][i];
       for (int k = 1; k < world; ++k) s = __fadd_rn(s, src[(owner + k) % world][i]);
       const float mean = __fdiv_rn(s, divisor);
-      if (mode == 0) {
-        for (int r = 0; r < world; ++r) {
-          float vv = __fadd_rn(__fmul_rn(p.v[r][i], mu), mean);
-          float w = __fsub_rn(p.theta[r][i], __fmul_rn(lr, vv));
+      for (int r = 0; r < world; ++r) {
+        float w = mean;
+        if (mode == 0) {
+          const float vv = __fadd_rn(__fmul_rn(p.v[r][i], mu), mean);
+          w = __fsub_rn(p.theta[r][i], __fmul_rn(lr, vv));
           p.v[r][i] = vv;
-          p.theta[r][i] = w;
-          if (p.snap[r]) p.snap[r][i] = __float2bfloat16_rn(w);
         }
-      } else {
-        for (int r = 0; r < world; ++r) {
-          p.theta[r][i] = mean;
-          if (p.snap[r]) p.snap[r][i] = __float2bfloat16_rn(mean);
-        }
+        p.theta[r][i] = w;
+        if (p.snap[r]) p.snap[r][i] = __float2bfloat16_rn(w);
       }
     }
   }
@@ -521,8 +562,13 @@ int op_group_reduce(int world, int rank, float* const* g, float* const* theta, f
     p.snap[r] = snap ? snap[r] : nullptr;
   }
   if (mode == 0 && (!g || !v)) return fail_arg("SGD allreduce needs gradient and velocity buffers");
+  for (int r = 0; r < world; ++r) {
+    uintptr_t al = reinterpret_cast<uintptr_t>(p.theta[r]) | reinterpret_cast<uintptr_t>(p.g[r]) |
+                   reinterpret_cast<uintptr_t>(p.v[r]) | (reinterpret_cast<uintptr_t>(p.snap[r]) & 7);
+    if (al & 15) return fail_arg("group reduce: buffers must be 16-byte aligned");
+  }
   const int64_t chunk = (dim + nchunks - 1) / nchunks;
-  group_reduce_kernel<<<ew_grid(chunk), kEW, 0, s>>>(p, world, rank, dim, chunk, nchunks, lr, mu, mode,
+  group_reduce_kernel<<<ew_grid(chunk / 4 + 1), kEW, 0, s>>>(p, world, rank, dim, chunk, nchunks, lr, mu, mode,
                                                      divisor > 0.f ? divisor : (float)world);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;

@@ -70,29 +70,71 @@ struct ShardArgs {
   __nv_bfloat16* snap[kMaxPeers];
 };
 
-// chunks j = rank, rank + world, ... of ceil(n / nchunks) elements
+// one element of the owner's chunk (reference order: owner, owner+1, ...)
+__device__ __forceinline__ float shard_elem(const ShardArgs& a, int world, int rank, int owner, float gsum_or_theta,
+                                            float* v_own, int64_t i, float lr, float mu, int mode, float divisor) {
+  if (mode == 0) {
+    const float gm = __fdiv_rn(gsum_or_theta, divisor);
+    const float vv = __fadd_rn(__fmul_rn(v_own[i], mu), gm);
+    v_own[i] = vv;
+    return __fsub_rn(a.theta[rank][i], __fmul_rn(lr, vv));
+  }
+  return __fdiv_rn(gsum_or_theta, divisor);
+}
+
+// chunks j = rank, rank + world, ... of ceil(n / nchunks) elements; float4
+// vectors inside a chunk (scalar at its ragged edges), same arithmetic order
+// as the reference's canonical ring sum.
 __global__ void shard_step_kernel(ShardArgs a, int world, int rank, int64_t n, int64_t chunk, int nchunks,
                                   float* __restrict__ v_own, float lr, float mu, int mode, float divisor) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
   for (int j = rank; j < nchunks; j += world) {
     const int64_t lo = min(n, (int64_t)j * chunk), hi = min(n, (int64_t)(j + 1) * chunk);
     const int owner = j % world;  // == rank
-    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      float w;
-      if (mode == 0) {
-        float s = a.g[owner][i];
-        for (int k = 1; k < world; ++k) s = __fadd_rn(s, a.g[(owner + k) % world][i]);
-        const float gm = __fdiv_rn(s, divisor);
-        const float vv = __fadd_rn(__fmul_rn(v_own[i], mu), gm);
-        v_own[i] = vv;
-        w = __fsub_rn(a.theta[rank][i], __fmul_rn(lr, vv));
-      } else {
-        float s = a.theta[owner][i];
-        for (int k = 1; k < world; ++k) s = __fadd_rn(s, a.theta[(owner + k) % world][i]);
-        w = __fdiv_rn(s, divisor);
+    const float* const* src = mode == 0 ? a.g : a.theta;
+    const int64_t lo4 = (lo + 3) / 4, hi4 = hi / 4;
+    for (int64_t i4 = lo4 + tid; i4 < hi4; i4 += nth) {
+      float4 sum = reinterpret_cast<const float4*>(src[owner])[i4];
+      for (int k = 1; k < world; ++k) {
+        const float4 x = reinterpret_cast<const float4*>(src[(owner + k) % world])[i4];
+        sum.x = __fadd_rn(sum.x, x.x);
+        sum.y = __fadd_rn(sum.y, x.y);
+        sum.z = __fadd_rn(sum.z, x.z);
+        sum.w = __fadd_rn(sum.w, x.w);
       }
-      const __nv_bfloat16 wb = __float2bfloat16_rn(w);
+      float4 w;
+      if (mode == 0) {
+        const float4 tv = reinterpret_cast<const float4*>(a.theta[rank])[i4];
+        float4 vv = reinterpret_cast<const float4*>(v_own)[i4];
+        vv.x = __fadd_rn(__fmul_rn(vv.x, mu), __fdiv_rn(sum.x, divisor));
+        vv.y = __fadd_rn(__fmul_rn(vv.y, mu), __fdiv_rn(sum.y, divisor));
+        vv.z = __fadd_rn(__fmul_rn(vv.z, mu), __fdiv_rn(sum.z, divisor));
+        vv.w = __fadd_rn(__fmul_rn(vv.w, mu), __fdiv_rn(sum.w, divisor));
+        reinterpret_cast<float4*>(v_own)[i4] = vv;
+        w = make_float4(__fsub_rn(tv.x, __fmul_rn(lr, vv.x)), __fsub_rn(tv.y, __fmul_rn(lr, vv.y)),
+                        __fsub_rn(tv.z, __fmul_rn(lr, vv.z)), __fsub_rn(tv.w, __fmul_rn(lr, vv.w)));
+      } else {
+        w = make_float4(__fdiv_rn(sum.x, divisor), __fdiv_rn(sum.y, divisor), __fdiv_rn(sum.z, divisor),
+                        __fdiv_rn(sum.w, divisor));
+      }
+      __nv_bfloat162 b0 = __floats2bfloat162_rn(w.x, w.y), b1 = __floats2bfloat162_rn(w.z, w.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&b0);
+      pk.y = *reinterpret_cast<uint32_t*>(&b1);
       for (int r = 0; r < world; ++r) {  // all-gather: owner's result into every replica
+        reinterpret_cast<float4*>(a.theta[r])[i4] = w;
+        if (a.snap[r]) reinterpret_cast<uint2*>(a.snap[r])[i4] = pk;
+      }
+    }
+    // ragged chunk edges
+    const int64_t e0 = lo, e1 = min(hi, lo4 * 4), f0 = max(lo, hi4 * 4), f1 = hi;
+    for (int64_t t = tid; t < (e1 - e0) + (f1 - f0); t += nth) {
+      const int64_t i = t < (e1 - e0) ? e0 + t : f0 + (t - (e1 - e0));
+      float sum = src[owner][i];
+      for (int k = 1; k < world; ++k) sum = __fadd_rn(sum, src[(owner + k) % world][i]);
+      const float w = shard_elem(a, world, rank, owner, sum, v_own, i, lr, mu, mode, divisor);
+      const __nv_bfloat16 wb = __float2bfloat16_rn(w);
+      for (int r = 0; r < world; ++r) {
         a.theta[r][i] = w;
         if (a.snap[r]) a.snap[r][i] = wb;
       }
@@ -242,6 +284,12 @@ int ds_shard_step(int32_t world, int32_t rank, const float* const* grads, float*
   if (nchunks < world) return fail_arg("chunk_count must be >= world");
   if (!thetas || n < 1) return fail_arg("null argument");
   if (mode != 0 && mode != 1) return fail_arg("mode must be 0 (sgd) or 1 (average)");
+  for (int r = 0; r < world; ++r) {
+    const uintptr_t al = reinterpret_cast<uintptr_t>(thetas[r]) | (grads ? reinterpret_cast<uintptr_t>(grads[r]) : 0) |
+                         (snaps ? reinterpret_cast<uintptr_t>(snaps[r]) & 7 : 0);
+    if (al & 15) return fail_arg("shard step: buffers must be 16-byte aligned");
+  }
+  if (v_own && (reinterpret_cast<uintptr_t>(v_own) & 15)) return fail_arg("shard step: velocity must be 16-byte aligned");
   if (mode == 0 && (!grads || !v_own)) return fail_arg("SGD step needs gradients and the velocity");
   if (mode == 0 && !(lr > 0.f)) return fail_arg("learning rate must be > 0");
   ShardArgs a;
@@ -253,7 +301,7 @@ int ds_shard_step(int32_t world, int32_t rank, const float* const* grads, float*
     if (!a.theta[r] || (mode == 0 && !a.g[r])) return fail_arg("null member buffer");
   }
   const int64_t chunk = (n + nchunks - 1) / nchunks;
-  shard_step_kernel<<<ew_grid(chunk), kEW, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  shard_step_kernel<<<ew_grid(chunk / 4 + 1), kEW, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       a, world, rank, n, chunk, nchunks, v_own, lr, mu, mode, divisor > 0.f ? divisor : (float)world);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
