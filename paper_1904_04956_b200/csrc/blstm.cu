@@ -53,6 +53,7 @@ struct ds_blstm {
   // fused training step: per-layer SGD on a side stream while the next BPTT runs
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork[kMaxLayers + 2] = {}, ev_join[kMaxLayers + 2] = {};
+  cudaEvent_t ev_aux[4] = {};  // output-layer bias reductions on the side stream
   // graph cache
   struct Key {
     int B;
@@ -261,6 +262,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
 #define MARK(k) TRY(mark(h, k, s))
   int& nl = h->launches;
   nl = 0;
+  bool aux_join = false;
 
   MARK(PH_OTHER);
   TRY(op_gather(idx, B, T, h->feats, h->labels, h->n_seq, h->x0, h->lab, flag, s));
@@ -348,7 +350,17 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     TRY(ce_grad_dz_launch(ca, s));
     MARK(PH_OTHER);
-    TRY(op_rowsum(h->biaspart, ((N + kGemmBM - 1) / kGemmBM) * 4, C, grad + L.off_bo, s));
+    // db_o only feeds the output-layer update: reduce it on the side stream
+    // (joined before the first BPTT, which reuses the partials buffer)
+    cudaStream_t rs = s;
+    if (sg.theta && !h->profile) {
+      DS_CUDA_TRY(cudaEventRecord(h->ev_aux[0], s));
+      DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_aux[0], 0));
+      rs = h->side;
+    }
+    TRY(op_rowsum(h->biaspart, ((N + kGemmBM - 1) / kGemmBM) * 4, C, grad + L.off_bo, rs));
+    if (rs != s) DS_CUDA_TRY(cudaEventRecord(h->ev_aux[1], rs));
+    aux_join = rs != s;
     TRY(op_splitk_bf16(h->splitk, S, (int64_t)N * bott, h->dz, s));
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
@@ -444,7 +456,14 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
     if (Sb > 1) TRY(op_splitk_f32(h->splitk, Sb, (int64_t)bott * kLayerOut, grad + L.off_wb, s));
-    TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, s));
+    if (aux_join) {  // db_b (column sums of dZ) on the side stream too; the output SGD follows it there
+      DS_CUDA_TRY(cudaEventRecord(h->ev_aux[2], s));
+      DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_aux[2], 0));
+      TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, h->side));
+      DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_aux[1], 0));  // biaspart free for the BPTT
+    } else {
+      TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, s));
+    }
     nl += Sb > 1 ? 4 : 3;
     // bottleneck + output layer gradients are final: update them beside BPTT_{L-1}
     TRY(sgd_segment(h, sg, grad, flag, L.off_wb, L.total - L.off_wb, true, s));
@@ -601,6 +620,7 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
     e = cudaEventCreateWithFlags(&h->ev_fork[k], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join[k], cudaEventDisableTiming);
   }
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_aux[k], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     cudaFree(h->arena);
     delete h;
@@ -618,6 +638,8 @@ int ds_blstm_destroy(ds_blstm* h) {
     if (h->ev_fork[k]) cudaEventDestroy(h->ev_fork[k]);
     if (h->ev_join[k]) cudaEventDestroy(h->ev_join[k]);
   }
+  for (int k = 0; k < 4; ++k)
+    if (h->ev_aux[k]) cudaEventDestroy(h->ev_aux[k]);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->arena) cudaFree(h->arena);
   delete h;
