@@ -54,6 +54,9 @@ struct ds_blstm {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork[kMaxLayers + 2] = {}, ev_join[kMaxLayers + 2] = {};
   cudaEvent_t ev_aux[4] = {};  // output-layer bias reductions on the side stream
+  // per-layer bias-gradient row sums beside the layer's weight-gradient GEMMs
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_rs[kMaxLayers][2] = {};
   // graph cache
   struct Key {
     int B;
@@ -505,10 +508,19 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       TRY(gemm_bf16_output(&p3));
       gb.nprob = 4;
     }
+    // db = row sums of the BPTT's bias partials: off the critical path, beside the GEMMs; joined
+    // before the layer's update and before BPTT_{l-1} reuses biaspart
+    const bool rs_side = !h->profile;
     MARK(PH_OTHER);
-    TRY(op_rowsum(h->biaspart, ((B + 127) / 128) * 4, kGates2, grad + L.off_b[l], s));
+    if (rs_side) {
+      DS_CUDA_TRY(cudaEventRecord(h->ev_rs[l][0], s));
+      DS_CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev_rs[l][0], 0));
+    }
+    TRY(op_rowsum(h->biaspart, ((B + 127) / 128) * 4, kGates2, grad + L.off_b[l], rs_side ? h->side2 : s));
+    if (rs_side) DS_CUDA_TRY(cudaEventRecord(h->ev_rs[l][1], h->side2));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
+    if (rs_side) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l][1], 0));
     nl += 2;
     // layer l's gradients are final: update them beside BPTT_{l-1} (layer 0 on the critical path)
     TRY(sgd_segment(h, sg, grad, flag, L.off_wih[l], L.off_b[l] + kGates2 - L.off_wih[l], l > 0, s));
@@ -621,6 +633,9 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join[k], cudaEventDisableTiming);
   }
   for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_aux[k], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side2, cudaStreamNonBlocking);
+  for (int k = 0; k < kMaxLayers * 2 && e == cudaSuccess; ++k)
+    e = cudaEventCreateWithFlags(&h->ev_rs[k / 2][k % 2], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     cudaFree(h->arena);
     delete h;
@@ -640,6 +655,9 @@ int ds_blstm_destroy(ds_blstm* h) {
   }
   for (int k = 0; k < 4; ++k)
     if (h->ev_aux[k]) cudaEventDestroy(h->ev_aux[k]);
+  for (int k = 0; k < kMaxLayers * 2; ++k)
+    if (h->ev_rs[k / 2][k % 2]) cudaEventDestroy(h->ev_rs[k / 2][k % 2]);
+  if (h->side2) cudaStreamDestroy(h->side2);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->arena) cudaFree(h->arena);
   delete h;
