@@ -134,6 +134,12 @@ int32_t ds_blstm_kernel_count(ds_blstm* h);
  * a_mn/b_mn select MN-major storage ([K][M] / [K][N]). */
 int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C,
                        int64_t ldc, int32_t M, int32_t N, int32_t K, ds_stream_t stream);
+/* Record a per-CTA, per-tile timeline of the `launch`-th GEMM launch issued
+ * from now on into `buf` (device, zeroed, >= 2*80*8*8 uint64); buf = NULL turns
+ * it off; launch = -1 traces the fused soft-max/dZ kernel instead.  Profiling
+ * aid for tools/gemm_trace.py and tools/cedz_trace.py; never used on the
+ * product path. */
+int ds_debug_gemm_trace(void* buf, int32_t launch);
 
 /* ---------------------------------------------------------------------------
  * Multi-process data parallelism (one process per GPU, NVLink P2P).

@@ -806,6 +806,16 @@ int ds_blstm_profile_list(ds_blstm* h, float* ms, int32_t* kinds, int32_t max_n,
   return DS_OK;
 }
 
+int ds_debug_gemm_trace(void* buf, int32_t launch) {
+  if (launch == -1) {  // the fused soft-max/dZ kernel instead (every launch while set)
+    ce_grad_dz_set_trace(static_cast<unsigned long long*>(buf));
+    return DS_OK;
+  }
+  if (buf && launch < 0) return fail_arg("launch index must be >= 0 (or -1: soft-max/dZ kernel)");
+  gemm_set_trace(static_cast<unsigned long long*>(buf), launch);
+  return DS_OK;
+}
+
 int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C,
                        int64_t ldc, int32_t M, int32_t N, int32_t K, ds_stream_t stream) {
   GemmBatch gb;

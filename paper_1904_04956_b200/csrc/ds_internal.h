@@ -108,7 +108,11 @@ struct GemmBatch {
   int sched;                            // 1: use order/pstart
   uint16_t pstart[kMaxPairs + 1];       // pair p runs order[pstart[p] .. pstart[p+1])
   uint16_t order[kMaxSched];
+  // debug: per-CTA per-tile timeline (tools/gemm_trace.py), null in production
+  unsigned long long* trace;
 };
+// debug: trace the `launch`-th gemm_launch from now on into `buf` (null: off)
+void gemm_set_trace(unsigned long long* buf, int launch);
 
 // Host helpers -------------------------------------------------------------
 // Describe one problem. A/B are device pointers with the given row pitches

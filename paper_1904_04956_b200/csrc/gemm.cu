@@ -49,6 +49,10 @@ constexpr int kStageC = 32 * 32 * 2;  // per-epilogue-warp bf16 staging box (32 
 constexpr int kEpiWarps = 16;
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + kEpiWarps * kStageC + 256;
 
+// trace record: [cta][tile < kTrTiles][kTrFields] (globaltimer ns / clock64 cycles)
+constexpr int kTrTiles = 8, kTrFields = 8;
+enum { TR_MMA_START, TR_MMA_FULLSTALL, TR_MMA_END, TR_EPI_START, TR_EPI_END, TR_EPI_LAST, TR_PROD_STALL, TR_CTA_START };
+
 struct TileCoord {
   int prob, tm, tn, ks;
 };
@@ -142,6 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const uint32_t crank = cluster_ctarank();  // 0 = leader (issues the pair MMAs)
   const bool leader = crank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  unsigned long long* const trace = batch.trace ? batch.trace + (size_t)blockIdx.x * kTrTiles * kTrFields : nullptr;
+  if (trace && threadIdx.x == 0) trace[TR_CTA_START] = globaltimer();
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < batch.nprob; ++i) {
@@ -180,8 +186,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int m0 = tc.tm * kPairM + (int)crank * BM, n0 = tc.tn * BN + (int)crank * kBHalf;
         int kb0, kb1;
         kb_range(P, tc.ks, kb0, kb1);
+        long long pst = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
+          const long long c0 = trace ? clock64() : 0;
           mbar_wait(&empty[stage], phase ^ 1);  // the pair MMA that read this stage (both CTAs) is done
+          if (trace) pst += clock64() - c0;
           uint8_t* sA = smem + stage * kStageBytes;
           uint8_t* sB = sA + kABytes;
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
@@ -212,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             phase ^= 1;
           }
         }
+        if (trace && ti < kTrTiles) trace[ti * kTrFields + TR_PROD_STALL] = pst;
       }
     }
   } else if (warp == 1) {
@@ -231,9 +241,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const uint32_t idesc = idesc_bf16_f32(kPairM, BN, P.a_mn, P.b_mn);
         mbar_wait_acq_cluster(&tempty[acc], acc_phase ^ 1);  // both CTAs' epilogues drained it
         tc_fence_after();
+        const bool tr = trace && ti < kTrTiles;
+        if (tr && lane == 0) trace[ti * kTrFields + TR_MMA_START] = globaltimer();
+        long long fst = 0;
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
+          const long long c0 = tr ? clock64() : 0;
           mbar_wait(&full[stage], phase);
+          if (tr) fst += clock64() - c0;
           tc_fence_after();
           if (elect_one()) {
             const uint32_t aBase = smem_u32(smem + stage * kStageBytes);
@@ -254,6 +269,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             stage = 0;
             phase ^= 1;
           }
+        }
+        if (tr && lane == 0) {
+          trace[ti * kTrFields + TR_MMA_END] = globaltimer();
+          trace[ti * kTrFields + TR_MMA_FULLSTALL] = fst;
         }
       }
     }
@@ -289,8 +308,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         lbl = P.labels[row];
         if (epi == EPI_CE_GRAD) l = P.lse[row];
       }
+      // the warp's 64 bias values, lane i holding columns n0+i and n0+32+i (broadcast by
+      // shuffles below): the loads' latency hides behind the accumulator wait
+      float bias_lo = 0.f, bias_hi = 0.f;
+      if (bias && epi != EPI_CE_GRAD) {
+        if (n0 + (int)lane < n_valid) bias_lo = __ldg(bias + n0 + lane);
+        if (n0 + 32 + (int)lane < n_valid) bias_hi = __ldg(bias + n0 + 32 + lane);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (trace && ti < kTrTiles && e == 0 && lane == 0) trace[ti * kTrFields + TR_EPI_START] = globaltimer();
       const uint32_t t_row = tmem_base + acc * BN + ((q * 32) << 16) + part * kCols;
 
       if (epi == EPI_CE_STATS) {
@@ -307,16 +334,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const int nb = n0 + c;
           // logits in the log2 domain: one FFMA with the log2(e)-scaled bias
           float cm = -INFINITY;
+          const float bsrc = c == 0 ? bias_lo : bias_hi;
           if (full_cols) {
             float m8[8];
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
-              const float4 bb = bias ? __ldg(reinterpret_cast<const float4*>(bias + nb + i))
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-              v[i] = fmaf(v[i], kLog2e, bb.x);
-              v[i + 1] = fmaf(v[i + 1], kLog2e, bb.y);
-              v[i + 2] = fmaf(v[i + 2], kLog2e, bb.z);
-              v[i + 3] = fmaf(v[i + 3], kLog2e, bb.w);
+              v[i] = fmaf(v[i], kLog2e, __shfl_sync(0xffffffffu, bsrc, i));
+              v[i + 1] = fmaf(v[i + 1], kLog2e, __shfl_sync(0xffffffffu, bsrc, i + 1));
+              v[i + 2] = fmaf(v[i + 2], kLog2e, __shfl_sync(0xffffffffu, bsrc, i + 2));
+              v[i + 3] = fmaf(v[i + 3], kLog2e, __shfl_sync(0xffffffffu, bsrc, i + 3));
               m8[i >> 2] = fmaxf(fmaxf(v[i], v[i + 1]), fmaxf(v[i + 2], v[i + 3]));
             }
             // max as a tree (independent FMNMX) instead of a 32-long chain
@@ -325,7 +351,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const bool in = nb + i < n_valid;
-              v[i] = in ? fmaf(v[i], kLog2e, bias ? __ldg(bias + nb + i) : 0.f) : -INFINITY;
+              const float bv = __shfl_sync(0xffffffffu, bsrc, i);
+              v[i] = in ? fmaf(v[i], kLog2e, bv) : -INFINITY;
               cm = fmaxf(cm, v[i]);
             }
           }
@@ -404,14 +431,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const int nb = n0 + c;
           if (nb >= n_valid) continue;
           if (bias) {
+            const float bsrc = c == 0 ? bias_lo : bias_hi;
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + nb + i));
-              v[i] += bb.x;
-              v[i + 1] += bb.y;
-              v[i + 2] += bb.z;
-              v[i + 3] += bb.w;
-            }
+            for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xffffffffu, bsrc, i);
           }
           if (P.c_tma) {
             store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, rt * BM + q * 32);
@@ -451,6 +473,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       }
       tc_fence_before();
       __syncwarp();
+      if (trace && ti < kTrTiles && lane == 0) {
+        if (e == 0) trace[ti * kTrFields + TR_EPI_END] = globaltimer();
+        atomicMax(&trace[ti * kTrFields + TR_EPI_LAST], (unsigned long long)globaltimer());
+      }
       if (lane == 0) {
         if (leader)
           mbar_arrive(&tempty[acc]);
@@ -589,7 +615,16 @@ static void schedule_tiles(GemmBatch* b, int pairs) {
   b->sched = 1;
 }
 
+static unsigned long long* g_trace = nullptr;
+static int g_trace_countdown = -1;
+void gemm_set_trace(unsigned long long* buf, int launch) {
+  g_trace = buf;
+  g_trace_countdown = buf ? launch : -1;
+}
+
 int gemm_launch(GemmBatch* b, cudaStream_t stream) {
+  b->trace = nullptr;
+  if (g_trace_countdown >= 0 && g_trace_countdown-- == 0) b->trace = g_trace;
   static bool attr_set = false;
   if (!attr_set) {
     DS_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));

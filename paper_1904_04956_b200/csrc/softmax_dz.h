@@ -10,7 +10,7 @@ namespace ds {
 struct CeGradDzParams {
   CUtensorMap tmZ;  // Z [rows][bott] bf16, box 64 x 128
   CUtensorMap tmW;  // W_o [classes][bott] bf16 (operand snapshot), box 64 x 128
-  CUtensorMap tmP;  // dlogits, 64x64-blocked 4D, box 64 x 64 (TMA store)
+  CUtensorMap tmP;  // dlogits, 64x64-blocked 4D [ceil(rows/64)][classes/64][64][64], box 16 x 32 (TMA store)
   const float* bias;    // b_o [classes]
   const int* labels;    // [rows], -1 = no target
   const float* lse;     // [rows]
@@ -19,7 +19,9 @@ struct CeGradDzParams {
   float scale;          // 1 / frames
   int bott, classes, m_valid, dz_rows;
   int n_rb, n_ct, n_cs, ct_per;
+  unsigned long long* trace;  // debug timeline (tools/cedz_trace.py), null in production
 };
+void ce_grad_dz_set_trace(unsigned long long* buf);
 
 struct CeGradDzArgs {
   const __nv_bfloat16* z;

@@ -26,7 +26,7 @@ def _spec(obj):
                        classes=obj.classes, frames=obj.frames)
 
 
-@pytest.mark.parametrize("layers,B,T,classes", [(2, 24, 6, 512), (1, 136, 5, 256), (1, 40, 3, 1280)])
+@pytest.mark.parametrize("layers,B,T,classes", [(2, 24, 6, 512), (1, 136, 5, 256), (1, 40, 3, 1280), (1, 8, 3, 32000)])
 def test_fwd_bwd_matches_oracle(layers, B, T, classes):
     obj = BlstmObjective(layers=layers, classes=classes, frames=T)
     spec = _spec(obj)

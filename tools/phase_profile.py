@@ -29,8 +29,19 @@ kinds = (ctypes.c_int32 * 256)()
 n = ctypes.c_int32()
 _lib.check(_lib.load().ds_blstm_profile_list(L.handle, ms, kinds, 256, ctypes.byref(n)))
 names = {0: "gemm", 1: "lstm_fwd", 2: "lstm_bwd", 3: "other"}
+# algorithmic GFLOP of the GEMM segments in issue order (paper model, N = 21 B)
+N = 21 * B
+G2, H, LO, BT, C, D0 = 4096, 512, 1024, 256, 32000, 260
+gf = [2 * N * G2 * D0] + [2 * N * G2 * LO] * 5 + [2 * N * BT * LO, 2 * N * C * BT, 4 * N * C * BT, 2 * N * C * BT,
+                                                  4 * N * BT * LO]
+gf += [2 * N * G2 * LO * 2 + 2 * 2 * N * 4 * H * H] * 5 + [2 * N * G2 * D0 + 2 * 2 * N * 4 * H * H]
+gi = 0
 tot = 0.0
 for i in range(n.value):
     tot += ms[i]
-    print(f"{i:3d} {names.get(kinds[i], '?'):9s} {ms[i] * 1e3:9.1f} us")
+    extra = ""
+    if kinds[i] == 0 and ms[i] > 0.004 and gi < len(gf):
+        extra = f"  {gf[gi] / 1e9:7.1f} GF  {gf[gi] / (ms[i] * 1e-3) / 1e12:7.1f} TF/s"
+        gi += 1
+    print(f"{i:3d} {names.get(kinds[i], '?'):9s} {ms[i] * 1e3:9.1f} us{extra}")
 print(f"total {tot:.3f} ms")
