@@ -195,7 +195,8 @@ int ds_pair_mix(float* self, float* peer, void* snap_self, void* snap_peer, int6
 /* Recurrent-kernel self-test hooks (tests only): run one bidirectional layer's
  * forward / backward recurrence on caller buffers (layouts of lstm_rec.cu;
  * whh = W_hh bf16 [4096, 512] for both directions of recurrence).
- * counters: >= 512*ceil(B/128) words; trace (nullable): [grid][T][4] u64
+ * counters: >= 640*ceil(B/128) words, zeroed once (the flags count up across
+ * launches, so the buffer is reused without resetting); trace (nullable): [grid][T][4] u64
  * globaltimer marks (producer ready, loads issued, MMA done, step published). */
 int ds_debug_lstm_fwd(int32_t B, int32_t T, void* gates, float* cstate, void* y_full, const void* whh,
                       uint32_t* counters, uint64_t* trace, ds_stream_t stream);

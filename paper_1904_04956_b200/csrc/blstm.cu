@@ -626,7 +626,8 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
     return fail_cuda(e, "cudaMalloc(workspace)");
   }
   carve(h, reinterpret_cast<char*>(h->arena), &total);
-  e = cudaMemset(h->counters, 0, sizeof(uint32_t) * 64);
+  // recurrent-kernel flags count up across launches: zero once
+  e = cudaMemset(h->counters, 0, sizeof(uint32_t) * (lstm_counter_words(h->Bmax) + 64));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
   for (int k = 0; k < kMaxLayers + 2 && e == cudaSuccess; ++k) {
     e = cudaEventCreateWithFlags(&h->ev_fork[k], cudaEventDisableTiming);

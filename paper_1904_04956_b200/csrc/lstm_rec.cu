@@ -80,6 +80,13 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target)
 //     8ks..8ks+7 = segment ks.
 constexpr int kFlagLine = 32;                   // words per line
 constexpr int kGroupFlagWords = 8 * kFlagLine;  // 8 lines per group (4 used)
+// Flag words per 128 batch rows: backward groups (2 directions) then forward
+// lines (2 directions x 2 blocks of 64 rows), so the two kernels never share
+// a word.  Flags are never reset: every CTA of a group publishes exactly T
+// times per launch, so all flags of a group are equal when a launch starts;
+// each CTA reads its own flag as the launch's base and waits / publishes
+// relative to it (no memset node ahead of every recurrent launch).
+constexpr int kFlagWords128 = 2 * kGroupFlagWords + 4 * kFlagLine;
 __device__ __forceinline__ uint32_t* fwd_flag(uint32_t* base, int f) { return base + (f >> 2) * kFlagLine + (f & 3); }
 __device__ __forceinline__ uint32_t* bwd_flag(uint32_t* base, int c) { return base + (c >> 3) * kFlagLine + (c & 7); }
 
@@ -181,7 +188,10 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
   const int pr = pg % kPairs;
   const int bb = (pg / kPairs) % P.n_btile;  // batch block of 64 (n_btile counts blocks here)
   const int dir = pg / (kPairs * P.n_btile);
-  uint32_t* flags = P.counters + (dir * P.n_btile + bb) * kFlagLine;  // 16 flags: CTA = 2*pair + rank
+  const int gblk = P.b0 / kNB + bb;  // global 64-row block
+  uint32_t* flags = P.counters + (size_t)(gblk >> 1) * kFlagWords128 + 2 * kGroupFlagWords +
+                    ((gblk & 1) * 2 + dir) * kFlagLine;  // 16 flags: CTA = 2*pair + rank
+  __shared__ uint32_t s_base;
   const int T = P.T, B = P.B;
   const int b0 = P.b0 + bb * kNB;
 
@@ -195,10 +205,12 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_pair(tmem_slot, 128);
+  if (threadIdx.x == 0) s_base = ld_relaxed_gpu(flags + (pr >> 2) * 8 + (pr & 3) * 2 + (int)rank);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t base = s_base;  // flag value at launch start (same for every CTA of the group)
 
   if (warp == 0) {
     if (elect_one()) {
@@ -220,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
           uint64_t* fb = &full[buf * 8 + k];
           if (leader) mbar_arrive_expect_tx(fb, 2 * kChunkB);
           if (s > 0) {  // chunk k of h_{t-1} = both CTAs of pair k (flags 2k, 2k+1)
-            wait_seg<2>(seg[k >> 2], flags + (k >> 2) * 8, (k & 3) * 2, (uint32_t)s);
+            wait_seg<2>(seg[k >> 2], flags + (k >> 2) * 8, (k & 3) * 2, base + (uint32_t)s);
             fence_proxy_async_global();
           }
           tma_load_2d_pair(sB + buf * kBufB + k * kChunkB, &P.tmA, full_c + (uint32_t)(buf * 8 + k) * 8,
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
     for (int s = 0; s < T; ++s) {
       named_bar_sync(kPub, kEpiT + 32);
       if (lane == 0) {
-        st_release_gpu(myflag, (uint32_t)(s + 1));
+        st_release_gpu(myflag, base + (uint32_t)(s + 1));
         trace_mark(P.trace, T, s, 4);
       }
       __syncwarp();
@@ -458,10 +470,12 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   const int ug = (blockIdx.x / kKS) % (kH / kGU);
   const int btile = (blockIdx.x / (kKS * (kH / kGU))) % P.n_btile;
   const int dir = blockIdx.x / (kKS * (kH / kGU) * P.n_btile);
-  uint32_t* flags = P.counters + (dir * P.n_btile + btile) * kGroupFlagWords;
+  uint32_t* flags = P.counters + (size_t)(P.b0 / 128 + btile) * kFlagWords128 + dir * kGroupFlagWords;
   const int T = P.T, B = P.B;
   const int brow0 = P.b0 + btile * 128;
   const int my_chunk = ug * kKS + ks;
+  __shared__ uint32_t s_base;
+  if (threadIdx.x == 0) s_base = ld_relaxed_gpu(bwd_flag(flags, my_chunk));
 
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < kStagesB; ++i) {
@@ -482,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   cluster_sync_all();  // peers' barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t base = s_base;  // flag value at launch start (same for every chunk of the group)
 
   if (warp == 0) {
     if (elect_one()) {
@@ -506,20 +521,20 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
           mbar_arrive_expect_tx(&full[stage], kTileA);
           if (kMulticastB) {  // the pair alternates chunks; multicast to both
             if ((j & 1) == upair) {
-              wait_flag(bwd_flag(flags, chunk), (uint32_t)s);
+              wait_flag(bwd_flag(flags, chunk), base + (uint32_t)s);
               acquire_for_tma(bwd_flag(flags, chunk), P.variant);
               tma_load_2d_mc(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow,
                              pair_mask);
             }
           } else {
             if (P.variant & 256) {  // experiment: relaxed polls, one acquire load once satisfied
-              if (seg.v[j] < (uint32_t)s) {
+              if (seg.v[j] < base + (uint32_t)s) {
                 do ld_relaxed_gpu_v8(myseg, seg.v);
-                while (seg.v[j] < (uint32_t)s);
+                while (seg.v[j] < base + (uint32_t)s);
                 ld_acquire_gpu_v8(myseg, seg.v);
               }
             } else {
-              wait_seg<1>(seg, myseg, j, (uint32_t)s);  // one 32-byte acquire poll covers the step's 8 chunks
+              wait_seg<1>(seg, myseg, j, base + (uint32_t)s);  // one 32-byte acquire poll covers the step's 8 chunks
             }
             if (!(P.variant & 128)) fence_proxy_async_global();
             tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
@@ -710,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
         }
       }
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
-      publish(bwd_flag(flags, my_chunk), (uint32_t)(s + 1), P.variant);
+      publish(bwd_flag(flags, my_chunk), base + (uint32_t)(s + 1), P.variant);
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 4);
     }
     if (threadIdx.x == kEpiWarp0 * 32) bulk_wait0();  // outgoing exchange copies complete
@@ -762,7 +777,7 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
 // 64 CTAs per 128-row batch tile in clusters of 4
 int lstm_max_tiles() { return (num_sms() >= 132 ? 128 : num_sms()) / 64; }
 static int lstm_bwd_max_tiles() { return lstm_max_tiles(); }
-int lstm_counter_words(int B) { return 2 * kGroupFlagWords * ((B + 127) / 128); }
+int lstm_counter_words(int B) { return kFlagWords128 * ((B + 127) / 128); }
 
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   static bool attr_set = false;
@@ -798,8 +813,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
       P.b0 = b0;
       P.nb = nb;
       P.n_btile = (nb + fwd2::kNB - 1) / fwd2::kNB;  // 64-row blocks
-      P.counters = a.counters + (b0 / fwd2::kNB) * 2 * kFlagLine;
-      DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * kFlagLine * P.n_btile, stream));
+      P.counters = a.counters;
       rc = launch_coop((const void*)lstm_fwd2_kernel, 2 * fwd2::kCtas * P.n_btile, P, stream, fwd2::kSmem, 2);
       if (rc) return rc;
       P.trace = nullptr;  // trace only the first chunk
@@ -835,8 +849,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.b0 = b0;
     P.nb = nb;
     P.n_btile = (nb + 127) / 128;
-    P.counters = a.counters + (b0 / 128) * 2 * kGroupFlagWords;
-    DS_CUDA_TRY(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * 2 * kGroupFlagWords * P.n_btile, stream));
+    P.counters = a.counters;
     rc = launch_coop((const void*)lstm_bwd_kernel, 64 * P.n_btile, P, stream, bwd::kSmem, bwd::kClB);
     if (rc) return rc;
     P.trace = nullptr;  // trace only the first chunk
