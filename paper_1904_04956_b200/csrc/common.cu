@@ -1,5 +1,6 @@
 // common.cu — error reporting, device queries and TMA descriptor encoding.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -45,6 +46,17 @@ static EncodeTiledFn get_encode() {
       fn = reinterpret_cast<EncodeTiledFn>(p);
   });
   return fn;
+}
+
+// Programmatic dependent launch for the big kernels (GEMM, recurrences, fused
+// soft-max/dZ); DS_NO_PDL=1 turns it off (A/B measurements).
+bool use_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 int make_tmap_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t outer,

@@ -157,6 +157,14 @@ DS_DEV void red_release_gpu_add(uint32_t* p, uint32_t v) {
 }
 
 // ----------------------------------------------------------------------------
+// programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialization attribute may start while its predecessor finishes;
+// griddep_wait() blocks until the predecessor grid completed and its memory
+// is visible, griddep_launch() lets this grid's own dependents start early.
+DS_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DS_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ----------------------------------------------------------------------------
 // clusters / distributed shared memory
 DS_DEV uint32_t cluster_ctarank() {
   uint32_t r;

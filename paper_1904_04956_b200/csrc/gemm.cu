@@ -171,6 +171,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / complete_tx
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done: wait for the predecessor's outputs, then let the next kernel start its own
+  griddep_wait();
+  griddep_launch();
 
 
   if (warp == 0) {
@@ -650,13 +653,15 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = use_pdl() ? 2 : 1;
   DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel, *b));
   return DS_OK;
 }

@@ -211,6 +211,9 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t base = s_base;  // flag value at launch start (same for every CTA of the group)
+  // programmatic launch: the W_hh slice (operand snapshot, not written by the predecessor) is
+  // fetched before waiting for the predecessor grid; everything else after
+  if (warp != 0) griddep_wait();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -219,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
       mbar_arrive_expect_tx(wbar, kWB);
       const int wrow = dir * 4 * kH + pr * 256 + (int)rank * 128;
       for (int kb = 0; kb < kH / 64; ++kb) tma_load_2d(sW + kb * 16384, &P.tmW, wbar, kb * 64, wrow);
+      griddep_wait();
       const uint32_t full_c = mapa_shared(smem_u32(full), 0);
       FlagSeg seg[2];
 #pragma unroll
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
 #pragma unroll
     for (int i = 0; i < 8; ++i) c[i] = 0.f;
     for (int s = 0; s < T; ++s) {
+      if (s == T - 1) griddep_launch();  // the next kernel may start its prologue
       const int t = dir == 0 ? s : T - 1 - s;
       // prefetch the input projection (i,f,g,o of this unit) for my 8 batch rows
       uint2 gp[8];
@@ -497,6 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t base = s_base;  // flag value at launch start (same for every chunk of the group)
+  if (warp != 0) griddep_wait();  // programmatic launch (see the forward kernel)
 
   if (warp == 0) {
     if (elect_one()) {
@@ -505,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
       mbar_arrive_expect_tx(wbar, kWBytesB);
       for (int j = 0; j < kChunks; ++j)  // W_hh rows (K) ks*512 + 64j.., units (N) ug*64..: MN-major boxes
         tma_load_2d(sW + j * 8192, &P.tmW, wbar, ug * kGU, dir * 4 * kH + ks * kKSlice + j * 64);
+      griddep_wait();
       int stage = 0;
       uint32_t phase = 0;
       FlagSeg seg;
@@ -607,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
 #pragma unroll
     for (int i = 0; i < 32; ++i) dbacc[i] = 0.f;
     for (int s = 0; s < T; ++s) {
+      if (s == T - 1) griddep_launch();  // the next kernel may start its prologue
       const int t = dir == 0 ? T - 1 - s : s;
       const int tc = dir == 0 ? t - 1 : t + 1;
       const bool has_cprev = tc >= 0 && tc < T;
@@ -751,7 +759,7 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
   if (cluster > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
@@ -762,6 +770,11 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
   } else {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na].val.cooperative = 1;
+    ++na;
+  }
+  if (use_pdl()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
   cfg.attrs = attr;

@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t acc2 = tmem + kAcc * kCT;
+  griddep_wait();  // lse / labels come from the immediately preceding kernels
+  griddep_launch();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -336,8 +338,17 @@ int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream) {
   if ((a.splits - 1) * P.ct_per >= P.n_ct) return fail_arg("fused soft-max/dZ: empty class range");
   const int items = P.n_rb * P.n_cs;
   const int grid = items < num_sms() ? items : num_sms();
-  ce_grad_dz_kernel<<<grid, kThreads, kSmem, stream>>>(P);
-  DS_CUDA_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, ce_grad_dz_kernel, P));
   return DS_OK;
 }
 
