@@ -50,6 +50,7 @@ struct ds_blstm {
   float* splitk = nullptr;    // split-K fp32 partials of dZ
   uint32_t* counters = nullptr;
   float* d_lr = nullptr;  // fused training step: learning rate read by the SGD kernels
+  float lr_host = -1.f;   // value last written to d_lr (written again only when it changes)
   // fused training step: per-layer SGD on a side stream while the next BPTT runs
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork[kMaxLayers + 2] = {}, ev_join[kMaxLayers + 2] = {};
@@ -333,8 +334,11 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   }
 
   // ---- backward ----
+  GemmProblem pwo;  // fused path: dW_o joins the dW_b / dY launch below
+  bool have_wo = false;
   if (fused_ce_dz(h)) {
-    // soft-max gradient + dZ in one pass (softmax_dz.cu), then dW_o alone
+    // soft-max gradient + dZ in one pass (softmax_dz.cu); dW_o then shares one GEMM launch
+    // with dW_b and dY (their tiles fill the wave-quantisation gap of dW_o's 125 tiles)
     const int S = fused_dz_splits(h, N);
     CeGradDzArgs ca;
     ca.z = h->z;
@@ -365,18 +369,13 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     if (rs != s) DS_CUDA_TRY(cudaEventRecord(h->ev_aux[1], rs));
     aux_join = rs != s;
     TRY(op_splitk_bf16(h->splitk, S, (int64_t)N * bott, h->dz, s));
-    GemmBatch gb;
-    memset(&gb, 0, sizeof(gb));
-    gb.nprob = 1;
-    GemmProblem& p0 = gb.p[0];  // dW_o = dlogits^T Z
-    TRY(gemm_problem(&p0, h->dlogits, C, 1, h->z, bott, 1, C, bott, N));
-    TRY(gemm_blocked_a(&p0, h->dlogits, N, C));
-    p0.epi = EPI_F32;
-    p0.out = grad + L.off_wo;
-    p0.ldo = bott;
-    MARK(PH_GEMM);
-    TRY(gemm_launch(&gb, s));
-    nl += 4;
+    TRY(gemm_problem(&pwo, h->dlogits, C, 1, h->z, bott, 1, C, bott, N));  // dW_o = dlogits^T Z
+    TRY(gemm_blocked_a(&pwo, h->dlogits, N, C));
+    pwo.epi = EPI_F32;
+    pwo.out = grad + L.off_wo;
+    pwo.ldo = bott;
+    have_wo = true;
+    nl += 3;
   } else {
   {
     GemmBatch gb;
@@ -440,16 +439,18 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   {
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
-    gb.nprob = 2;
-    GemmProblem& p0 = gb.p[0];  // dW_b = dZ^T Y (split-K fp32 partials, reduced below in split order)
+    const int q0 = have_wo ? 1 : 0;
+    if (have_wo) gb.p[0] = pwo;
+    gb.nprob = q0 + 2;
+    GemmProblem& p0 = gb.p[q0];  // dW_b = dZ^T Y (alone: split-K fp32 partials, reduced below in split order)
     TRY(gemm_problem(&p0, h->dz, bott, 1, Y(Lh - 1), kLayerOut, 1, bott, kLayerOut, N));
     p0.epi = EPI_F32;
-    const int Sb = ksplit_for(N, kWbSplit);
+    const int Sb = have_wo ? 1 : ksplit_for(N, kWbSplit);
     p0.out = Sb > 1 ? h->splitk : grad + L.off_wb;
     p0.ldo = kLayerOut;
     p0.ksplit = Sb;
     p0.split_stride = (long long)bott * kLayerOut;
-    GemmProblem& p1 = gb.p[1];  // dY = dZ W_b
+    GemmProblem& p1 = gb.p[q0 + 1];  // dY = dZ W_b
     TRY(gemm_problem(&p1, h->dz, bott, 0, h->snap + L.off_wb, kLayerOut, 1, N, kLayerOut, bott));
     p1.epi = EPI_BF16;
     p1.out = h->dy;
@@ -707,8 +708,13 @@ int ds_blstm_train_step(ds_blstm* h, const int64_t* idx, int32_t B, float* theta
     return fail_arg("sgd: buffers must be 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   DS_CUDA_TRY(cudaSetDevice(h->device));
-  // pageable source: staged by the driver before the call returns
-  DS_CUDA_TRY(cudaMemcpyAsync(h->d_lr, &lr, sizeof(float), cudaMemcpyHostToDevice, s));
+  // pageable source: staged by the driver before the call returns.  Only when the rate
+  // changes (schedules change it per epoch): a copy-engine node ahead of every step's graph
+  // costs several microseconds of device time
+  if (lr != h->lr_host) {
+    DS_CUDA_TRY(cudaMemcpyAsync(h->d_lr, &lr, sizeof(float), cudaMemcpyHostToDevice, s));
+    h->lr_host = lr;
+  }
   SgdCtx sg;
   sg.theta = theta;
   sg.vel = vel;
