@@ -277,209 +277,6 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-// ---------------------------------------------------------------------------
-// Soft-max statistics (loss pass).  Z block in tensor memory (MMA A operand,
-// copied in row-per-lane by the epilogue warps), W_o streamed in 64-class
-// tiles through a 6-stage ring (a stage is released as soon as its MMA1
-// completes), logits in four TMEM buffers.  With A in TMEM the N=64 MMA reads
-// only its 2 KB B slice from shared memory per instruction (an SS MMA of that
-// shape is bound by shared-memory operand bandwidth).  All 16 epilogue warps
-// take every tile (32 rows x 16 classes each: lane quadrant x class quarter),
-// keep a running (max, sum 2^(x - max)) per row in registers and release the
-// accumulator right after reading it; the four class quarters of a row are
-// merged through shared memory once per item.
-namespace st {
-constexpr int kWStages = 6;
-constexpr int kAcc = 4;
-constexpr int kQ = kCT / 4;            // classes per warp and tile
-constexpr int kZCols = kMaxBott / 2;   // Z row in TMEM: 2 bf16 per 32-bit column
-constexpr size_t kSmem = 1024 + kWStages * kWB + 4 * kRows * 8 + 256;
-}  // namespace st
-
-__global__ void __launch_bounds__(kThreads, 1) ce_stats_kernel(const __grid_constant__ CeStatsParams P) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sW = sm;
-  float2* sPart = reinterpret_cast<float2*>(sW + st::kWStages * kWB);  // [4 quarters][128 rows]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sPart + 4 * kRows);
-  uint64_t* zready = bars;                  // Z block written into TMEM (16 epilogue warps)
-  uint64_t* zfree = zready + 1;             // MMA1s of the item done with it
-  uint64_t* wfull = zfree + 1;              // [kWStages]
-  uint64_t* wempty = wfull + st::kWStages;  // [kWStages]
-  uint64_t* tfull = wempty + st::kWStages;  // [kAcc]
-  uint64_t* tempty = tfull + st::kAcc;      // [kAcc]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + st::kAcc);
-
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const int bott = P.bott, nkb = bott / 64;
-  const int items = P.n_rb * P.n_cs;
-  unsigned long long* const tr = P.trace ? P.trace + (size_t)blockIdx.x * 80 * 4 : nullptr;
-  if (warp == 1 && lane == 0) {
-    mbar_init(zready, kEpiWarps);
-    mbar_init(zfree, 1);
-    for (int i = 0; i < st::kWStages; ++i) {
-      mbar_init(&wfull[i], 1);
-      mbar_init(&wempty[i], 1);
-    }
-    for (int i = 0; i < st::kAcc; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tlog = tmem + st::kZCols;  // logits buffers after the Z block
-  griddep_wait();  // Z comes from the preceding bottleneck GEMM
-  griddep_launch();
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&P.tmW);
-      int g = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int cs = item / P.n_rb;
-        const int ct0 = cs * P.ct_per, ct1 = min(P.n_ct, ct0 + P.ct_per);
-        for (int ct = ct0; ct < ct1; ++ct, ++g) {
-          const int stg = g % st::kWStages;
-          mbar_wait(&wempty[stg], ((g / st::kWStages) & 1) ^ 1);
-          if (tr && g < 80) tr[g * 4 + 1] = globaltimer();
-          mbar_arrive_expect_tx(&wfull[stg], kCT * bott * 2);
-          for (int kb = 0; kb < nkb; ++kb)
-            tma_load_2d(sW + stg * kWB + kb * (kCT * 128), &P.tmW, &wfull[stg], kb * 64, ct * kCT);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (elect_one()) {
-      const uint32_t id1 = idesc_bf16_f32(kRows, kCT, 0, 0);
-      const uint32_t wb = smem_u32(sW);
-      int g = 0, it = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        const int cs = item / P.n_rb;
-        const int ct0 = cs * P.ct_per, ct1 = min(P.n_ct, ct0 + P.ct_per);
-        mbar_wait(zready, it & 1);
-        tc_fence_after();
-        for (int ct = ct0; ct < ct1; ++ct, ++g) {
-          const int stg = g % st::kWStages, a = g % st::kAcc;
-          mbar_wait(&wfull[stg], (g / st::kWStages) & 1);
-          mbar_wait(&tempty[a], ((g / st::kAcc) & 1) ^ 1);
-          tc_fence_after();
-          if (tr && g < 80) tr[g * 4 + 0] = globaltimer();
-#pragma unroll 1
-          for (int kk = 0; kk < bott / 16; ++kk) {
-            const uint64_t bd = smem_desc_sw128(wb + stg * kWB + (kk >> 2) * (kCT * 128) + (kk & 3) * 32, 16, 1024);
-            mma_bf16_ts(tlog + a * kCT, tmem + kk * 8, bd, id1, kk ? 1u : 0u);
-          }
-          mma_commit(&tfull[a]);
-          mma_commit(&wempty[stg]);
-        }
-        mma_commit(zfree);
-      }
-    }
-  } else if (warp >= kEpiWarp0) {
-    const uint32_t e = warp - kEpiWarp0;
-    const uint32_t q = e & 3, part = e >> 2;  // lane quadrant, class quarter of the tile / Z quarter
-    const uint32_t tq = tlog + ((q * 32) << 16) + part * st::kQ;
-    const int rloc = (int)(q * 32 + lane);
-    int g = 0, it = 0;
-    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-      const int rb = item % P.n_rb, cs = item / P.n_rb;
-      const int ct0 = cs * P.ct_per, ct1 = min(P.n_ct, ct0 + P.ct_per);
-      const int row = rb * kRows + rloc;
-      const bool row_ok = row < P.m_valid;
-      const int lbl = row_ok ? P.labels[row] : -1;
-      {  // Z row quarter -> TMEM columns part * bott/8 .. (packed bf16 pairs, lane = row)
-        const int zc = bott / 8;  // columns per quarter
-        const uint4* zr = reinterpret_cast<const uint4*>(P.z + (size_t)row * bott + part * (bott / 4));
-        if (it > 0) mbar_wait(zfree, (it - 1) & 1);  // previous item's MMA1s are done with the block
-        tc_fence_after();
-        for (int c8 = 0; c8 < zc; c8 += 8) {
-          uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
-          if (row_ok) {
-            w0 = __ldg(zr + c8 / 4);
-            w1 = __ldg(zr + c8 / 4 + 1);
-          }
-          const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-          tmem_st8(tmem + ((q * 32) << 16) + part * zc + c8, u);
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(zready);
-      }
-      float mx = -INFINITY, se = 0.f, tg = 0.f;
-      bool have_t = false;
-      float bnext = __ldg(P.bias_log2 + ct0 * kCT + (int)part * st::kQ + (lane & (st::kQ - 1)));
-      for (int ct = ct0; ct < ct1; ++ct, ++g) {
-        const int a = g % st::kAcc;
-        const int nb = ct * kCT + (int)part * st::kQ;
-        const float bsrc = bnext;
-        mbar_wait(&tfull[a], (g / st::kAcc) & 1);
-        tc_fence_after();
-        if (tr && g < 80 && e == 0 && lane == 0) tr[g * 4 + 2] = globaltimer();
-        float v[st::kQ];
-        tmem_ld16(tq + a * kCT, v);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[a]);  // accumulator free for MMA1 of tile g + kAcc
-        if (ct + 1 < ct1) bnext = __ldg(P.bias_log2 + nb + kCT + (lane & (st::kQ - 1)));
-        // logits in the log2 domain: one FFMA with the log2(e)-scaled bias
-        float m4[4];
-#pragma unroll
-        for (int i = 0; i < st::kQ; ++i) v[i] = fmaf(v[i], kLog2e, __shfl_sync(0xffffffffu, bsrc, i));
-#pragma unroll
-        for (int i = 0; i < 4; ++i) m4[i] = fmaxf(fmaxf(v[4 * i], v[4 * i + 1]), fmaxf(v[4 * i + 2], v[4 * i + 3]));
-        const float cm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-        if (lbl >= nb && lbl < nb + st::kQ) {
-#pragma unroll
-          for (int i = 0; i < st::kQ; ++i)
-            if (lbl == nb + i) tg = v[i];
-          have_t = true;
-        }
-        const float nm = fmaxf(mx, cm);
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-        for (int i = 0; i < st::kQ; i += 4) {
-          s0 += ex2_fast(v[i] - nm);
-          s1 += ex2_fast(v[i + 1] - nm);
-          s2 += ex2_fast(v[i + 2] - nm);
-          s3 += ex2_fast(v[i + 3] - nm);
-        }
-        se = se * ex2_fast(mx - nm) + ((s0 + s1) + (s2 + s3));
-        mx = nm;
-        if (tr && g < 80 && e == 0 && lane == 0) tr[g * 4 + 3] = globaltimer();
-      }
-      if (have_t && row_ok) P.tgt[row] = tg / kLog2e;
-      // merge the four class quarters of each row (natural-log units on output)
-      sPart[part * kRows + rloc] = make_float2(mx, se);
-      named_bar_sync(1, kEpiWarps * 32);
-      if (part == 0 && row_ok) {
-        float M = sPart[rloc].x;
-#pragma unroll
-        for (int k = 1; k < 4; ++k) M = fmaxf(M, sPart[k * kRows + rloc].x);
-        float S = 0.f;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 pk = sPart[k * kRows + rloc];
-          if (pk.y > 0.f) S += pk.y * ex2_fast(pk.x - M);
-        }
-        P.stats[(size_t)cs * P.stats_ld + row] = make_float2(M / kLog2e, S);
-      }
-      named_bar_sync(1, kEpiWarps * 32);  // sPart reused by the next item
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 512);
-}
-
 }  // namespace
 
 bool ce_grad_dz_supported(int classes, int bott) {
@@ -552,47 +349,6 @@ int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = use_pdl() ? 1 : 0;
   DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, ce_grad_dz_kernel, P));
-  return DS_OK;
-}
-
-int ce_stats_launch(const CeStatsArgs& a, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    DS_CUDA_TRY(cudaFuncSetAttribute(ce_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st::kSmem));
-    attr_set = true;
-  }
-  if (!ce_grad_dz_supported(a.classes, a.bott)) return fail_arg("soft-max statistics: unsupported shape");
-  CeStatsParams P;
-  memset(&P, 0, sizeof(P));
-  int rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.bott, a.classes, (uint64_t)a.bott * 2, 64, kCT);
-  if (rc) return rc;
-  P.z = a.z;
-  P.bias_log2 = a.bias_log2;
-  P.labels = a.labels;
-  P.stats = a.stats;
-  P.stats_ld = a.stats_ld;
-  P.tgt = a.tgt;
-  P.trace = g_trace;
-  P.bott = a.bott;
-  P.classes = a.classes;
-  P.m_valid = a.rows;
-  P.n_rb = (a.rows + kRows - 1) / kRows;
-  P.n_ct = a.classes / kCT;
-  P.n_cs = a.splits;
-  P.ct_per = (P.n_ct + a.splits - 1) / a.splits;
-  if ((a.splits - 1) * P.ct_per >= P.n_ct) return fail_arg("soft-max statistics: empty class range");
-  const int items = P.n_rb * P.n_cs;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(items < num_sms() ? items : num_sms());
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = st::kSmem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = use_pdl() ? 1 : 0;
-  DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, ce_stats_kernel, P));
   return DS_OK;
 }
 

@@ -36,34 +36,6 @@ struct CeGradDzArgs {
   int rows, classes, bott, splits;
 };
 
-// Soft-max statistics of the logits Z W_o^T + b_o (the loss pass): per row and
-// class range, (max, sum exp(x - max)) in natural-log units, plus the target
-// logit of every labelled row.  Same row-block x class-range work split as the
-// gradient kernel; combined across ranges by op_ce_combine.
-struct CeStatsArgs {
-  const __nv_bfloat16* z;
-  const __nv_bfloat16* w;
-  const float* bias_log2;  // b_o * log2(e)
-  const int* labels;
-  float2* stats;           // [splits][stats_ld]
-  int64_t stats_ld;
-  float* tgt;              // [rows]
-  int rows, classes, bott, splits;
-};
-struct CeStatsParams {
-  CUtensorMap tmW;
-  const __nv_bfloat16* z;  // [rows][bott], copied row-per-lane into tensor memory (MMA A operand)
-  const float* bias_log2;
-  const int* labels;
-  float2* stats;
-  int64_t stats_ld;
-  float* tgt;
-  int bott, classes, m_valid;
-  int n_rb, n_ct, n_cs, ct_per;
-  unsigned long long* trace;  // debug timeline (shares ce_grad_dz_set_trace), null in production
-};
-int ce_stats_launch(const CeStatsArgs& a, cudaStream_t stream);
-
 bool ce_grad_dz_supported(int classes, int bott);
 int ce_grad_dz_splits(int rows, int classes, int max_splits);  // class ranges per row block (none empty)
 int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream);
