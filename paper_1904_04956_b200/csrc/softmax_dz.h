@@ -8,9 +8,10 @@
 namespace ds {
 
 struct CeGradDzParams {
-  CUtensorMap tmZ;  // Z [rows][bott] bf16, box 64 x 128
-  CUtensorMap tmW;  // W_o [classes][bott] bf16 (operand snapshot), box 64 x 128
-  CUtensorMap tmP;  // dlogits, 64x64-blocked 4D [ceil(rows/64)][classes/64][64][64], box 16 x 32 (TMA store)
+  CUtensorMap tmZ;   // Z [rows][bott] bf16, box 64 x 128
+  CUtensorMap tmW1;  // W_o [classes][bott] bf16 (operand snapshot), box 64 x 64 (MMA1 view)
+  CUtensorMap tmW2;  // same tensor, box 64 x 128 (MMA2 view)
+  CUtensorMap tmP;   // dlogits, 64x64-blocked 4D [ceil(rows/64)][classes/64][64][64], box 32 x 32 (TMA store)
   const float* bias;    // b_o [classes]
   const int* labels;    // [rows], -1 = no target
   const float* lse;     // [rows]
@@ -18,7 +19,7 @@ struct CeGradDzParams {
   float* dzpart;        // [n_cs][rows][bott] fp32 dZ partials
   float scale;          // 1 / frames
   int bott, classes, m_valid, dz_rows;
-  int n_rb, n_ct, n_cs, ct_per;
+  int n_rbp, n_ct, n_cs, ct_per;  // row-block pairs, 128-class tiles, class ranges, tiles per range
   unsigned long long* trace;  // debug timeline (tools/cedz_trace.py), null in production
 };
 void ce_grad_dz_set_trace(unsigned long long* buf);

@@ -20,7 +20,8 @@ for r in data:
     d = launch.setdefault(r[ii], {"name": r[ki].split("(")[0].replace("ds::<unnamed>::", "")})
     v = float(r[vi].replace(",", ""))
     u = r[ui]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1,
+             "msecond": 1e3, "ms": 1e3}
     d[r[mi]] = v * scale.get(u, 1)
 seq = list(launch.values())
 gi = [i for i, s in enumerate(seq) if "gather" in s["name"]]
