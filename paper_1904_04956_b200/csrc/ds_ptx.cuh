@@ -400,8 +400,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N, ui
 // Column sums of a warp's 32 x 32 block (lane = row, v[j] = column j): a
 // butterfly reduce-scatter (16+8+4+2+1 = 31 shuffles); on return lane L's
 // v[0] holds the sum of column L over the 32 lanes (fixed order: deterministic).
-DS_DEV float warp_colsum32(float* v) {
-  const uint32_t lane = lane_id();
+DS_DEV float warp_colsum32(float* v, uint32_t lane) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     const bool up = (lane & off) != 0;

@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             store_bf16x16(orow + nb + 16, v + 16);
           }
           if (colpart && rt * BM < P.m_valid) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
-            const float cs = warp_colsum32(v);
+            const float cs = warp_colsum32(v, lane);
             colpart[(size_t)(rt * 4 + q) * n_valid + nb + lane] = cs;
           }
         }

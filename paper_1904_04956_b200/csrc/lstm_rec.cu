@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
     }
     if (threadIdx.x == kEpiWarp0 * 32) bulk_wait0();  // outgoing exchange copies complete
     if (P.dbpart) {  // fused bias gradient: sum over this warp's 32 batch rows and all steps
-      const float cs = warp_colsum32(dbacc);
+      const float cs = warp_colsum32(dbacc, lane);
       P.dbpart[((size_t)(P.b0 / 128 + btile) * 4 + q) * (8 * kH) + col_g + lane] = cs;
     }
   }

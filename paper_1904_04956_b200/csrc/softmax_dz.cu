@@ -40,13 +40,14 @@ constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 16;
 constexpr int kRows = 128;      // Z rows per CTA (MMA M per CTA)
 constexpr int kCT = 128;        // classes per tile (MMA1 N, MMA2 K)
-constexpr int kWarpCls = kCT / 4;  // classes per epilogue warp and tile (4 parts x 4 lane quadrants)
+constexpr int kPartCls = 32;       // classes per epilogue chunk / TMEM hand-off slice
+constexpr int kWarpCls = 64;       // classes per epilogue warp and tile (2 halves x 4 lane quadrants per group)
 constexpr int kMaxBott = 256;
 constexpr int kZB = kRows * kMaxBott * 2;        // 64 KB resident Z block
 constexpr int kW1B = (kCT / 2) * kMaxBott * 2;   // 32 KB MMA1 view: 64 classes x bott
 constexpr int kW2B = kCT * (kMaxBott / 2) * 2;   // 32 KB MMA2 view: 128 classes x bott/2
-constexpr int kCB = 32 * kWarpCls * 2;           // 2 KB dlogits box per epilogue warp
-constexpr size_t kSmem = 1024 + kZB + 2 * kW1B + 2 * kW2B + kEpiWarps * kCB + 512;
+constexpr int kCB = 32 * kWarpCls * 2;           // 4 KB dlogits box per epilogue warp (32 rows x 64 classes)
+constexpr size_t kSmem = 1024 + kZB + 2 * kW1B + kW2B + kEpiWarps * kCB + 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
 __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_constant__ CeGradDzParams P) {
@@ -54,18 +55,18 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sZ = sm;
   uint8_t* sW1 = sZ + kZB;        // [2]
-  uint8_t* sW2 = sW1 + 2 * kW1B;  // [2]
-  uint8_t* sC = sW2 + 2 * kW2B;   // [kEpiWarps] dlogits store boxes
+  uint8_t* sW2 = sW1 + 2 * kW1B;  // single stage: loaded while the epilogue runs
+  uint8_t* sC = sW2 + kW2B;       // [kEpiWarps] dlogits store boxes (SW128)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kEpiWarps * kCB);
   uint64_t* zfull = bars;          // leader: both CTAs' Z blocks landed
   uint64_t* zempty = zfull + 1;    // every CTA: the item's MMA1s are done with its Z
   uint64_t* w1full = zempty + 1;   // [2] leader
   uint64_t* w1empty = w1full + 2;  // [2] every CTA
-  uint64_t* w2full = w1empty + 2;  // [2] leader
-  uint64_t* w2empty = w2full + 2;  // [2] every CTA
-  uint64_t* tfull = w2empty + 2;   // [2] every CTA: logits ready
+  uint64_t* w2full = w1empty + 2;  // leader
+  uint64_t* w2empty = w2full + 1;  // every CTA
+  uint64_t* tfull = w2empty + 1;   // [2] every CTA: logits ready
   uint64_t* tempty = tfull + 2;    // [2] leader: MMA2 read the dlogits written back into the buffer
-  uint64_t* pfull = tempty + 2;    // [2] leader: all 32 epilogue warps of the pair wrote their slice
+  uint64_t* pfull = tempty + 2;    // [2] leader: the 2 x 8 epilogue warps owning the tile wrote their slices
   uint64_t* dzfull = pfull + 2;    // every CTA: dZ accumulator complete
   uint64_t* dzempty = dzfull + 1;  // leader: both CTAs drained their dZ accumulators
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dzempty + 1);
@@ -85,12 +86,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
     for (int i = 0; i < 2; ++i) {
       mbar_init(&w1full[i], 1);
       mbar_init(&w1empty[i], 1);
-      mbar_init(&w2full[i], 1);
-      mbar_init(&w2empty[i], 1);
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 1);
-      mbar_init(&pfull[i], 2 * kEpiWarps);
+      mbar_init(&pfull[i], kEpiWarps);  // 8 warps per CTA x 2 CTAs
     }
+    mbar_init(w2full, 1);
+    mbar_init(w2empty, 1);
     mbar_init(dzfull, 1);
     mbar_init(dzempty, 2 * kEpiWarps);
     fence_barrier_init();
@@ -112,7 +113,6 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
       tma_prefetch_desc(&P.tmP);
       const uint32_t zfull_c = mapa_shared(smem_u32(zfull), 0);
       const uint32_t w1full_c = mapa_shared(smem_u32(w1full), 0);
-      const uint32_t w2full_c = mapa_shared(smem_u32(w2full), 0);
       int g = 0, it = 0;  // global class-tile counter, item counter
       for (int item = pair; item < items; item += npairs, ++it) {
         const int rbp = item % P.n_rbp, cs = item / P.n_rbp;
@@ -129,12 +129,21 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
           if (leader) mbar_arrive_expect_tx(&w1full[s], 2 * (kCT / 2) * bott * 2);
           for (int kb = 0; kb < nkb; ++kb)
             tma_load_2d_pair(sW1 + s * kW1B + kb * 8192, &P.tmW1, w1full_c + s * 8, kb * 64, ct * kCT + (int)rank * 64);
-          // MMA2 view: all 128 classes of the tile, bott rank*bott/2 .. (MN-major 128 x 64 blocks)
-          mbar_wait(&w2empty[s], ph);
-          if (leader) mbar_arrive_expect_tx(&w2full[s], 2 * kCT * (bott / 2) * 2);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (elect_one()) {  // MMA2 view producer: all 128 classes of the tile, bott rank*bott/2 .. (MN-major 128 x 64)
+      const uint32_t w2full_c = mapa_shared(smem_u32(w2full), 0);
+      int g = 0;
+      for (int item = pair; item < items; item += npairs) {
+        const int cs = item / P.n_rbp;
+        const int ct0 = cs * P.ct_per, ct1 = min(P.n_ct, ct0 + P.ct_per);
+        for (int ct = ct0; ct < ct1; ++ct, ++g) {
+          mbar_wait(w2empty, (g & 1) ^ 1);  // MMA2 of the previous tile is done with the stage
+          if (leader) mbar_arrive_expect_tx(w2full, 2 * kCT * (bott / 2) * 2);
           for (int j = 0; j < nkb / 2; ++j)
-            tma_load_2d_pair(sW2 + s * kW2B + j * 16384, &P.tmW2, w2full_c + s * 8, (int)rank * (bott / 2) + j * 64,
-                             ct * kCT);
+            tma_load_2d_pair(sW2 + j * 16384, &P.tmW2, w2full_c, (int)rank * (bott / 2) + j * 64, ct * kCT);
         }
       }
     }
@@ -147,18 +156,18 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
       auto mma2 = [&](int gp, bool first) {  // dZ += dlogits(gp) W_o(gp), dlogits from TMEM
         const int s = gp & 1;
         mbar_wait_acq_cluster(&pfull[s], (gp >> 1) & 1);
-        mbar_wait(&w2full[s], (gp >> 1) & 1);
+        mbar_wait(w2full, gp & 1);
         tc_fence_after();
         if (tr && gp < 80) tr[gp * 4 + 1] = globaltimer();
 #pragma unroll
         for (int kk = 0; kk < kCT / 16; ++kk) {
-          // classes kk*16.. : written by column part kk/2 into its columns (kk&1)*8..
-          const uint32_t at = tmem + s * kCT + (kk >> 1) * kWarpCls + (kk & 1) * 8;
-          const uint64_t bd = smem_desc_sw128(w2b + s * kW2B + kk * 2048, 16384, 1024);
+          // classes kk*16.. : written as slice kk/2 (32 classes) into its first columns (kk&1)*8..
+          const uint32_t at = tmem + s * kCT + (kk >> 1) * kPartCls + (kk & 1) * 8;
+          const uint64_t bd = smem_desc_sw128(w2b + kk * 2048, 16384, 1024);
           mma_bf16_ts_pair(acc2, at, bd, id2, (!first || kk) ? 1u : 0u);
         }
         mma_commit_pair_mc(&tempty[s], 0x1);
-        mma_commit_pair_mc(&w2empty[s], 0x3);
+        mma_commit_pair_mc(w2empty, 0x3);
       };
       for (int item = pair; item < items; item += npairs, ++it) {
         const int cs = item / P.n_rbp;
@@ -189,9 +198,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
       }
     }
   } else if (warp >= kEpiWarp0) {
+    // two groups of 8 warps take alternate tiles (group = TMEM buffer), so one group's TMEM
+    // reads and exponentials overlap the other's stores and column sums
     const uint32_t e = warp - kEpiWarp0;
-    const uint32_t q = e & 3;    // TMEM lane quadrant (== warp % 4)
-    const uint32_t part = e >> 2;  // 32-class quarter of the tile
+    const uint32_t q = e & 3;            // TMEM lane quadrant (== warp % 4)
+    const uint32_t half = (e >> 2) & 1;  // 64-class half of the tile
+    const int grp = (int)(e >> 3);       // tiles with g % 2 == grp
     const uint32_t tq = tmem + ((q * 32) << 16);
     const float* __restrict__ bias = P.bias;
     uint8_t* const myC = sC + e * kCB;
@@ -208,72 +220,91 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
       const float l2 = row_ok ? P.lse[row] * kLog2e : 0.f;
       const float sc = (row_ok && lbl >= 0) ? P.scale : 0.f;
       const int r0 = rb * kRows + (int)q * 32;  // first row of this warp's dlogits box
-      float bnext = __ldg(bias + ct0 * kCT + (int)part * kWarpCls + lane);
-      for (int ct = ct0; ct < ct1; ++ct, ++g) {
+      // own tiles: g % 2 == grp; lane i holds the bias of classes nb+i and nb+32+i, one own tile ahead
+      int c = ct0 + (((grp - g) % 2 + 2) % 2);
+      g += c - ct0;
+      float bn0 = 0.f, bn1 = 0.f;
+      if (c < ct1) {
+        bn0 = __ldg(bias + c * kCT + (int)half * kWarpCls + lane);
+        bn1 = __ldg(bias + c * kCT + (int)half * kWarpCls + kPartCls + lane);
+      }
+      for (; c < ct1; c += 2, g += 2) {
         const int s = g & 1;
-        const int nb = ct * kCT + (int)part * kWarpCls;
-        const float bsrc = bnext;
+        const int nb = c * kCT + (int)half * kWarpCls;
+        const float bs0 = bn0, bs1 = bn1;
         mbar_wait(&tfull[s], (g >> 1) & 1);
         tc_fence_after();
-        if (tr && g < 80 && e == 0 && lane == 0) tr[g * 4 + 2] = globaltimer();
-        float v[kWarpCls];
-        const uint32_t tcol = tq + s * kCT + part * kWarpCls;
-        tmem_ld32(tcol, v);
-        tmem_ld_wait();
+        if (tr && g < 80 && (e & 7) == 0 && lane == 0) tr[g * 4 + 2] = globaltimer();
+        if (lane == 0) bulk_wait_read0();  // this warp's previous box store has read the box
+        __syncwarp();
+        float cs0 = 0.f, cs1 = 0.f;
+#pragma unroll 1
+        for (int k = 0; k < 2; ++k) {  // two 32-class chunks
+          const int nk = nb + k * kPartCls;
+          const float bsrc = k ? bs1 : bs0;
+          float v[kPartCls];
+          const uint32_t tcol = tq + s * kCT + half * kWarpCls + k * kPartCls;
+          tmem_ld32(tcol, v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < kWarpCls; ++i)
-          v[i] = ex2_fast(fmaf(v[i] + __shfl_sync(0xffffffffu, bsrc, i), kLog2e, -l2));
-        if (lbl >= nb && lbl < nb + kWarpCls) {
+          for (int i = 0; i < kPartCls; ++i)
+            v[i] = ex2_fast(fmaf(v[i] + __shfl_sync(0xffffffffu, bsrc, i), kLog2e, -l2));
+          if (lbl >= nk && lbl < nk + kPartCls) {
 #pragma unroll
-          for (int i = 0; i < kWarpCls; ++i)
-            if (lbl == nb + i) v[i] -= 1.f;
+            for (int i = 0; i < kPartCls; ++i)
+              if (lbl == nk + i) v[i] -= 1.f;
+          }
+          uint32_t u[kPartCls / 2];
+#pragma unroll
+          for (int i = 0; i < kPartCls / 2; ++i) {
+            v[2 * i] *= sc;
+            v[2 * i + 1] *= sc;
+            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            u[i] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          // dlogits back into the first 16 columns of the chunk's TMEM slice (MMA2 operand)
+          tmem_st16(tcol, u);
+          tmem_st_wait();  // u is rewritten by the next chunk
+          // and into the box (row = lane, 128-byte rows, 128-byte swizzle)
+          const uint32_t d = smem_u32(myC) + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t chunk = (uint32_t)(k * 4 + j);
+            st_shared_v4(d + ((chunk ^ (lane & 7)) << 4), u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
+          }
+          if (P.colpart) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
+            const float csum = warp_colsum32(v, lane);
+            if (k) cs1 = csum; else cs0 = csum;
+          }
         }
-        uint32_t u[kWarpCls / 2];
-#pragma unroll
-        for (int i = 0; i < kWarpCls / 2; ++i) {
-          v[2 * i] *= sc;
-          v[2 * i + 1] *= sc;
-          __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-          u[i] = *reinterpret_cast<uint32_t*>(&h);
-        }
-        // dlogits back into the first 16 columns of this warp's logits slice, for MMA2
-        tmem_st16(tcol, u);
-        tmem_st_wait();
         tc_fence_before();
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
+          tma_store_4d(&P.tmP, myC, 0, r0 & 63, nb >> 6, r0 >> 6);
+          bulk_commit();
           if (leader)
             mbar_arrive(&pfull[s]);
           else
             mbar_arrive_remote(pfull_c + s * 8);
         }
-        {  // dlogits box (32 rows x 32 classes) -> blocked global via TMA
-          if (lane == 0) bulk_wait_read0();  // this warp's previous store has read the box
-          __syncwarp();
-          const uint32_t d = smem_u32(myC) + lane * 64;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) st_shared_v4(d + j * 16, u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_4d(&P.tmP, myC, nb & 63, r0 & 63, nb >> 6, r0 >> 6);
-            bulk_commit();
-          }
+        if (P.colpart && rb * kRows < P.m_valid) {
+          float* cp = P.colpart + (size_t)(rb * 4 + q) * P.classes + nb + lane;
+          cp[0] = cs0;
+          cp[kPartCls] = cs1;
         }
-        // next tile's bias: issued after the proxy fence above (which waits for this
-        // thread's outstanding loads), so its latency hides behind the rest of this tile
-        if (ct + 1 < ct1) bnext = __ldg(bias + nb + kCT + lane);
-        if (P.colpart) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
-          const float csum = warp_colsum32(v);
-          if (rb * kRows < P.m_valid) P.colpart[(size_t)(rb * 4 + q) * P.classes + nb + lane] = csum;
+        if (c + 2 < ct1) {  // next own tile's bias (after the proxy fence, which waits for loads in flight)
+          bn0 = __ldg(bias + nb + 2 * kCT + lane);
+          bn1 = __ldg(bias + nb + 2 * kCT + kPartCls + lane);
         }
-        if (tr && g < 80 && e == 0 && lane == 0) tr[g * 4 + 3] = globaltimer();
+        if (tr && g < 80 && (e & 7) == 0 && lane == 0) tr[g * 4 + 3] = globaltimer();
       }
+      g -= c - ct1;  // back to the item's tile count (the loop stepped past ct1)
       // dZ partial of this (row block, class range): fp32 [cs][row][bott]
       mbar_wait(dzfull, it & 1);
       tc_fence_after();
       const int cols = bott / 4;
-      const int dpart = (int)part;
+      const int dpart = (int)(e >> 2);
       float* dst = P.dzpart + ((size_t)cs * P.dz_rows + row) * bott + dpart * cols;
       for (int c0 = 0; c0 < cols; c0 += 16) {
         float w[16];
@@ -340,13 +371,13 @@ int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream) {
   if (rc) return rc;
   rc = make_tmap_2d(&P.tmW2, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.bott, a.classes, (uint64_t)a.bott * 2, 64, kCT);
   if (rc) return rc;
-  {  // dlogits, 64x64-blocked [row/64][class/64][64][64]; store box = one warp's 32 rows x 32 classes
+  {  // dlogits, 64x64-blocked [row/64][class/64][64][64]; store box = one warp's 32 rows x 64 classes
     const uint64_t nrb = (a.rows + 63) / 64, ncb = a.classes / 64;
     const uint64_t dims[4] = {64, 64, ncb, nrb};
     const uint64_t strides[3] = {128, 8192, ncb * 8192};
     const uint32_t box[4] = {(uint32_t)kWarpCls, 32, 1, 1};
     rc = make_tmap_4d(&P.tmP, a.dlogits, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dims, strides, box,
-                      CU_TENSOR_MAP_SWIZZLE_NONE);
+                      CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
   }
   P.trace = g_trace;
