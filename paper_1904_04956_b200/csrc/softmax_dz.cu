@@ -11,21 +11,20 @@
 //   MMA1 (pair, M=256 N=128 K=bott): logits of both row blocks into one of two
 //     TMEM buffers; B split by classes (CTA r stages classes r*64.. of the tile,
 //     K-major [64 classes x bott]).
-//   epilogue (16 warps per CTA, 32 rows x 32 classes each): dlogits =
-//     (softmax - onehot) * scale in fp32 -> bf16, written back into the first
-//     16 columns of the warp's TMEM slice, TMA-stored from a 2 KB smem box to
-//     the 64x64-blocked global dlogits (read by the dW_o GEMM), bias-gradient
-//     column sums of the warp's rows.  One mbarrier arrive per warp hands the
-//     slice to MMA2.
-//   MMA2 (pair, M=256 N=bott K=128, A = dlogits from TMEM): dZ of both row
-//     blocks accumulated in TMEM over the class range; B split by bott (CTA r
-//     stages [128 classes x bott/2] MN-major).
-// MMA1 runs one tile ahead of MMA2.  The two B views of a tile live in
-// separate 2-stage rings: the MMA1 view is freed as soon as MMA1 completes,
-// the MMA2 view is loaded while the epilogue runs.  Pair MMAs keep the tensor
-// pipe at full rate (measured: M256 N128 K16 in 64 cycles, vs 110 cycles for a
-// single-CTA M128 N<=128 instruction: tools/micro/mma_rate.cu).  The class
-// ranges of a row block are reduced afterwards (op_splitk_bf16, fixed order).
+//   epilogue: two groups of 8 warps per CTA take alternate tiles (group =
+//     TMEM buffer); a warp owns 32 rows x 64 classes: dlogits = (softmax -
+//     onehot) * scale in fp32 -> bf16 into its 4 KB SW128 smem box, bias-gradient
+//     column sums of its rows.  The buffer is released to MMA1 as soon as the
+//     logits are read; the box is TMA-stored to the 64x64-blocked global
+//     dlogits (read by the dW_o GEMM) and read in place by MMA2.
+//   MMA2 (pair, M=256 N=bott K=128): dZ of both row blocks accumulated in TMEM
+//     over the class range; A = the group's boxes (4 quadrant boxes stacked =
+//     a [128 rows x 64 classes] K-major SW128 block per half), B split by bott
+//     (CTA r stages [128 classes x bott/2] MN-major, one stage, own producer warp).
+// MMA2 trails MMA1 by two tiles.  Pair MMAs run at full tensor rate (measured:
+// M256 N128 K16 in 64 cycles, vs 110 cycles for a single-CTA M128 N<=128
+// instruction: tools/micro/mma_rate.cu).  The class ranges of a row block are
+// reduced afterwards (op_splitk_bf16, fixed order).
 #include "ds_internal.h"
 #include "ds_ptx.cuh"
 #include "softmax_dz.h"
@@ -65,9 +64,10 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
   uint64_t* w2full = w1empty + 2;  // leader
   uint64_t* w2empty = w2full + 1;  // every CTA
   uint64_t* tfull = w2empty + 1;   // [2] every CTA: logits ready
-  uint64_t* tempty = tfull + 2;    // [2] leader: MMA2 read the dlogits written back into the buffer
-  uint64_t* pfull = tempty + 2;    // [2] leader: the 2 x 8 epilogue warps owning the tile wrote their slices
-  uint64_t* dzfull = pfull + 2;    // every CTA: dZ accumulator complete
+  uint64_t* tempty = tfull + 2;    // [2] leader: the 2 x 8 epilogue warps of the buffer read their logits
+  uint64_t* pfull = tempty + 2;    // [2] leader: ... and wrote their dlogits boxes (MMA2's A operand)
+  uint64_t* bfree = pfull + 2;     // [2] every CTA: MMA2 done reading the group's boxes
+  uint64_t* dzfull = bfree + 2;    // every CTA: dZ accumulator complete
   uint64_t* dzempty = dzfull + 1;  // leader: both CTAs drained their dZ accumulators
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dzempty + 1);
 
@@ -87,8 +87,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
       mbar_init(&w1full[i], 1);
       mbar_init(&w1empty[i], 1);
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 1);
-      mbar_init(&pfull[i], kEpiWarps);  // 8 warps per CTA x 2 CTAs
+      mbar_init(&tempty[i], kEpiWarps);  // 8 warps per CTA x 2 CTAs
+      mbar_init(&pfull[i], kEpiWarps);
+      mbar_init(&bfree[i], 1);
     }
     mbar_init(w2full, 1);
     mbar_init(w2empty, 1);
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
     if (leader && elect_one()) {
       const uint32_t id1 = idesc_bf16_f32(2 * kRows, kCT, 0, 0);
       const uint32_t id2 = idesc_bf16_f32(2 * kRows, bott, 0, 1);
-      const uint32_t zb = smem_u32(sZ), w1b = smem_u32(sW1), w2b = smem_u32(sW2);
+      const uint32_t zb = smem_u32(sZ), w1b = smem_u32(sW1), w2b = smem_u32(sW2), cb = smem_u32(sC);
       int g = 0, it = 0;
       auto mma2 = [&](int gp, bool first) {  // dZ += dlogits(gp) W_o(gp), dlogits from TMEM
         const int s = gp & 1;
@@ -161,12 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
         if (tr && gp < 80) tr[gp * 4 + 1] = globaltimer();
 #pragma unroll
         for (int kk = 0; kk < kCT / 16; ++kk) {
-          // classes kk*16.. : written as slice kk/2 (32 classes) into its first columns (kk&1)*8..
-          const uint32_t at = tmem + s * kCT + (kk >> 1) * kPartCls + (kk & 1) * 8;
+          // A = the group's dlogits boxes: per 64-class half, 4 quadrant boxes of [32 rows x 128 B]
+          // stacked = a [128 rows x 64 classes] K-major SW128 block
+          const uint64_t ad = smem_desc_sw128(cb + s * 8 * kCB + (kk >> 2) * 4 * kCB + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = smem_desc_sw128(w2b + kk * 2048, 16384, 1024);
-          mma_bf16_ts_pair(acc2, at, bd, id2, (!first || kk) ? 1u : 0u);
+          mma_bf16_ss_pair(acc2, ad, bd, id2, (!first || kk) ? 1u : 0u);
         }
-        mma_commit_pair_mc(&tempty[s], 0x1);
+        mma_commit_pair_mc(&bfree[s], 0x3);
         mma_commit_pair_mc(w2empty, 0x3);
       };
       for (int item = pair; item < items; item += npairs, ++it) {
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
         for (int ct = ct0; ct < ct1; ++ct, ++g) {
           const int s = g & 1;
           mbar_wait(&w1full[s], (g >> 1) & 1);
-          mbar_wait(&tempty[s], ((g >> 1) & 1) ^ 1);  // MMA2 of tile g-2 read its dlogits
+          mbar_wait_acq_cluster(&tempty[s], ((g >> 1) & 1) ^ 1);  // the epilogue of tile g-2 read its logits
           tc_fence_after();
           if (tr && g < 80) tr[g * 4 + 0] = globaltimer();
 #pragma unroll 1
@@ -191,9 +193,11 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
           mma_commit_pair_mc(&tfull[s], 0x3);
           mma_commit_pair_mc(&w1empty[s], 0x3);
           if (ct == ct1 - 1) mma_commit_pair_mc(zempty, 0x3);
-          if (g > g0) mma2(g - 1, g - 1 == g0);
+          // MMA2 trails MMA1 by two tiles: the issuer never blocks on a tile's epilogue
+          // before the next tile's logits are queued
+          if (g - 2 >= g0) mma2(g - 2, g - 2 == g0);
         }
-        mma2(g - 1, g - 1 == g0);
+        for (int gp = max(g0, g - 2); gp < g; ++gp) mma2(gp, gp == g0);
         mma_commit_pair_mc(dzfull, 0x3);
       }
     }
@@ -208,6 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
     const float* __restrict__ bias = P.bias;
     uint8_t* const myC = sC + e * kCB;
     const uint32_t pfull_c = mapa_shared(smem_u32(pfull), 0);
+    const uint32_t tempty_c = mapa_shared(smem_u32(tempty), 0);
+    int own = 0;  // own tiles processed (box reuse parity)
     const uint32_t dzempty_c = mapa_shared(smem_u32(dzempty), 0);
     int g = 0, it = 0;
     for (int item = pair; item < items; item += npairs, ++it) {
@@ -236,6 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
         tc_fence_after();
         if (tr && g < 80 && (e & 7) == 0 && lane == 0) tr[g * 4 + 2] = globaltimer();
         if (lane == 0) bulk_wait_read0();  // this warp's previous box store has read the box
+        if (own > 0) mbar_wait(&bfree[s], (own - 1) & 1);  // ... and MMA2 of the previous own tile
+        ++own;
         __syncwarp();
         float cs0 = 0.f, cs1 = 0.f;
 #pragma unroll 1
@@ -246,6 +254,16 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
           const uint32_t tcol = tq + s * kCT + half * kWarpCls + k * kPartCls;
           tmem_ld32(tcol, v);
           tmem_ld_wait();
+          if (k == 1) {  // logits of the tile read: the buffer is free for MMA1 of tile g + 2
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (leader)
+                mbar_arrive(&tempty[s]);
+              else
+                mbar_arrive_remote(tempty_c + s * 8);
+            }
+          }
 #pragma unroll
           for (int i = 0; i < kPartCls; ++i)
             v[i] = ex2_fast(fmaf(v[i] + __shfl_sync(0xffffffffu, bsrc, i), kLog2e, -l2));
@@ -262,10 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
             __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
             u[i] = *reinterpret_cast<uint32_t*>(&h);
           }
-          // dlogits back into the first 16 columns of the chunk's TMEM slice (MMA2 operand)
-          tmem_st16(tcol, u);
-          tmem_st_wait();  // u is rewritten by the next chunk
-          // and into the box (row = lane, 128-byte rows, 128-byte swizzle)
+          // dlogits into the box (row = lane, 128-byte rows, 128-byte swizzle): TMA-stored to the
+          // blocked global dlogits and read in place by MMA2 as its A operand
           const uint32_t d = smem_u32(myC) + lane * 128;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -277,7 +293,6 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
             if (k) cs1 = csum; else cs0 = csum;
           }
         }
-        tc_fence_before();
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
