@@ -325,7 +325,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.tgt = h->tgt;
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
-    TRY(op_ce_combine(h->stats, 4 * p.tiles_n, h->Nmax, h->tgt, N, h->lse, h->colpart, loss, flag, s));
+    TRY(op_ce_combine(h->stats, gemm_stats_parts() * p.tiles_n, h->Nmax, h->tgt, N, h->lse, h->colpart, loss, flag, s));
     nl += 4;  // gather, ce stats gemm, combine (2 kernels)
   }
   if (!grad) {

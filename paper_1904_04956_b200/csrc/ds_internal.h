@@ -121,6 +121,7 @@ void gemm_set_trace(unsigned long long* buf, int launch);
 int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const void* B, long long ldb, int b_mn,
                  int M, int N, int K);
 int gemm_launch(GemmBatch* batch, cudaStream_t stream);
+int gemm_stats_parts();  // EPI_CE_STATS partial statistics per column tile
 // Attach the TMA store map for a bf16 output (call after setting out/ldo/n_valid/m_valid).
 int gemm_bf16_output(GemmProblem* p);
 // 64x64-blocked bf16 matrices (rows x cols, see GemmProblem::a_blk): element

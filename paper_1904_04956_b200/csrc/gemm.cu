@@ -47,6 +47,7 @@ constexpr int kEpiWarp0 = 4;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kStageC = 32 * 32 * 2;  // per-epilogue-warp bf16 staging box (32 rows x 32 cols, SW64)
 constexpr int kEpiWarps = 16;
+constexpr int kEpiGroups = 1;  // epilogue warp groups taking alternate tiles (1 or 2; 2 measured slower)
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + kEpiWarps * kStageC + 256;
 
 // trace record: [cta][tile < kTrTiles][kTrFields] (globaltimer ns / clock64 cycles)
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * kEpiWarps);  // every epilogue warp of both CTAs drained it
+      mbar_init(&tempty[a], 2 * kEpiWarps / kEpiGroups);  // the accumulator's epilogue warps of both CTAs
     }
     fence_barrier_init();
   }
@@ -283,13 +284,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     // ---------------- epilogue ----------------
     const uint32_t e = warp - kEpiWarp0;
     const uint32_t q = e & 3;     // TMEM lane quadrant (== warp % 4)
-    const uint32_t part = e >> 2; // column quarter of the 256-wide tile
-    constexpr int kCols = BN / 4; // 64 columns per thread
+    // kEpiGroups groups of warps take alternate tiles (group = accumulator), so one group's TMEM
+    // reads and exponentials overlap the other's stores instead of every warp hitting the same
+    // phase at once
+    constexpr int kParts = 4 / kEpiGroups;         // column parts of the 256-wide tile
+    constexpr int kCols = BN / kParts;             // columns per thread
+    const uint32_t part = (e >> 2) % kParts;
+    const int grp = (int)(e >> 2) / kParts;
     constexpr float kLog2e = 1.4426950408889634f;
     const uint32_t tempty_c = mapa_shared(smem_u32(tempty), 0);
     int it = 0;
     const int ntl = pair_tile_count(batch, pair, npairs);
     for (int ti = 0; ti < ntl; ++ti, ++it) {
+      if ((it & 1) % kEpiGroups != grp) continue;  // kEpiGroups == 2: accumulator it & 1 is group grp's
       TileCoord tc = locate(batch, pair_tile(batch, pair, npairs, ti));
       const GemmProblem& P = batch.p[tc.prob];
       const int rt = tc.tm * 2 + (int)crank;  // 128-row tile of this CTA
@@ -313,10 +320,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       }
       // the warp's 64 bias values, lane i holding columns n0+i and n0+32+i (broadcast by
       // shuffles below): the loads' latency hides behind the accumulator wait
-      float bias_lo = 0.f, bias_hi = 0.f;
-      if (bias && epi != EPI_CE_GRAD) {
-        if (n0 + (int)lane < n_valid) bias_lo = __ldg(bias + n0 + lane);
-        if (n0 + 32 + (int)lane < n_valid) bias_hi = __ldg(bias + n0 + 32 + lane);
+      float bias_r[kCols / 32];
+#pragma unroll
+      for (int j = 0; j < kCols / 32; ++j) {
+        bias_r[j] = 0.f;
+        if (bias && epi != EPI_CE_GRAD && n0 + 32 * j + (int)lane < n_valid) bias_r[j] = __ldg(bias + n0 + 32 * j + lane);
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const int nb = n0 + c;
           // logits in the log2 domain: one FFMA with the log2(e)-scaled bias
           float cm = -INFINITY;
-          const float bsrc = c == 0 ? bias_lo : bias_hi;
+          const float bsrc = bias_r[c >> 5];
           if (full_cols) {
             float m8[8];
 #pragma unroll
@@ -382,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
         if (row_ok) {
           // stats in natural-log units: max, sum exp(x - max)
-          P.stats[(size_t)(tc.tn * 4 + part) * P.stats_ld + row] = make_float2(mx / kLog2e, se);
+          P.stats[(size_t)(tc.tn * kParts + part) * P.stats_ld + row] = make_float2(mx / kLog2e, se);
           if (have_t) P.tgt[row] = tg / kLog2e;
         }
       } else if (epi == EPI_CE_GRAD) {
@@ -434,7 +442,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const int nb = n0 + c;
           if (nb >= n_valid) continue;
           if (bias) {
-            const float bsrc = c == 0 ? bias_lo : bias_hi;
+            float bsrc = bias_r[0];
+#pragma unroll
+            for (int j = 1; j < kCols / 32; ++j)
+              if (c == 32 * j) bsrc = bias_r[j];  // selects: no dynamic register indexing
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xffffffffu, bsrc, i);
           }
@@ -498,6 +509,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 }
 
 }  // namespace
+
+int gemm_stats_parts() { return 4 / kEpiGroups; }
 
 int gemm_problem(GemmProblem* p, const void* A, long long lda, int a_mn, const void* B, long long ldb, int b_mn,
                  int M, int N, int K) {

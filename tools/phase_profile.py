@@ -32,8 +32,8 @@ names = {0: "gemm", 1: "lstm_fwd", 2: "lstm_bwd", 3: "other"}
 # algorithmic GFLOP of the GEMM segments in issue order (paper model, N = 21 B)
 N = 21 * B
 G2, H, LO, BT, C, D0 = 4096, 512, 1024, 256, 32000, 260
-gf = [2 * N * G2 * D0] + [2 * N * G2 * LO] * 5 + [2 * N * BT * LO, 2 * N * C * BT, 4 * N * C * BT, 2 * N * C * BT,
-                                                  4 * N * BT * LO]
+gf = [2 * N * G2 * D0] + [2 * N * G2 * LO] * 5 + [2 * N * BT * LO, 2 * N * C * BT, 4 * N * C * BT,
+                                                  2 * N * C * BT + 4 * N * BT * LO]  # dW_o + dW_b + dY: one launch
 gf += [2 * N * G2 * LO * 2 + 2 * 2 * N * 4 * H * H] * 5 + [2 * N * G2 * D0 + 2 * 2 * N * 4 * H * H]
 gi = 0
 tot = 0.0
