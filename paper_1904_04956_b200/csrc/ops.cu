@@ -104,6 +104,38 @@ __global__ void rowsum_kernel(const float* __restrict__ part, int nrows, int nco
 
 // split-K finish: out(bf16)[m][n] = sum_s part[s][m][n] in split order
 __global__ void splitk_bf16_kernel(const float* __restrict__ part, int S, int64_t n, __nv_bfloat16* __restrict__ out) {
+  if ((n & 3) == 0) {  // 16-byte loads, all S partials of a vector in flight at once
+    const int64_t n4 = n >> 2;
+    const float4* p4 = reinterpret_cast<const float4*>(part);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+      float4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < S) v[k] = __ldg(p4 + (int64_t)k * n4 + i);
+      float4 a = v[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k)
+        if (k < S) {
+          a.x += v[k].x;
+          a.y += v[k].y;
+          a.z += v[k].z;
+          a.w += v[k].w;
+        }
+      for (int k = 8; k < S; ++k) {  // beyond 8 splits (not used by the step)
+        const float4 b = __ldg(p4 + (int64_t)k * n4 + i);
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+      }
+      __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&lo);
+      w.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out)[i] = w;
+    }
+    return;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float s = part[i];
     for (int k = 1; k < S; ++k) s += part[(int64_t)k * n + i];
@@ -132,15 +164,15 @@ __global__ void ce_rows_kernel(const float2* __restrict__ stats, int ntiles, int
   const int m = blockIdx.x * kCeRows + lane;
   float mx = -INFINITY, s = 0.f;
   if (m < M) {
-    for (int j0 = g; j0 < ntiles; j0 += 4 * kCeGroups) {  // online combine, four loads in flight
-      float2 st[4];
+    for (int j0 = g; j0 < ntiles; j0 += 8 * kCeGroups) {  // online combine, eight loads in flight
+      float2 st[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int j = j0 + u * kCeGroups;
         st[u] = j < ntiles ? stats[j * ld + m] : make_float2(-INFINITY, 0.f);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         if (!(st[u].y > 0.f)) continue;  // fully masked column block / past the end
         if (st[u].x > mx) {
           s = s * __expf(mx - st[u].x) + st[u].y;
