@@ -205,24 +205,27 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_pair(tmem_slot, 128);
-  if (threadIdx.x == 0) s_base = ld_relaxed_gpu(flags + (pr >> 2) * 8 + (pr & 3) * 2 + (int)rank);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t base = s_base;  // flag value at launch start (same for every CTA of the group)
   // programmatic launch: the W_hh slice (operand snapshot, not written by the predecessor) is
-  // fetched before waiting for the predecessor grid; everything else after
-  if (warp != 0) griddep_wait();
+  // fetched before waiting for the predecessor grid; everything else after.  The launch's flag
+  // base is read after the wait: a previous launch on the same flags may still be publishing.
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&P.tmA);
+    tma_prefetch_desc(&P.tmW);
+    mbar_arrive_expect_tx(wbar, kWB);
+    const int wrow = dir * 4 * kH + pr * 256 + (int)rank * 128;
+    for (int kb = 0; kb < kH / 64; ++kb) tma_load_2d(sW + kb * 16384, &P.tmW, wbar, kb * 64, wrow);
+  }
+  griddep_wait();
+  if (threadIdx.x == 0) s_base = ld_relaxed_gpu(flags + (pr >> 2) * 8 + (pr & 3) * 2 + (int)rank);
+  __syncthreads();
+  const uint32_t base = s_base;  // flag value at launch start (same for every CTA of the group)
 
   if (warp == 0) {
     if (elect_one()) {
-      tma_prefetch_desc(&P.tmA);
-      tma_prefetch_desc(&P.tmW);
-      mbar_arrive_expect_tx(wbar, kWB);
-      const int wrow = dir * 4 * kH + pr * 256 + (int)rank * 128;
-      for (int kb = 0; kb < kH / 64; ++kb) tma_load_2d(sW + kb * 16384, &P.tmW, wbar, kb * 64, wrow);
-      griddep_wait();
       const uint32_t full_c = mapa_shared(smem_u32(full), 0);
       FlagSeg seg[2];
 #pragma unroll
@@ -480,7 +483,6 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   const int brow0 = P.b0 + btile * 128;
   const int my_chunk = ug * kKS + ks;
   __shared__ uint32_t s_base;
-  if (threadIdx.x == 0) s_base = ld_relaxed_gpu(bwd_flag(flags, my_chunk));
 
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < kStagesB; ++i) {
@@ -501,17 +503,20 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
   cluster_sync_all();  // peers' barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) {  // programmatic launch: W_hh slice first, flag base after the wait (see forward)
+    tma_prefetch_desc(&P.tmA);
+    tma_prefetch_desc(&P.tmW);
+    mbar_arrive_expect_tx(wbar, kWBytesB);
+    for (int j = 0; j < kChunks; ++j)  // W_hh rows (K) ks*512 + 64j.., units (N) ug*64..: MN-major boxes
+      tma_load_2d(sW + j * 8192, &P.tmW, wbar, ug * kGU, dir * 4 * kH + ks * kKSlice + j * 64);
+  }
+  griddep_wait();
+  if (threadIdx.x == 0) s_base = ld_relaxed_gpu(bwd_flag(flags, my_chunk));
+  __syncthreads();
   const uint32_t base = s_base;  // flag value at launch start (same for every chunk of the group)
-  if (warp != 0) griddep_wait();  // programmatic launch (see the forward kernel)
 
   if (warp == 0) {
     if (elect_one()) {
-      tma_prefetch_desc(&P.tmA);
-      tma_prefetch_desc(&P.tmW);
-      mbar_arrive_expect_tx(wbar, kWBytesB);
-      for (int j = 0; j < kChunks; ++j)  // W_hh rows (K) ks*512 + 64j.., units (N) ug*64..: MN-major boxes
-        tma_load_2d(sW + j * 8192, &P.tmW, wbar, ug * kGU, dir * 4 * kH + ks * kKSlice + j * 64);
-      griddep_wait();
       int stage = 0;
       uint32_t phase = 0;
       FlagSeg seg;
