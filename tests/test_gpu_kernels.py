@@ -141,3 +141,36 @@ def test_lstm_recurrent_fwd_bwd(B, T):
     err = (dg.float() - ref).abs().max().item()
     scale = ref.abs().max().item()
     assert err <= 2e-2 * scale, f"dG err {err} scale {scale}"
+
+
+@pytest.mark.timeout(300)
+def test_lstm_back_to_back_launches_reuse_flags():
+    """The recurrent kernels' step flags count up across launches (no reset): a
+    second, third, ... launch on the same counters, issued back to back under
+    programmatic dependent launch, must neither hang nor change the result."""
+    lib = _lib.load()
+    H, B, T = 512, 256, 5
+    N = T * B
+    g = torch.Generator(device=DEV).manual_seed(7)
+    G = (torch.randn(N, 8 * H, device=DEV, generator=g) * 0.5).bfloat16()
+    W = (torch.randn(8 * H, H, device=DEV, generator=g) * 0.05).bfloat16()
+    dY = torch.randn(N, 2 * H, device=DEV, generator=g).bfloat16()
+    counters = torch.zeros(16384, device=DEV, dtype=torch.int32)
+    outs = []
+    for _ in range(3):
+        gates = G.clone()
+        cstate = torch.zeros(N, 2 * H, device=DEV)
+        yfull = torch.zeros((T + 2) * B, 2 * H, device=DEV, dtype=torch.bfloat16)
+        dg = torch.zeros(N, 8 * H, device=DEV, dtype=torch.bfloat16)
+        s = _lib.stream_ptr()
+        for _ in range(2):  # two forward launches, then two backward launches, nothing in between
+            _lib.check(lib.ds_debug_lstm_fwd(B, T, gates.data_ptr(), cstate.data_ptr(), yfull.data_ptr(), W.data_ptr(),
+                                             counters.data_ptr(), None, s), "lstm_fwd")
+        for _ in range(2):
+            _lib.check(lib.ds_debug_lstm_bwd(B, T, gates.data_ptr(), cstate.data_ptr(), W.data_ptr(), dY.data_ptr(),
+                                             dg.data_ptr(), counters.data_ptr(), None, s), "lstm_bwd")
+        torch.cuda.synchronize()
+        outs.append((yfull.clone(), cstate.clone(), dg.clone()))
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert torch.equal(a, b)
