@@ -311,7 +311,26 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     nl += 1;
   }
-  {
+  if (fused_ce_dz(h)) {  // soft-max statistics on CTA pairs (softmax_dz.cu): (max, sum) per row and class range
+    const int S = fused_dz_splits(h, N);
+    CeStatsArgs ca;
+    ca.z = h->z;
+    ca.w = h->snap + L.off_wo;
+    ca.bias_log2 = bias_o + C;  // pre-scaled by log2(e)
+    ca.labels = h->lab;
+    ca.stats = h->stats;
+    ca.stats_ld = h->Nmax;
+    ca.tgt = h->tgt;
+    ca.rows = N;
+    ca.classes = C;
+    ca.bott = bott;
+    ca.splits = S;
+    MARK(PH_GEMM);
+    TRY(ce_stats_launch(ca, s));
+    MARK(PH_OTHER);
+    TRY(op_ce_combine(h->stats, S, h->Nmax, h->tgt, N, h->lse, h->colpart, loss, flag, s));
+    nl += 4;  // gather, statistics kernel, combine (2 kernels)
+  } else {
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
     gb.nprob = 1;

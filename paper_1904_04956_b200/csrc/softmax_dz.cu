@@ -350,6 +350,216 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
   if (warp == 2) tmem_dealloc_pair(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// Soft-max statistics (loss pass) on the same CTA-pair skeleton: MMA1 only
+// (pair M256 N128 K=bott into two TMEM buffers, W_o MMA1 view through a
+// 4-stage ring), two epilogue groups on alternate tiles keeping a running
+// (max, sum 2^(x - max)) per row in registers; the buffer is released as soon
+// as its logits are read.  The four partials of a row (2 groups x 2 class
+// halves) are merged through shared memory once per item.
+namespace stp {
+constexpr int kWStages = 4;
+constexpr int kAcc = 4;  // TMEM logits buffers = epilogue groups
+constexpr size_t kSmem = 1024 + kZB + kWStages * kW1B + 4 * kRows * 8 + 256;
+}  // namespace stp
+
+__global__ void __launch_bounds__(kThreads, 1) ce_stats_kernel(const __grid_constant__ CeStatsParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sZ = sm;
+  uint8_t* sW1 = sZ + kZB;  // [kWStages]
+  float2* sPart = reinterpret_cast<float2*>(sW1 + stp::kWStages * kW1B);  // [4 partials][128 rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sPart + 4 * kRows);
+  uint64_t* zfull = bars;
+  uint64_t* zempty = zfull + 1;
+  uint64_t* w1full = zempty + 1;              // [kWStages] leader
+  uint64_t* w1empty = w1full + stp::kWStages;  // [kWStages] every CTA
+  uint64_t* tfull = w1empty + stp::kWStages;   // [kAcc] every CTA
+  uint64_t* tempty = tfull + stp::kAcc;        // [kAcc] leader: the buffer's 2 x 4 epilogue warps read it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + stp::kAcc);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int bott = P.bott, nkb = bott / 64;
+  const int items = P.n_rbp * P.n_cs;
+  if (warp == 1 && lane == 0) {
+    mbar_init(zfull, 1);
+    mbar_init(zempty, 1);
+    for (int i = 0; i < stp::kWStages; ++i) {
+      mbar_init(&w1full[i], 1);
+      mbar_init(&w1empty[i], 1);
+    }
+    for (int i = 0; i < stp::kAcc; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, stp::kAcc * kCT);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // Z comes from the preceding bottleneck GEMM
+  griddep_launch();
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&P.tmZ);
+      tma_prefetch_desc(&P.tmW1);
+      const uint32_t zfull_c = mapa_shared(smem_u32(zfull), 0);
+      const uint32_t w1full_c = mapa_shared(smem_u32(w1full), 0);
+      int g = 0, it = 0;
+      for (int item = pair; item < items; item += npairs, ++it) {
+        const int rbp = item % P.n_rbp, cs = item / P.n_rbp;
+        const int ct0 = cs * P.ct_per, ct1 = min(P.n_ct, ct0 + P.ct_per);
+        mbar_wait(zempty, (it & 1) ^ 1);
+        if (leader) mbar_arrive_expect_tx(zfull, 2 * kRows * bott * 2);
+        for (int kb = 0; kb < nkb; ++kb)
+          tma_load_2d_pair(sZ + kb * 16384, &P.tmZ, zfull_c, kb * 64, (2 * rbp + (int)rank) * kRows);
+        for (int ct = ct0; ct < ct1; ++ct, ++g) {
+          const int st = g % stp::kWStages;
+          mbar_wait(&w1empty[st], ((g / stp::kWStages) & 1) ^ 1);
+          if (leader) mbar_arrive_expect_tx(&w1full[st], 2 * (kCT / 2) * bott * 2);
+          for (int kb = 0; kb < nkb; ++kb)
+            tma_load_2d_pair(sW1 + st * kW1B + kb * 8192, &P.tmW1, w1full_c + st * 8, kb * 64,
+                             ct * kCT + (int)rank * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && elect_one()) {
+      const uint32_t id1 = idesc_bf16_f32(2 * kRows, kCT, 0, 0);
+      const uint32_t zb = smem_u32(sZ), w1b = smem_u32(sW1);
+      int g = 0, it = 0;
+      for (int item = pair; item < items; item += npairs, ++it) {
+        const int cs = item / P.n_rbp;
+        const int ct0 = cs * P.ct_per, ct1 = min(P.n_ct, ct0 + P.ct_per);
+        mbar_wait(zfull, it & 1);
+        tc_fence_after();
+        for (int ct = ct0; ct < ct1; ++ct, ++g) {
+          const int st = g % stp::kWStages, s = g % stp::kAcc;
+          mbar_wait(&w1full[st], (g / stp::kWStages) & 1);
+          mbar_wait_acq_cluster(&tempty[s], ((g / stp::kAcc) & 1) ^ 1);  // epilogue read tile g-kAcc's logits
+          tc_fence_after();
+#pragma unroll 1
+          for (int kk = 0; kk < bott / 16; ++kk) {
+            const uint64_t ad = smem_desc_sw128(zb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+            const uint64_t bd = smem_desc_sw128(w1b + st * kW1B + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
+            mma_bf16_ss_pair(tmem + s * kCT, ad, bd, id1, kk ? 1u : 0u);
+          }
+          mma_commit_pair_mc(&tfull[s], 0x3);
+          mma_commit_pair_mc(&w1empty[st], 0x3);
+          if (ct == ct1 - 1) mma_commit_pair_mc(zempty, 0x3);
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // four groups of 4 warps (one per TMEM lane quadrant) take every fourth tile, one TMEM
+    // buffer each: the groups run offset by one MMA, so TMEM reads and exponentials overlap
+    const uint32_t e = warp - kEpiWarp0;
+    const uint32_t q = e & 3;
+    const int grp = (int)(e >> 2);
+    const uint32_t tq = tmem + ((q * 32) << 16);
+    const uint32_t tempty_c = mapa_shared(smem_u32(tempty), 0);
+    const int rloc = (int)(q * 32 + lane);
+    int g = 0;
+    for (int item = pair; item < items; item += npairs) {
+      const int rbp = item % P.n_rbp, cs = item / P.n_rbp;
+      const int rb = 2 * rbp + (int)rank;
+      const int ct0 = cs * P.ct_per, ct1 = min(P.n_ct, ct0 + P.ct_per);
+      const int row = rb * kRows + rloc;
+      const bool row_ok = row < P.m_valid;
+      const int lbl = row_ok ? P.labels[row] : -1;
+      float mx = -INFINITY, se = 0.f, tg = 0.f;
+      bool have_t = false;
+      int c = ct0 + (((grp - g) % stp::kAcc + stp::kAcc) % stp::kAcc);
+      g += c - ct0;
+      for (; c < ct1; c += stp::kAcc, g += stp::kAcc) {
+        const int s = g % stp::kAcc;
+        const int nb = c * kCT;
+        float b4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b4[j] = __ldg(P.bias_log2 + nb + j * kPartCls + lane);
+        mbar_wait(&tfull[s], (g / stp::kAcc) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+          const int nk = nb + k * kPartCls;
+          float bsrc = b4[0];
+#pragma unroll
+          for (int j = 1; j < 4; ++j)
+            if (k == j) bsrc = b4[j];
+          float v[kPartCls];
+          tmem_ld32(tq + s * kCT + k * kPartCls, v);
+          tmem_ld_wait();
+          if (k == 3) {  // logits of the tile read: buffer free for MMA1 of tile g + kAcc
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (leader)
+                mbar_arrive(&tempty[s]);
+              else
+                mbar_arrive_remote(tempty_c + s * 8);
+            }
+          }
+          // logits in the log2 domain: one FFMA with the log2(e)-scaled bias
+          float m8[8];
+#pragma unroll
+          for (int i = 0; i < kPartCls; ++i) v[i] = fmaf(v[i], kLog2e, __shfl_sync(0xffffffffu, bsrc, i));
+#pragma unroll
+          for (int i = 0; i < 8; ++i) m8[i] = fmaxf(fmaxf(v[4 * i], v[4 * i + 1]), fmaxf(v[4 * i + 2], v[4 * i + 3]));
+          const float cm = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+          if (lbl >= nk && lbl < nk + kPartCls) {
+#pragma unroll
+            for (int i = 0; i < kPartCls; ++i)
+              if (lbl == nk + i) tg = v[i];
+            have_t = true;
+          }
+          const float nm = fmaxf(mx, cm);
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+          for (int i = 0; i < kPartCls; i += 4) {
+            s0 += ex2_fast(v[i] - nm);
+            s1 += ex2_fast(v[i + 1] - nm);
+            s2 += ex2_fast(v[i + 2] - nm);
+            s3 += ex2_fast(v[i + 3] - nm);
+          }
+          se = se * ex2_fast(mx - nm) + ((s0 + s1) + (s2 + s3));
+          mx = nm;
+        }
+      }
+      g -= c - ct1;
+      if (have_t && row_ok) P.tgt[row] = tg / kLog2e;
+      // merge the row's four partials (one per group); natural-log units on output
+      sPart[grp * kRows + rloc] = make_float2(mx, se);
+      named_bar_sync(1, kEpiWarps * 32);
+      if (grp == 0 && row_ok) {
+        float M = sPart[rloc].x;
+#pragma unroll
+        for (int k = 1; k < 4; ++k) M = fmaxf(M, sPart[k * kRows + rloc].x);
+        float S = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 pk = sPart[k * kRows + rloc];
+          if (pk.y > 0.f) S += pk.y * ex2_fast(pk.x - M);
+        }
+        P.stats[(size_t)cs * P.stats_ld + row] = make_float2(M / kLog2e, S);
+      }
+      named_bar_sync(1, kEpiWarps * 32);  // sPart reused by the next item
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair(tmem, stp::kAcc * kCT);
+}
+
 }  // namespace
 
 bool ce_grad_dz_supported(int classes, int bott) {
@@ -429,6 +639,54 @@ int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = use_pdl() ? 2 : 1;
   DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, ce_grad_dz_kernel, P));
+  return DS_OK;
+}
+
+int ce_stats_launch(const CeStatsArgs& a, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    DS_CUDA_TRY(cudaFuncSetAttribute(ce_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stp::kSmem));
+    attr_set = true;
+  }
+  if (!ce_grad_dz_supported(a.classes, a.bott)) return fail_arg("soft-max statistics: unsupported shape");
+  CeStatsParams P;
+  memset(&P, 0, sizeof(P));
+  int rc = make_tmap_2d(&P.tmZ, a.z, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.bott, a.rows, (uint64_t)a.bott * 2, 64, kRows);
+  if (rc) return rc;
+  rc = make_tmap_2d(&P.tmW1, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.bott, a.classes, (uint64_t)a.bott * 2, 64,
+                    kCT / 2);
+  if (rc) return rc;
+  P.bias_log2 = a.bias_log2;
+  P.labels = a.labels;
+  P.stats = a.stats;
+  P.stats_ld = a.stats_ld;
+  P.tgt = a.tgt;
+  P.bott = a.bott;
+  P.classes = a.classes;
+  P.m_valid = a.rows;
+  P.n_rbp = (a.rows + 2 * kRows - 1) / (2 * kRows);
+  P.n_ct = a.classes / kCT;
+  P.n_cs = a.splits;
+  P.ct_per = (P.n_ct + a.splits - 1) / a.splits;
+  if ((a.splits - 1) * P.ct_per >= P.n_ct) return fail_arg("soft-max statistics: empty class range");
+  const int items = P.n_rbp * P.n_cs;
+  const int max_pairs = num_sms() / 2;
+  const int pairs = items < max_pairs ? items : max_pairs;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = stp::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = use_pdl() ? 2 : 1;
+  DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, ce_stats_kernel, P));
   return DS_OK;
 }
 

@@ -37,6 +37,32 @@ struct CeGradDzArgs {
   int rows, classes, bott, splits;
 };
 
+// Soft-max statistics of the logits Z W_o^T + b_o on CTA pairs (the loss pass):
+// per row and class range (max, sum exp(x - max)) in natural-log units, and the
+// target logit of every labelled row; same work split as the gradient kernel,
+// combined across class ranges by op_ce_combine.
+struct CeStatsArgs {
+  const __nv_bfloat16* z;
+  const __nv_bfloat16* w;
+  const float* bias_log2;  // b_o * log2(e)
+  const int* labels;
+  float2* stats;           // [splits][stats_ld]
+  int64_t stats_ld;
+  float* tgt;              // [rows]
+  int rows, classes, bott, splits;
+};
+struct CeStatsParams {
+  CUtensorMap tmZ, tmW1;
+  const float* bias_log2;
+  const int* labels;
+  float2* stats;
+  int64_t stats_ld;
+  float* tgt;
+  int bott, classes, m_valid;
+  int n_rbp, n_ct, n_cs, ct_per;
+};
+int ce_stats_launch(const CeStatsArgs& a, cudaStream_t stream);
+
 bool ce_grad_dz_supported(int classes, int bott);
 int ce_grad_dz_splits(int rows, int classes, int max_splits);  // class ranges per row block (none empty)
 int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream);
