@@ -352,11 +352,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
 
 // ---------------------------------------------------------------------------
 // Soft-max statistics (loss pass) on the same CTA-pair skeleton: MMA1 only
-// (pair M256 N128 K=bott into two TMEM buffers, W_o MMA1 view through a
-// 4-stage ring), two epilogue groups on alternate tiles keeping a running
-// (max, sum 2^(x - max)) per row in registers; the buffer is released as soon
-// as its logits are read.  The four partials of a row (2 groups x 2 class
-// halves) are merged through shared memory once per item.
+// (pair M256 N128 K=bott into four TMEM buffers, W_o MMA1 view through a
+// 4-stage ring).  Four epilogue groups of 4 warps (one per TMEM lane quadrant)
+// take every fourth tile, offset by one MMA each; a warp keeps a running
+// (max, sum 2^(x - max)) for its 32 rows over 128 classes per own tile and
+// releases the buffer as soon as its logits are read.  The four partials of a
+// row are merged through shared memory once per item.  (Half the exponentials
+// as an FMA-pipe polynomial measured slower: the epilogue is issue-bound.)
 namespace stp {
 constexpr int kWStages = 4;
 constexpr int kAcc = 4;  // TMEM logits buffers = epilogue groups
