@@ -170,3 +170,38 @@ def test_fused_train_step_equals_gradient_then_sgd(layers, B, T, classes):
             assert torch.equal(a, r), (step, name, (a - r).abs().max().item())
     A.close()
     R.close()
+
+
+def test_unfused_output_layer_matches_fused(tmp_path):
+    """DS_NO_FUSED_CE=1 selects the GEMM-epilogue output layer (soft-max
+    statistics / gradient epilogues + separate dW_o, dZ GEMMs) instead of the
+    CTA-pair statistics and soft-max/dZ kernels: both paths agree within the
+    BF16 tolerance (the switch is read once per process: subprocess)."""
+    import os
+    import subprocess
+    import sys
+
+    script = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from oracle import blstm_ref as O
+from paper_1904_04956_b200.blstm import BlstmObjective, DeviceDataset, Learner
+obj = BlstmObjective(layers=1, classes=1280, frames=5)
+spec = O.BlstmSpec(layers=1, input_dim=obj.input_dim, hidden=512, bottleneck=obj.bottleneck, classes=1280, frames=5)
+x, y, _, _ = O.make_dataset(spec, 80, seed=3)
+w = O.initial_weights(spec, 3)
+L = Learner(obj, DeviceDataset(x, y), max_batch=64, theta0=w)
+L.gradient(np.arange(64))
+np.save(sys.argv[1], np.concatenate([[L.mean_loss()], L.grad.double().cpu().numpy()]))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_val in ("0", "1"):
+        out = tmp_path / f"g{env_val}.npy"
+        env = dict(os.environ, DS_NO_FUSED_CE=env_val)
+        subprocess.run([sys.executable, "-c", script, str(out)], check=True, env=env, timeout=300)
+        outs.append(np.load(out))
+    a, b = outs
+    assert abs(a[0] - b[0]) <= 1e-3 * abs(a[0]), (a[0], b[0])
+    ga, gb = a[1:], b[1:]
+    rel = np.linalg.norm(ga - gb) / np.linalg.norm(gb)
+    assert rel <= 1e-2, rel
