@@ -117,6 +117,11 @@ int ds_average(int32_t n, float* const* srcs, float* out, int64_t dim, ds_stream
  * SURVEY §8 a19).  0 restores the per-batch mean. */
 int ds_blstm_set_grad_scale(ds_blstm* h, float frames_total);
 
+/* Read one device float (the step's loss sum) back to the host: 4-byte copy
+ * through the handle's pinned slot on `stream`, then waits for the stream
+ * (everything queued before it included). */
+int ds_blstm_read_loss(ds_blstm* h, const float* loss_sum_dev, ds_stream_t stream, float* out);
+
 /* Phase profiling (bench/tests): when enabled the step is issued without the
  * CUDA graph and CUDA events bracket every phase; ds_blstm_profile_read sums
  * the per-kind milliseconds since the last read into ms_by_kind[0..nkinds):

@@ -39,6 +39,7 @@ SIGNATURES = {
     "ds_average": (_I32, [_I32, _VP, _VP, _I64, _VP]),
     "ds_blstm_set_grad_scale": (_I32, [_VP, _F32]),
     "ds_blstm_set_profile": (_I32, [_VP, _I32]),
+    "ds_blstm_read_loss": (_I32, [_VP, _VP, _VP, ctypes.POINTER(ctypes.c_float)]),
     "ds_blstm_profile_read": (_I32, [_VP, _VP, _I32]),
     "ds_blstm_kernel_count": (_I32, [_VP]),
     "ds_blstm_profile_list": (_I32, [_VP, _VP, _VP, _I32, _VP]),

@@ -299,8 +299,11 @@ class Learner:
             raise ValueError("minibatch index outside the dataset")
 
     def mean_loss(self) -> float:
-        self.stream.synchronize()
-        return float(self.loss_sum.item()) / (self.batch * self.obj.frames)
+        """Mean CE of the last step (waits for self.stream; one pinned 4-byte copy)."""
+        out = ctypes.c_float()
+        _lib.check(_lib.load().ds_blstm_read_loss(self.handle, self.loss_sum.data_ptr(), self.stream.cuda_stream,
+                                                  ctypes.byref(out)), "ds_blstm_read_loss")
+        return float(out.value) / (self.batch * self.obj.frames)
 
     def close(self) -> None:
         if getattr(self, "handle", None):

@@ -51,6 +51,7 @@ struct ds_blstm {
   uint32_t* counters = nullptr;
   float* d_lr = nullptr;  // fused training step: learning rate read by the SGD kernels
   float lr_host = -1.f;   // value last written to d_lr (written again only when it changes)
+  float* loss_pinned = nullptr;  // pinned host slot for ds_blstm_read_loss
   // fused training step: per-layer SGD on a side stream while the next BPTT runs
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork[kMaxLayers + 2] = {}, ev_join[kMaxLayers + 2] = {};
@@ -680,6 +681,7 @@ int ds_blstm_destroy(ds_blstm* h) {
     if (h->ev_rs[k / 2][k % 2]) cudaEventDestroy(h->ev_rs[k / 2][k % 2]);
   if (h->side2) cudaStreamDestroy(h->side2);
   if (h->side) cudaStreamDestroy(h->side);
+  if (h->loss_pinned) cudaFreeHost(h->loss_pinned);
   if (h->arena) cudaFree(h->arena);
   delete h;
   return DS_OK;
@@ -791,6 +793,17 @@ int ds_blstm_set_grad_scale(ds_blstm* h, float frames_total) {
   if (!h) return fail_arg("null handle");
   if (frames_total < 0.f) return fail_arg("frames_total must be >= 0");
   h->grad_frames = frames_total;
+  return DS_OK;
+}
+
+int ds_blstm_read_loss(ds_blstm* h, const float* loss_sum_dev, ds_stream_t stream, float* out) {
+  if (!h || !loss_sum_dev || !out) return fail_arg("null argument");
+  DS_CUDA_TRY(cudaSetDevice(h->device));
+  if (!h->loss_pinned) DS_CUDA_TRY(cudaMallocHost(&h->loss_pinned, sizeof(float)));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DS_CUDA_TRY(cudaMemcpyAsync(h->loss_pinned, loss_sum_dev, sizeof(float), cudaMemcpyDeviceToHost, s));
+  DS_CUDA_TRY(cudaStreamSynchronize(s));
+  *out = *h->loss_pinned;
   return DS_OK;
 }
 
