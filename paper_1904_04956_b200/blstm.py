@@ -158,7 +158,9 @@ class Learner:
         # ring of pinned staging buffers: a batch upload only waits for the
         # copy that used the same slot several uploads ago
         self._ring = [torch.zeros(max_batch, dtype=torch.int64).pin_memory() for _ in range(4)]
-        self._ring_ev = [None] * 4
+        self._ring_ptr = [t.data_ptr() for t in self._ring]
+        self._ring_ev = [torch.cuda.Event() for _ in range(4)]
+        self._ring_used = [False] * 4
         self._ring_i = 0
         self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
         self.batch = 0
@@ -188,22 +190,20 @@ class Learner:
 
     # -- hot path -------------------------------------------------------------
     def _upload_batch(self, batch: np.ndarray) -> int:
-        import torch
-
         B = len(batch)
         if not 1 <= B <= self.max_batch:
             raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
         k = self._ring_i
         self._ring_i = (k + 1) % len(self._ring)
-        if self._ring_ev[k] is not None:
-            self._ring_ev[k].synchronize()  # slot's previous H2D copy has finished
-        host = self._ring[k]
-        host[:B] = torch.from_numpy(np.asarray(batch, dtype=np.int64))
-        with torch.cuda.stream(self.stream):
-            self.idx[:B].copy_(host[:B], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(self.stream)
-        self._ring_ev[k] = ev
+        ev = self._ring_ev[k]
+        if self._ring_used[k]:
+            ev.synchronize()  # the slot's previous H2D copy has finished
+        arr = np.ascontiguousarray(batch, dtype=np.int64)
+        ctypes.memmove(self._ring_ptr[k], arr.ctypes.data, B * 8)  # into pinned memory
+        _lib.check(_lib.load().ds_device_copy(self.idx.data_ptr(), self._ring_ptr[k], B * 8, self.stream.cuda_stream),
+                   "ds_device_copy")
+        ev.record(self.stream)
+        self._ring_used[k] = True
         return B
 
     def gradient(self, batch: np.ndarray) -> None:
