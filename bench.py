@@ -336,15 +336,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     gemm_tfs = gemm_flops / (ph["gemm"] * 1e-3) / 1e12 if ph["gemm"] > 0 else 0.0
     traffic = None  # DRAM bytes of the same GEMM launches of one step, from the committed ncu capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r1e_gemm_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1f_gemm_traffic.json")) as f:
             tj = json.load(f)
         if B == 256 and obj.layers == 6:
             traffic = {"bytes_per_step": tj["gemm_dram_bytes_per_step"], "launches": tj["gemm_launches_per_step"],
-                       "source": "profiles/r1e_gemm_traffic.json (ncu dram__bytes_read+write)"}
+                       "source": "profiles/r1f_gemm_traffic.json (ncu dram__bytes_read+write)"}
     except Exception:
         pass
     roof = {"bound": "tensor",
-            "kernel": "tcgen05 bf16 GEMM-class launches of one step (gemm_kernel + fused soft-max/dZ kernel)",
+            "kernel": "tcgen05 bf16 GEMM-class launches of one step (gemm_kernel + soft-max statistics + soft-max/dZ kernels)",
             "achieved": round(gemm_tfs, 1), "peak": burst, "unit": "TFLOP/s", "frac": round(gemm_tfs / burst, 4),
             "peak_kind": f"{peak_kind} burst bf16", "traffic": traffic,
             "algorithmic_flop_per_step": gemm_flops,

@@ -1,4 +1,4 @@
-"""DRAM traffic of the GEMM-class launches (gemm_kernel + the fused soft-max/dZ
+"""DRAM traffic of the GEMM-class launches (gemm_kernel + the soft-max statistics and soft-max/dZ
 kernel) of one paper-size training step, from an ncu metrics CSV of
 tools/phase_profile.py (4 gradient steps; the last one is used):
 
@@ -26,7 +26,7 @@ for r in data:
 seq = list(launch.values())
 gi = [i for i, s in enumerate(seq) if "gather" in s["name"]]
 step = seq[gi[-1]:]
-gemm = [s for s in step if s["name"] in ("gemm_kernel", "ce_grad_dz_kernel")]
+gemm = [s for s in step if s["name"] in ("gemm_kernel", "ce_grad_dz_kernel", "ce_stats_kernel")]
 dram = lambda s: s.get("dram__bytes_read.sum", 0) + s.get("dram__bytes_write.sum", 0)  # noqa: E731
 print(json.dumps({
     "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum ({sys.argv[1]}), last gradient step of "
