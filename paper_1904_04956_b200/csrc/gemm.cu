@@ -419,17 +419,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               if (lbl == nb + i) v[i] -= 1.f;
           }
           const float sc = row_ok ? scale : 0.f;
+          if (nb + 32 <= n_valid) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= sc;
+            for (int i = 0; i < 32; ++i) v[i] *= sc;
+          } else {  // last column tile: classes >= n_valid carry no probability (and no store)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = nb + i < n_valid ? v[i] * sc : 0.f;
+          }
           if (P.c_tma) {
             store_box_tma(&P.tmC, cstage + e * kStageC, v, nb, rt * BM + q * 32, P.c_blk);
           } else if (row_ok) {
             store_bf16x16(orow + nb, v);
-            store_bf16x16(orow + nb + 16, v + 16);
+            if (nb + 16 < n_valid) store_bf16x16(orow + nb + 16, v + 16);  // n_valid is a multiple of 16
           }
           if (colpart && rt * BM < P.m_valid) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
             const float cs = warp_colsum32(v, lane);
-            colpart[(size_t)(rt * 4 + q) * n_valid + nb + lane] = cs;
+            if (nb + (int)lane < n_valid) colpart[(size_t)(rt * 4 + q) * n_valid + nb + lane] = cs;
           }
         }
       } else if (epi == EPI_BF16) {

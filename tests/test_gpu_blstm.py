@@ -26,7 +26,8 @@ def _spec(obj):
                        classes=obj.classes, frames=obj.frames)
 
 
-@pytest.mark.parametrize("layers,B,T,classes", [(2, 24, 6, 512), (1, 136, 5, 256), (1, 40, 3, 1280), (1, 8, 3, 32000)])
+@pytest.mark.parametrize("layers,B,T,classes", [(2, 24, 6, 512), (1, 136, 5, 256), (1, 40, 3, 1280), (1, 8, 3, 32000),
+                                                  (1, 24, 4, 1008)])  # 1008: not a multiple of 128 -> GEMM-epilogue path
 def test_fwd_bwd_matches_oracle(layers, B, T, classes):
     obj = BlstmObjective(layers=layers, classes=classes, frames=T)
     spec = _spec(obj)
