@@ -206,3 +206,39 @@ np.save(sys.argv[1], np.concatenate([[L.mean_loss()], L.grad.double().cpu().nump
     ga, gb = a[1:], b[1:]
     rel = np.linalg.norm(ga - gb) / np.linalg.norm(gb)
     assert rel <= 1e-2, rel
+
+
+@pytest.mark.parametrize("layers,B,T,classes,bott,din", [
+    (1, 1, 4, 512, 256, 260),     # one sequence: batch tiles of one row
+    (2, 5, 1, 256, 256, 260),     # one frame: the recurrences have a single step (no recurrent term)
+    (1, 17, 3, 384, 64, 40),      # bottleneck 64 (GEMM-epilogue soft-max path), narrow input
+    (1, 300, 2, 128, 128, 260),   # batch > one recurrent launch's 256 rows: two sub-launches
+])
+def test_fwd_bwd_edge_shapes_match_oracle(layers, B, T, classes, bott, din):
+    """Edge shapes of the same path against the float64 oracle (tolerances as above)."""
+    obj = BlstmObjective(layers=layers, classes=classes, frames=T, bottleneck=bott, input_dim=din)
+    spec = O.BlstmSpec(layers=layers, input_dim=din, hidden=512, bottleneck=bott, classes=classes, frames=T)
+    assert spec.param_dim == obj.param_dim
+    x, y, _, _ = O.make_dataset(spec, B + 2, seed=11)
+    w = O.initial_weights(spec, 11)
+    batch = np.arange(B)
+    xb = torch.from_numpy(x).bfloat16().double().numpy()
+    loss_ref, g_ref = O.loss_and_grad(spec, w, xb[batch], y[batch])
+    L = Learner(obj, DeviceDataset(x, y), max_batch=B, theta0=w)
+    L.gradient(batch)
+    L.check_finite()
+    loss = L.mean_loss()
+    g = L.grad.double().cpu().numpy()
+    assert abs(loss - loss_ref) <= 5e-3 * abs(loss_ref), (loss, loss_ref)
+    for k, v in offsets(obj).items():
+        if k == "total":
+            continue
+        o, shape = v
+        n = int(np.prod(shape))
+        a, r = g[o:o + n], g_ref[o:o + n]
+        if np.linalg.norm(r) == 0:
+            continue
+        rel = np.linalg.norm(a - r) / np.linalg.norm(r)
+        cos = float(a @ r / max(np.linalg.norm(a) * np.linalg.norm(r), 1e-30))
+        assert rel <= 2.5e-2 and cos >= 0.9995, (k, rel, cos)
+    L.close()
