@@ -152,8 +152,8 @@ def test_two_process_ipc_ssgd_and_mix_bit_exact():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("strategy", ["ssgd", "adpsgd"])
-def test_bench_multiprocess_p2p_same_device(strategy):
+@pytest.mark.parametrize("strategy,nproc", [("ssgd", 2), ("adpsgd", 2), ("hadpsgd", 4)])
+def test_bench_multiprocess_p2p_same_device(strategy, nproc):
     """bench.py's one-process-per-GPU path (torchrun, P2P transport) runs end
     to end with both ranks on cuda:0 and prints one JSON line (functional
     check: ranks time-slice one GPU, the value is not a scaling number)."""
@@ -165,14 +165,14 @@ def test_bench_multiprocess_p2p_same_device(strategy):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2", "--steps",
-           "3", "--warmup", "3", "--no-cpu", "--n-seq", "1024", "--batch", "64", "--same-device", "--strategy",
-           strategy]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus",
+           str(nproc), "--steps", "3", "--warmup", "3", "--no-cpu", "--n-seq", "1024", "--batch", "64",
+           "--same-device", "--strategy", strategy, "--groups", "2"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     rec = json.loads(lines[0])
-    assert rec["n_gpus"] == 2 and rec["config"]["strategy"] == strategy and rec["config"]["transport"] == "p2p"
+    assert rec["n_gpus"] == nproc and rec["config"]["strategy"] == strategy and rec["config"]["transport"] == "p2p"
     assert rec["value"] > 0 and rec["e2e"]["value"] > 0
