@@ -292,11 +292,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     launches_per_step = L.kernel_count() + sync_launches
 
     # ---- end to end through the public Learner API (host indices in, loss out)
-    e2e_steps = max(3, min(args.steps, 20))
+    e2e_steps = max(3, min(args.steps, 60))
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
+    pending = None  # every step's loss is read back; the host issues step k+1 before reading step k's
     for k in range(e2e_steps):
         j = k % q
         lr = learning_rate(sched, 1, j, q)
@@ -308,7 +309,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         else:
             L.gradient(mine[j])
             sync(args.warmup + args.steps + k, lr)
-        _ = L.mean_loss()
+        fut = L.loss_async()
+        if pending is not None:
+            _ = pending()
+        pending = fut
+    _ = pending()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist is not None:

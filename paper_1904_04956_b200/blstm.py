@@ -162,6 +162,11 @@ class Learner:
         self._ring_ev = [torch.cuda.Event() for _ in range(4)]
         self._ring_used = [False] * 4
         self._ring_i = 0
+        self._loss_slots = torch.zeros(4, dtype=torch.float32).pin_memory()
+        self._loss_ptr = self._loss_slots.data_ptr()
+        self._loss_ev = [torch.cuda.Event() for _ in range(4)]
+        self._loss_used = [False] * 4
+        self._loss_i = 0
         self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
         self.batch = 0
         if theta0 is not None:
@@ -297,6 +302,29 @@ class Learner:
         if int(self.flag.item()) & 2:
             self.flag.zero_()
             raise ValueError("minibatch index outside the dataset")
+
+    def loss_async(self):
+        """Queue the read-back of the last step's loss on the learner stream and
+        return a callable that waits for that copy and gives the mean CE: the
+        host can issue the next step before the loss arrives (pinned 4-slot ring;
+        call each callable before issuing four more)."""
+        k = self._loss_i
+        self._loss_i = (k + 1) % len(self._loss_ev)
+        ev = self._loss_ev[k]
+        if self._loss_used[k]:
+            ev.synchronize()  # the slot's previous copy was consumed
+        ptr = self._loss_ptr + 4 * k
+        _lib.check(_lib.load().ds_device_copy(ptr, self.loss_sum.data_ptr(), 4, self.stream.cuda_stream),
+                   "ds_device_copy")
+        ev.record(self.stream)
+        self._loss_used[k] = True
+        slots, denom = self._loss_slots, float(self.batch * self.obj.frames)
+
+        def result() -> float:
+            ev.synchronize()
+            return float(slots[k]) / denom
+
+        return result
 
     def mean_loss(self) -> float:
         """Mean CE of the last step (waits for self.stream; one pinned 4-byte copy)."""

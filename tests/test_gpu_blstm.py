@@ -242,3 +242,25 @@ def test_fwd_bwd_edge_shapes_match_oracle(layers, B, T, classes, bott, din):
         cos = float(a @ r / max(np.linalg.norm(a) * np.linalg.norm(r), 1e-30))
         assert rel <= 2.5e-2 and cos >= 0.9995, (k, rel, cos)
     L.close()
+
+
+def test_loss_async_matches_mean_loss():
+    """Learner.loss_async (pinned ring, read after the next step is issued) gives
+    each step's own mean loss."""
+    obj = BlstmObjective(layers=1, classes=256, frames=3)
+    spec = _spec(obj)
+    x, y, _, _ = O.make_dataset(spec, 64, seed=2)
+    L = Learner(obj, DeviceDataset(x, y), max_batch=32, theta0=O.initial_weights(spec, 2))
+    futs, refs = [], []
+    for k in range(6):
+        L.train_step(np.arange(k, k + 32) % 64, 0.05)
+        futs.append(L.loss_async())
+        if k >= 1:
+            refs.append(futs[k - 1]())
+    refs.append(futs[-1]())
+    R = Learner(obj, DeviceDataset(x, y), max_batch=32, theta0=O.initial_weights(spec, 2))
+    for k in range(6):
+        R.train_step(np.arange(k, k + 32) % 64, 0.05)
+        assert R.mean_loss() == refs[k], k
+    L.close()
+    R.close()
