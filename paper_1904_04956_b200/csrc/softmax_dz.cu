@@ -241,10 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
         mbar_wait(&tfull[s], (g >> 1) & 1);
         tc_fence_after();
         if (tr && g < 80 && (e & 7) == 0 && lane == 0) tr[g * 4 + 2] = globaltimer();
-        if (lane == 0) bulk_wait_read0();  // this warp's previous box store has read the box
-        if (own > 0) mbar_wait(&bfree[s], (own - 1) & 1);  // ... and MMA2 of the previous own tile
+        const bool reuse = own > 0;
+        const uint32_t reuse_phase = (uint32_t)(own - 1) & 1;
         ++own;
-        __syncwarp();
         float cs0 = 0.f, cs1 = 0.f;
 #pragma unroll 1
         for (int k = 0; k < 2; ++k) {  // two 32-class chunks
@@ -282,6 +281,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
           }
           // dlogits into the box (row = lane, 128-byte rows, 128-byte swizzle): TMA-stored to the
           // blocked global dlogits and read in place by MMA2 as its A operand
+          if (k == 0) {  // box free: this warp's previous store has read it and MMA2 of the
+                         // previous own tile is done (waited here, after the first chunk's math)
+            if (lane == 0) bulk_wait_read0();
+            if (reuse) mbar_wait(&bfree[s], reuse_phase);
+            __syncwarp();
+          }
           const uint32_t d = smem_u32(myC) + lane * 128;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
