@@ -136,6 +136,8 @@ bool fused_ce_dz(const ds_blstm* h) {
   }
   return !off && blocked_dlogits(h) && ce_grad_dz_supported(h->L.classes, h->L.bottleneck);
 }
+// the soft-max combine's last-block ticket: a word of the zeroed slack after the recurrent flags
+unsigned* ce_ticket(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax); }
 int fused_dz_splits(const ds_blstm* h, int N) {
   // h->splitk holds kDzPartMax x N x bottleneck floats
   return ce_grad_dz_splits(N, h->L.classes, kDzPartMax);
@@ -329,8 +331,8 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     TRY(ce_stats_launch(ca, s));
     MARK(PH_OTHER);
-    TRY(op_ce_combine(h->stats, S, h->Nmax, h->tgt, N, h->lse, h->colpart, loss, flag, s));
-    nl += 4;  // gather, statistics kernel, combine (2 kernels)
+    TRY(op_ce_combine(h->stats, S, h->Nmax, h->tgt, N, h->lse, h->colpart, ce_ticket(h), loss, flag, s));
+    nl += 3;  // gather, statistics kernel, combine
   } else {
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
@@ -345,8 +347,9 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p.tgt = h->tgt;
     TRY(gemm_launch(&gb, s));
     MARK(PH_OTHER);
-    TRY(op_ce_combine(h->stats, gemm_stats_parts() * p.tiles_n, h->Nmax, h->tgt, N, h->lse, h->colpart, loss, flag, s));
-    nl += 4;  // gather, ce stats gemm, combine (2 kernels)
+    TRY(op_ce_combine(h->stats, gemm_stats_parts() * p.tiles_n, h->Nmax, h->tgt, N, h->lse, h->colpart,
+                      ce_ticket(h), loss, flag, s));
+    nl += 3;  // gather, ce stats gemm, combine
   }
   if (!grad) {
     MARK(PH_END);

@@ -158,7 +158,8 @@ __global__ void splitk_f32_kernel(const float* __restrict__ part, int S, int64_t
 constexpr int kCeRows = 32;   // rows per block (lane = row: coalesced stats reads)
 constexpr int kCeGroups = 16;  // tile groups per block (warps)
 __global__ void ce_rows_kernel(const float2* __restrict__ stats, int ntiles, int64_t ld, const float* __restrict__ tgt,
-                               int M, float* __restrict__ lse, float* __restrict__ part) {
+                               int M, float* __restrict__ lse, float* __restrict__ part, unsigned* __restrict__ ticket,
+                               float* __restrict__ loss_sum, int* __restrict__ flag) {
   __shared__ float smx[kCeGroups][kCeRows], ssum[kCeGroups][kCeRows];
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = blockIdx.x * kCeRows + lane;
@@ -202,20 +203,29 @@ __global__ void ce_rows_kernel(const float2* __restrict__ stats, int ntiles, int
     for (int off = 16; off >= 1; off >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, off);
     if (lane == 0) part[blockIdx.x] = loss;
   }
-}
-__global__ void ce_sum_kernel(const float* __restrict__ part, int n, float* __restrict__ loss_sum, int* __restrict__ flag) {
-  __shared__ float red[1024];
+  // the last block to finish sums the block partials in index order (deterministic) and
+  // re-arms the ticket: no separate reduction launch
+  __shared__ bool last;
+  __shared__ float red[kCeGroups * 32];
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   float acc = 0.f;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) acc += __ldcg(part + i);
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     *loss_sum = red[0];
     if (flag && !isfinite(red[0])) atomicOr(flag, 1);
+    *ticket = 0u;
   }
 }
 
@@ -519,10 +529,9 @@ int op_rowsum(const float* part, int nrows, int ncols, float* out, cudaStream_t 
 }
 
 int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt, int M, float* lse, float* scratch,
-                  float* loss_sum, int* flag, cudaStream_t s) {
+                  unsigned* ticket, float* loss_sum, int* flag, cudaStream_t s) {
   const int nblk = (M + kCeRows - 1) / kCeRows;
-  ce_rows_kernel<<<nblk, kCeGroups * 32, 0, s>>>(stats, ntiles, ld, tgt, M, lse, scratch);
-  ce_sum_kernel<<<1, 1024, 0, s>>>(scratch, nblk, loss_sum, flag);
+  ce_rows_kernel<<<nblk, kCeGroups * 32, 0, s>>>(stats, ntiles, ld, tgt, M, lse, scratch, ticket, loss_sum, flag);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }

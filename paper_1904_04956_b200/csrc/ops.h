@@ -17,7 +17,7 @@ int op_splitk_bf16(const float* part, int S, int64_t n, __nv_bfloat16* out, cuda
 int op_splitk_f32(const float* part, int S, int64_t n, float* out, cudaStream_t s);
 int op_rowsum(const float* part, int nrows, int ncols, float* out, cudaStream_t s);
 int op_ce_combine(const float2* stats, int ntiles, int64_t ld, const float* tgt, int M, float* lse, float* scratch,
-                  float* loss_sum, int* flag, cudaStream_t s);
+                  unsigned* ticket, float* loss_sum, int* flag, cudaStream_t s);  // ticket: zeroed word, re-armed
 int op_sgd(float* theta, float* v, const float* g, float lr, float mu, int64_t n, __nv_bfloat16* snap, int* flag,
            cudaStream_t s);
 // lr from device memory; max_blocks > 0: at most that many 1024-thread blocks
