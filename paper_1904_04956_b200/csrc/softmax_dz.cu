@@ -244,25 +244,14 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
         const bool reuse = own > 0;
         const uint32_t reuse_phase = (uint32_t)(own - 1) & 1;
         ++own;
-        float cs0 = 0.f, cs1 = 0.f;
+        const uint32_t tcol0 = tq + s * kCT + half * kWarpCls;
+        float v[kPartCls];
+        tmem_ld32(tcol0, v);
+        tmem_ld_wait();
 #pragma unroll 1
         for (int k = 0; k < 2; ++k) {  // two 32-class chunks
           const int nk = nb + k * kPartCls;
           const float bsrc = k ? bs1 : bs0;
-          float v[kPartCls];
-          const uint32_t tcol = tq + s * kCT + half * kWarpCls + k * kPartCls;
-          tmem_ld32(tcol, v);
-          tmem_ld_wait();
-          if (k == 1) {  // logits of the tile read: the buffer is free for MMA1 of tile g + 2
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if (leader)
-                mbar_arrive(&tempty[s]);
-              else
-                mbar_arrive_remote(tempty_c + s * 8);
-            }
-          }
 #pragma unroll
           for (int i = 0; i < kPartCls; ++i)
             v[i] = ex2_fast(fmaf(v[i] + __shfl_sync(0xffffffffu, bsrc, i), kLog2e, -l2));
@@ -274,10 +263,21 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
           uint32_t u[kPartCls / 2];
 #pragma unroll
           for (int i = 0; i < kPartCls / 2; ++i) {
-            v[2 * i] *= sc;
-            v[2 * i + 1] *= sc;
-            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i] * sc, v[2 * i + 1] * sc);
             u[i] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          if (k == 0) {  // second chunk's logits into v (dead now): the TMEM buffer is then free
+                         // for MMA1 of tile g + 2 before this chunk's box wait and stores
+            tmem_ld32(tcol0 + kPartCls, v);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (leader)
+                mbar_arrive(&tempty[s]);
+              else
+                mbar_arrive_remote(tempty_c + s * 8);
+            }
           }
           // dlogits into the box (row = lane, 128-byte rows, 128-byte swizzle): TMA-stored to the
           // blocked global dlogits and read in place by MMA2 as its A operand
@@ -293,10 +293,6 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
             const uint32_t chunk = (uint32_t)(k * 4 + j);
             st_shared_v4(d + ((chunk ^ (lane & 7)) << 4), u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
           }
-          if (P.colpart) {  // bias gradient: column sums of this warp's 32 rows (fp32, pre-rounding)
-            const float csum = warp_colsum32(v, lane);
-            if (k) cs1 = csum; else cs0 = csum;
-          }
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -309,9 +305,35 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
             mbar_arrive_remote(pfull_c + s * 8);
         }
         if (P.colpart && rb * kRows < P.m_valid) {
-          float* cp = P.colpart + (size_t)(rb * 4 + q) * P.classes + nb + lane;
-          cp[0] = cs0;
-          cp[kPartCls] = cs1;
+          // bias gradient: column sums of the box as stored (bf16 dlogits, the values dW_o and
+          // dZ use), read back while the TMA store and MMA2 read it too: lane = 16-byte column
+          // chunk (8 classes) x row quarter, eight conflict-free 128-byte row reads per quarter
+          // warp, then two shuffle steps over the quarters
+          const uint32_t c8 = lane & 7, rq = lane >> 3, bx = smem_u32(myC);
+          float cs[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) cs[j] = 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t r = rq + 4 * i;
+            const uint4 w = ld_shared_v4(bx + r * 128 + ((c8 ^ (r & 7)) << 4));
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              cs[2 * j] += __uint_as_float(ww[j] << 16);
+              cs[2 * j + 1] += __uint_as_float(ww[j] & 0xffff0000u);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 8);
+            cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 16);
+          }
+          if (lane < 8) {
+            float4* cp = reinterpret_cast<float4*>(P.colpart + (size_t)(rb * 4 + q) * P.classes + nb + 8 * c8);
+            cp[0] = make_float4(cs[0], cs[1], cs[2], cs[3]);
+            cp[1] = make_float4(cs[4], cs[5], cs[6], cs[7]);
+          }
         }
         if (c + 2 < ct1) {  // next own tile's bias (after the proxy fence, which waits for loads in flight)
           bn0 = __ldg(bias + nb + 2 * kCT + lane);
