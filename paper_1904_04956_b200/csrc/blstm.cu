@@ -280,6 +280,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
     gb.nprob = 1;
+    gb.b_early = l > 0;  // B = W_ih snapshot; the predecessor (LSTM l-1) writes only A
     GemmProblem& p = gb.p[0];
     if (l == 0)
       TRY(gemm_problem(&p, h->x0, kInPad, 0, h->wih0pad, kInPad, 0, N, kGates2, kInPad));
@@ -302,6 +303,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
     gb.nprob = 1;
+    gb.b_early = 1;  // B = W_b snapshot
     GemmProblem& p = gb.p[0];
     TRY(gemm_problem(&p, Y(Lh - 1), kLayerOut, 0, h->snap + L.off_wb, kLayerOut, 0, N, bott, kLayerOut));
     p.epi = EPI_BF16;
@@ -503,6 +505,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     nl += 1 + (B - 1) / (128 * lstm_max_tiles());
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
+    gb.b_early = 1;  // B = X / Y / W_ih (forward pass, snapshot); the predecessor (BPTT l) writes only A = dG
     GemmProblem& p0 = gb.p[0];  // dW_ih = dG^T X
     if (l == 0) {
       TRY(gemm_problem(&p0, h->dg, kGates2, 1, h->x0, kInPad, 1, kGates2, kInPad, N));

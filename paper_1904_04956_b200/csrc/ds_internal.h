@@ -107,6 +107,8 @@ struct GemmBatch {
   int nprob;
   int total_tiles;
   int sched;                            // 1: use order/pstart
+  int b_early;                          // B of every problem is not written by the predecessor kernel:
+                                        // prefetch it before griddep_wait (PDL)
   uint16_t pstart[kMaxPairs + 1];       // pair p runs order[pstart[p] .. pstart[p+1])
   uint16_t order[kMaxSched];
   // debug: per-CTA per-tile timeline (tools/gemm_trace.py), null in production

@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // prologue done: wait for the predecessor's outputs, then let the next kernel start its own
-  griddep_wait();
+  // (b_early: the producer first prefetches the B operand of its first tile —
+  // never written by the predecessor kernel — and waits afterwards)
+  if (!(batch.b_early && warp == 0)) griddep_wait();
   griddep_launch();
 
 
@@ -184,6 +186,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       int stage = 0;
       uint32_t phase = 0;
       const int ntl = pair_tile_count(batch, pair, npairs);
+      int pre = 0;  // stages of tile 0 whose B load (and expect_tx) was issued before griddep_wait
+      if (batch.b_early) {
+        if (ntl > 0) {
+          TileCoord tc = locate(batch, pair_tile(batch, pair, npairs, 0));
+          const GemmProblem& P = batch.p[tc.prob];
+          const int n0 = tc.tn * BN + (int)crank * kBHalf;
+          int kb0, kb1;
+          kb_range(P, tc.ks, kb0, kb1);
+          pre = min(kStages, kb1 - kb0);
+          for (int s = 0; s < pre; ++s) {
+            uint8_t* sB = smem + s * kStageBytes + kABytes;
+            if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+            const uint32_t bar = full_c + s * 8;
+            const int k0 = (kb0 + s) * BK;
+            if (!P.b_mn) {
+              tma_load_2d_pair(sB, &P.tmB, bar, k0, n0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < kBHalf / 64; ++j) tma_load_2d_pair(sB + j * 8192, &P.tmB, bar, n0 + 64 * j, k0);
+            }
+          }
+        }
+        griddep_wait();
+      }
       for (int ti = 0; ti < ntl; ++ti) {
         TileCoord tc = locate(batch, pair_tile(batch, pair, npairs, ti));
         const GemmProblem& P = batch.p[tc.prob];
@@ -192,12 +218,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         kb_range(P, tc.ks, kb0, kb1);
         long long pst = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
+          const bool early = ti == 0 && kb - kb0 < pre;
           const long long c0 = trace ? clock64() : 0;
           mbar_wait(&empty[stage], phase ^ 1);  // the pair MMA that read this stage (both CTAs) is done
           if (trace) pst += clock64() - c0;
           uint8_t* sA = smem + stage * kStageBytes;
           uint8_t* sB = sA + kABytes;
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          if (leader && !early) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
           const uint32_t bar = full_c + stage * 8;
           const int k0 = kb * BK;
           if (P.a_blk) {  // 64x64-blocked A: whole 8 KB blocks (box spans 2 row blocks when K-major)
@@ -214,7 +241,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sA + j * 8192, &P.tmA, bar, m0 + 64 * j, k0);
           }
-          if (!P.b_mn) {
+          if (early) {
+          } else if (!P.b_mn) {
             tma_load_2d_pair(sB, &P.tmB, bar, k0, n0);
           } else {
 #pragma unroll
@@ -645,6 +673,8 @@ void gemm_set_trace(unsigned long long* buf, int launch) {
 
 int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   b->trace = nullptr;
+  static const bool no_bearly = getenv("DS_NO_BEARLY") != nullptr;  // A/B switch
+  if (no_bearly || !use_pdl()) b->b_early = 0;
   if (g_trace_countdown >= 0 && g_trace_countdown-- == 0) b->trace = g_trace;
   static bool attr_set = false;
   if (!attr_set) {
