@@ -225,6 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
       const int lbl = row_ok ? P.labels[row] : -1;
       const float l2 = row_ok ? P.lse[row] * kLog2e : 0.f;
       const float sc = (row_ok && lbl >= 0) ? P.scale : 0.f;
+      // (p - onehot) * sc with p * sc = 2^(x log2e - lse log2e + log2 sc) * 2^(b log2e): one FFMA2
+      // per class pair before the exponentials, one FMUL2 by the classes' exp(bias) after
+      const float nl2 = sc > 0.f ? log2f(sc) - l2 : -INFINITY;
       const int r0 = rb * kRows + (int)q * 32;  // first row of this warp's dlogits box
       // own tiles: g % 2 == grp; lane i holds the bias of classes nb+i and nb+32+i, one own tile ahead
       int c = ct0 + (((grp - g) % 2 + 2) % 2);
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
       for (; c < ct1; c += 2, g += 2) {
         const int s = g & 1;
         const int nb = c * kCT + (int)half * kWarpCls;
-        const float bs0 = bn0, bs1 = bn1;
+        const float eb0 = ex2_fast(bn0 * kLog2e), eb1 = ex2_fast(bn1 * kLog2e);
         mbar_wait(&tfull[s], (g >> 1) & 1);
         tc_fence_after();
         if (tr && g < 80 && (e & 7) == 0 && lane == 0) tr[g * 4 + 2] = globaltimer();
@@ -251,19 +254,23 @@ __global__ void __launch_bounds__(kThreads, 1) ce_grad_dz_kernel(const __grid_co
 #pragma unroll 1
         for (int k = 0; k < 2; ++k) {  // two 32-class chunks
           const int nk = nb + k * kPartCls;
-          const float bsrc = k ? bs1 : bs0;
+          const float ebsrc = k ? eb1 : eb0;
 #pragma unroll
-          for (int i = 0; i < kPartCls; ++i)
-            v[i] = ex2_fast(fmaf(v[i] + __shfl_sync(0xffffffffu, bsrc, i), kLog2e, -l2));
+          for (int i = 0; i < kPartCls; i += 2) {
+            float a0, a1;
+            ffma2(a0, a1, v[i], v[i + 1], kLog2e, kLog2e, nl2, nl2);
+            fmul2(v[i], v[i + 1], ex2_fast(a0), ex2_fast(a1), __shfl_sync(0xffffffffu, ebsrc, i),
+                  __shfl_sync(0xffffffffu, ebsrc, i + 1));
+          }
           if (lbl >= nk && lbl < nk + kPartCls) {
 #pragma unroll
             for (int i = 0; i < kPartCls; ++i)
-              if (lbl == nk + i) v[i] -= 1.f;
+              if (lbl == nk + i) v[i] -= sc;
           }
           uint32_t u[kPartCls / 2];
 #pragma unroll
           for (int i = 0; i < kPartCls / 2; ++i) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i] * sc, v[2 * i + 1] * sc);
+            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
             u[i] = *reinterpret_cast<uint32_t*>(&h);
           }
           if (k == 0) {  // second chunk's logits into v (dead now): the TMEM buffer is then free
