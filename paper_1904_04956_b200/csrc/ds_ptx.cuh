@@ -445,6 +445,17 @@ DS_DEV void fmul2(float& x, float& y, float a0, float a1, float b0, float b1) {
       : "=f"(x), "=f"(y)
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
+DS_DEV void fadd2(float& x, float& y, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(x), "=f"(y)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+DS_DEV float fmax3(float a, float b, float c) {  // FMNMX3
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 DS_DEV float sigmoid_fast(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
 DS_DEV void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];

@@ -541,28 +541,31 @@ __global__ void __launch_bounds__(kThreads, 1) ce_stats_kernel(const __grid_cons
                 mbar_arrive_remote(tempty_c + s * 8);
             }
           }
-          // logits in the log2 domain: one FFMA with the log2(e)-scaled bias
-          float m8[8];
+          // logits in the log2 domain: one FFMA2 per class pair with the log2(e)-scaled bias
 #pragma unroll
-          for (int i = 0; i < kPartCls; ++i) v[i] = fmaf(v[i], kLog2e, __shfl_sync(0xffffffffu, bsrc, i));
+          for (int i = 0; i < kPartCls; i += 2)
+            ffma2(v[i], v[i + 1], v[i], v[i + 1], kLog2e, kLog2e, __shfl_sync(0xffffffffu, bsrc, i),
+                  __shfl_sync(0xffffffffu, bsrc, i + 1));
+          float m3[11];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) m8[i] = fmaxf(fmaxf(v[4 * i], v[4 * i + 1]), fmaxf(v[4 * i + 2], v[4 * i + 3]));
-          const float cm = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+          for (int i = 0; i < 10; ++i) m3[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+          m3[10] = fmax3(v[30], v[31], mx);
+          const float nm = fmax3(fmax3(m3[0], m3[1], m3[2]), fmax3(m3[3], m3[4], m3[5]),
+                                 fmax3(fmax3(m3[6], m3[7], m3[8]), m3[9], m3[10]));
           if (lbl >= nk && lbl < nk + kPartCls) {
 #pragma unroll
             for (int i = 0; i < kPartCls; ++i)
               if (lbl == nk + i) tg = v[i];
             have_t = true;
           }
-          const float nm = fmaxf(mx, cm);
           float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
           for (int i = 0; i < kPartCls; i += 4) {
-            s0 += ex2_fast(v[i] - nm);
-            s1 += ex2_fast(v[i + 1] - nm);
-            s2 += ex2_fast(v[i + 2] - nm);
-            s3 += ex2_fast(v[i + 3] - nm);
+            float a0, a1, a2, a3;
+            fadd2(a0, a1, v[i], v[i + 1], -nm, -nm);
+            fadd2(a2, a3, v[i + 2], v[i + 3], -nm, -nm);
+            fadd2(s0, s1, s0, s1, ex2_fast(a0), ex2_fast(a1));
+            fadd2(s2, s3, s2, s3, ex2_fast(a2), ex2_fast(a3));
           }
           se = se * ex2_fast(mx - nm) + ((s0 + s1) + (s2 + s3));
           mx = nm;
