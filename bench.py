@@ -341,11 +341,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     gemm_tfs = gemm_flops / (ph["gemm"] * 1e-3) / 1e12 if ph["gemm"] > 0 else 0.0
     traffic = None  # DRAM bytes of the same GEMM launches of one step, from the committed ncu capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r1h_gemm_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1i_gemm_traffic.json")) as f:
             tj = json.load(f)
         if B == 256 and obj.layers == 6:
             traffic = {"bytes_per_step": tj["gemm_dram_bytes_per_step"], "launches": tj["gemm_launches_per_step"],
-                       "source": "profiles/r1h_gemm_traffic.json (ncu dram__bytes_read+write)"}
+                       "source": "profiles/r1i_gemm_traffic.json (ncu dram__bytes_read+write)"}
     except Exception:
         pass
     roof = {"bound": "tensor",
