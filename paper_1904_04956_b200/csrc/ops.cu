@@ -454,7 +454,8 @@ __global__ void group_reduce_kernel(GroupPtrs p, int world, int rank, int64_t di
         if (p.snap[r]) reinterpret_cast<uint2*>(p.snap[r])[i4] = f4_bf16(w);
       }
     }
-    const int64_t e0 = lo, e1 = min(hi, lo4 * 4), f0 = max(lo, hi4 * 4), f1 = hi;
+    // a chunk with no aligned float4 (lo4 > hi4) is all edge: one scalar range
+    const int64_t e0 = lo, e1 = lo4 > hi4 ? hi : min(hi, lo4 * 4), f0 = lo4 > hi4 ? hi : max(lo, hi4 * 4), f1 = hi;
     for (int64_t t = tid; t < (e1 - e0) + (f1 - f0); t += nth) {
       const int64_t i = t < (e1 - e0) ? e0 + t : f0 + (t - (e1 - e0));
       float s = src[owner][i];

@@ -127,7 +127,8 @@ __global__ void shard_step_kernel(ShardArgs a, int world, int rank, int64_t n, i
       }
     }
     // ragged chunk edges
-    const int64_t e0 = lo, e1 = min(hi, lo4 * 4), f0 = max(lo, hi4 * 4), f1 = hi;
+    // a chunk with no aligned float4 (lo4 > hi4) is all edge: one scalar range
+    const int64_t e0 = lo, e1 = lo4 > hi4 ? hi : min(hi, lo4 * 4), f0 = lo4 > hi4 ? hi : max(lo, hi4 * 4), f1 = hi;
     for (int64_t t = tid; t < (e1 - e0) + (f1 - f0); t += nth) {
       const int64_t i = t < (e1 - e0) ? e0 + t : f0 + (t - (e1 - e0));
       float sum = src[owner][i];
@@ -165,7 +166,7 @@ __global__ void pair_mix_kernel(float* __restrict__ self, float* __restrict__ pe
     }
   }
   // ragged edges (lo not 4-aligned / tail)
-  const int64_t a0 = lo, a1 = min(hi, lo4 * 4), b0 = max(lo, hi4 * 4), b1 = hi;
+  const int64_t a0 = lo, a1 = lo4 > hi4 ? hi : min(hi, lo4 * 4), b0 = lo4 > hi4 ? hi : max(lo, hi4 * 4), b1 = hi;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (a1 - a0) + (b1 - b0);
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = i < (a1 - a0) ? a0 + i : b0 + (i - (a1 - a0));

@@ -143,10 +143,12 @@ def test_mix_kernel_pair_sum_exact():
     assert np.array_equal(A.cpu().numpy() + Bt.cpu().numpy(), (a + b).astype(np.float32))
 
 
-@pytest.mark.parametrize("world,chunks", [(2, None), (3, 7), (4, None), (8, 16)])
-def test_group_reduce_canonical_order(world, chunks):
+@pytest.mark.parametrize("world,chunks,n", [(2, None, 100_003), (3, 7, 100_003), (4, None, 100_003),
+                                            (8, 16, 100_003), (2, 4, 10), (3, 5, 13)])
+def test_group_reduce_canonical_order(world, chunks, n):
+    """n=10 / 4 chunks: the last chunk [9, 10) holds no aligned float4 (its
+    edge ranges used to overlap and apply the step twice)."""
     lib = _lib.load()
-    n = 100_003
     chunks = chunks or world
     rng = np.random.default_rng(world)
     gs = [rng.standard_normal(n).astype(np.float32) * (10.0 ** k) for k in range(world)]
