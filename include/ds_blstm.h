@@ -122,6 +122,21 @@ int ds_blstm_set_grad_scale(ds_blstm* h, float frames_total);
  * (everything queued before it included). */
 int ds_blstm_read_loss(ds_blstm* h, const float* loss_sum_dev, ds_stream_t stream, float* out);
 
+/* Precision mode of the handle's gradient / loss / train-step calls:
+ *   DS_PREC_BF16 (default) — the performance path: bf16 tensor-core operands
+ *     and stored activations, fp32 accumulation, cell state and master weights;
+ *   DS_PREC_FP32 — the parity path for the reference's float64 arithmetic
+ *     (objectives.py:3-5, 236-263): every GEMM on tcgen05 kind::tf32 with the
+ *     3xTF32 split (hi*hi + hi*lo + lo*hi, ~fp32 products), fp32 activations,
+ *     accurate exp/tanh, materialised fp32 logits.  Allocates its own
+ *     workspace (~6 GB at B = 256 paper size) on first selection; the operand
+ *     snapshot becomes the fp32 hi/lo splits (call ds_blstm_cast_snapshot
+ *     after switching). */
+#define DS_PREC_BF16 0
+#define DS_PREC_FP32 1
+int ds_blstm_set_precision(ds_blstm* h, int32_t mode);
+int32_t ds_blstm_get_precision(ds_blstm* h);
+
 /* Phase profiling (bench/tests): when enabled the step is issued without the
  * CUDA graph and CUDA events bracket every phase; ds_blstm_profile_read sums
  * the per-kind milliseconds since the last read into ms_by_kind[0..nkinds):
@@ -207,6 +222,11 @@ int ds_debug_lstm_fwd(int32_t B, int32_t T, void* gates, float* cstate, void* y_
                       uint32_t* counters, uint64_t* trace, ds_stream_t stream);
 int ds_debug_lstm_bwd(int32_t B, int32_t T, const void* gates, const float* cstate, const void* whh, const void* dy,
                       void* dg, uint32_t* counters, uint64_t* trace, ds_stream_t stream);
+
+/* GEMM self-test hook (tests only): C[M,N] (+)= A . B^T, fp32 row-major
+ * operands through the FP32-parity 3xTF32 tcgen05 GEMM. */
+int ds_debug_gemm_tf32x3(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int32_t M,
+                         int32_t N, int32_t K, int32_t accumulate, ds_stream_t stream);
 
 const char* ds_last_error(void);
 

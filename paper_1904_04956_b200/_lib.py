@@ -18,6 +18,8 @@ DS_OK = 0
 DS_ERR_ARG = -1
 DS_ERR_CUDA = -2
 DS_ERR_NONFINITE = -3
+DS_PREC_BF16 = 0
+DS_PREC_FP32 = 1
 
 # Every symbol of include/ds_blstm.h with its ctypes signature.
 _VP = ctypes.c_void_p
@@ -57,6 +59,9 @@ SIGNATURES = {
     "ds_peer_barrier": (_I32, [_I32, _VP, _VP, _I32, _VP, ctypes.c_uint32, _VP, ctypes.c_double, _VP]),
     "ds_shard_step": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _I64, _I32, _F32, _F32, _I32, _F32, _VP]),
     "ds_pair_mix": (_I32, [_VP, _VP, _VP, _VP, _I64, _I32, _VP]),
+    "ds_blstm_set_precision": (_I32, [_VP, _I32]),
+    "ds_blstm_get_precision": (_I32, [_VP]),
+    "ds_debug_gemm_tf32x3": (_I32, [_VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _I32, _VP]),
     "ds_last_error": (ctypes.c_char_p, []),
 }
 

@@ -38,7 +38,8 @@ def _ptr_array(ptrs):
 class GpuBackend:
     elem_bytes = 4
 
-    def __init__(self, objective: BlstmObjective, dataset, device: int = 0, max_batch: int = 256):
+    def __init__(self, objective: BlstmObjective, dataset, device: int = 0, max_batch: int = 256,
+                 precision: str = "bf16"):
         import torch
 
         if not isinstance(objective, BlstmObjective):
@@ -49,6 +50,7 @@ class GpuBackend:
         self.obj = objective
         self.device = device
         self.max_batch = max_batch
+        self.precision = precision
         torch.cuda.set_device(device)
         self.stream = torch.cuda.Stream(device=torch.device("cuda", device))
         self.data = dataset
@@ -62,7 +64,7 @@ class GpuBackend:
     # -- learners -----------------------------------------------------------
     def create(self, w0: np.ndarray, momentum: float) -> Learner:
         L = Learner(self.obj, self.ddata, self.max_batch, device=self.device, theta0=w0, momentum=momentum,
-                    stream=self.stream)
+                    stream=self.stream, precision=self.precision)
         self.learners.append(L)
         return L
 
@@ -134,7 +136,8 @@ class GpuBackend:
         import torch
 
         if self._eval is None:
-            self._eval = Learner(self.obj, self.ddata, self.max_batch, device=self.device, stream=self.stream)
+            self._eval = Learner(self.obj, self.ddata, self.max_batch, device=self.device, stream=self.stream,
+                                 precision=self.precision)
         E = self._eval
         src = w.theta if isinstance(w, Learner) else w
         with torch.cuda.stream(self.stream):

@@ -112,6 +112,13 @@ class DeviceDataset:
         n, T, D = inputs.shape
         if targets.shape != (n, T):
             raise ValueError(f"blstm targets must be [n_seq, frames] = {(n, T)}, got {targets.shape}")
+        targets = np.asarray(targets)
+        if targets.dtype.kind not in "iu":
+            if not np.all(np.isfinite(targets)) or not np.all(targets == np.round(targets)):
+                raise ValueError("blstm targets must be integer class ids")
+        # checked against the objective's class count by Learner (the soft-max
+        # kernels never see an out-of-range label)
+        self.label_range = (int(targets.min()), int(targets.max())) if targets.size else (0, 0)
         self.n_seq, self.frames, self.input_dim = n, T, D
         self.device = device
         dev = torch.device("cuda", device)
@@ -129,11 +136,17 @@ class Learner:
     simulated learners sharing a GPU)."""
 
     def __init__(self, obj: BlstmObjective, data: DeviceDataset, max_batch: int, device: int = 0,
-                 theta0: np.ndarray | None = None, momentum: float = 0.9, stream=None):
+                 theta0: np.ndarray | None = None, momentum: float = 0.9, stream=None, precision: str = "bf16"):
         import torch
 
         if data.frames != obj.frames or data.input_dim != obj.input_dim:
             raise ValueError("dataset shape does not match the objective (frames / input_dim)")
+        lo, hi = data.label_range
+        if lo < 0 or hi >= obj.classes:
+            raise ValueError(f"blstm targets must be class ids in [0, {obj.classes}), got range [{lo}, {hi}]")
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"precision must be 'bf16' (performance) or 'fp32' (parity), got {precision!r}")
+        self.precision = precision
         self.obj = obj
         self.data = data
         self.device = device
@@ -146,6 +159,8 @@ class Learner:
         cfg = obj.cfg(max_batch)
         _lib.check(lib.ds_blstm_create(ctypes.byref(cfg), device, ctypes.byref(h)), "ds_blstm_create")
         self.handle = h
+        if precision == "fp32":
+            _lib.check(lib.ds_blstm_set_precision(h, _lib.DS_PREC_FP32), "ds_blstm_set_precision")
         _lib.check(lib.ds_blstm_set_dataset(h, data.feats.data_ptr(), data.labels.data_ptr(), data.n_seq),
                    "ds_blstm_set_dataset")
         P = obj.param_dim

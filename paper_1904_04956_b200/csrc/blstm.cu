@@ -11,6 +11,7 @@
 #include "layout.h"
 #include "lstm_rec.h"
 #include "ops.h"
+#include "parity.h"
 #include "softmax_dz.h"
 
 using namespace ds;
@@ -88,6 +89,9 @@ struct ds_blstm {
   int launches = 0;  // kernel launches issued by the last step
   float grad_frames = 0.f;  // CE gradient divisor override (0: B*T)
   int pad_B = -1;           // batch size the Y_full zero pads were laid out for
+  // precision mode: 0 = BF16 perf path, 1 = FP32 parity (3xTF32 tcgen05, parity.cu)
+  int prec = 0;
+  ParityWs* par = nullptr;
 };
 
 namespace {
@@ -579,6 +583,15 @@ int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, i
   if (!h->feats) return fail_arg("dataset not bound (ds_blstm_set_dataset)");
   if (!loss) return fail_arg("loss_sum pointer is required");
   DS_CUDA_TRY(cudaSetDevice(h->device));
+  if (h->prec == 1) {  // FP32 parity: plain launch sequence, then the unfused update
+    int rc = parity_step(h->par, h->L, h->T, idx, B, h->feats, h->labels, h->n_seq, h->grad_frames, grad, loss, flag,
+                         s, &h->launches);
+    if (rc || !sg.theta) return rc;
+    rc = op_sgd_lr(sg.theta, sg.vel, grad, h->d_lr, sg.mu, h->L.total, nullptr, flag, 0, s);
+    if (!rc) rc = parity_snapshot(h->par, h->L, sg.theta, s);
+    h->launches += 1 + 4 * h->L.layers + 3;
+    return rc;
+  }
   if (h->pad_B != B) {  // zero rows of Y_full (h_{-1}, h_T): no kernel ever writes them
     for (int l = 0; l < h->L.layers; ++l) {
       DS_CUDA_TRY(cudaMemsetAsync(h->yfull[l], 0, (size_t)B * kLayerOut * 2, s));
@@ -688,6 +701,7 @@ int ds_blstm_destroy(ds_blstm* h) {
   if (h->side2) cudaStreamDestroy(h->side2);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->loss_pinned) cudaFreeHost(h->loss_pinned);
+  parity_destroy(h->par);
   if (h->arena) cudaFree(h->arena);
   delete h;
   return DS_OK;
@@ -707,10 +721,25 @@ int ds_blstm_cast_snapshot(ds_blstm* h, const float* theta, ds_stream_t stream) 
   if (!h || !theta) return fail_arg("null argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   DS_CUDA_TRY(cudaSetDevice(h->device));
+  if (h->prec == 1) return parity_snapshot(h->par, h->L, theta, s);
   int rc = op_cast(theta, h->L.total, h->snap, s);
   if (rc) return rc;
   return op_snapshot_aux(theta, h->L, h->wih0pad, h->bias_snap, s);
 }
+
+int ds_blstm_set_precision(ds_blstm* h, int32_t mode) {
+  if (!h) return fail_arg("null handle");
+  if (mode != DS_PREC_BF16 && mode != DS_PREC_FP32) return fail_arg("precision mode must be 0 (bf16) or 1 (fp32)");
+  DS_CUDA_TRY(cudaSetDevice(h->device));
+  if (mode == DS_PREC_FP32 && !h->par) {
+    int rc = parity_create(&h->par, h->L, h->T, h->Bmax);
+    if (rc) return rc;
+  }
+  h->prec = mode;
+  return DS_OK;
+}
+
+int32_t ds_blstm_get_precision(ds_blstm* h) { return h ? h->prec : -1; }
 
 int ds_blstm_snapshot_aux(ds_blstm* h, const float* theta, ds_stream_t stream) {
   if (!h || !theta) return fail_arg("null argument");
@@ -761,6 +790,10 @@ int ds_sgd_momentum(float* theta, float* v, const float* g, float lr, float mu, 
   if (!(lr > 0.f)) return fail_arg("learning rate must be > 0");
   if (snap_owner && snap_owner->L.total != n) return fail_arg("snapshot owner has a different param_dim");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (snap_owner && snap_owner->prec == 1) {  // FP32 parity snapshot: hi/lo splits of the new theta
+    int rc = op_sgd(theta, v, g, lr, mu, n, nullptr, nonfinite, s);
+    return rc ? rc : parity_snapshot(snap_owner->par, snap_owner->L, theta, s);
+  }
   int rc = op_sgd(theta, v, g, lr, mu, n, snap_owner ? snap_owner->snap : nullptr, nonfinite, s);
   if (rc || !snap_owner) return rc;
   return op_snapshot_aux(theta, snap_owner->L, snap_owner->wih0pad, snap_owner->bias_snap, s);
