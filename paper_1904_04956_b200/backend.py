@@ -77,6 +77,15 @@ class GpuBackend:
             L._gscale = frames_total
         L.gradient(np.asarray(batch))
 
+    def train_step(self, L: Learner, batch, lr: float) -> None:
+        """gradient then sgd_step of one learner (engines/single.py:53-55) as
+        the fused device step: each layer's update runs beside the next BPTT
+        (bit-identical to gradient + sgd_step, tests/test_gpu_blstm.py)."""
+        if getattr(L, "_gscale", 0.0):
+            L.set_grad_scale(0.0)
+            L._gscale = 0.0
+        L.train_step(np.asarray(batch), lr)
+
     def zero_grad(self, L: Learner) -> None:
         import torch
 
@@ -143,14 +152,7 @@ class GpuBackend:
         with torch.cuda.stream(self.stream):
             E.theta.copy_(src)
         E.snapshot()
-        total = 0.0
-        idx = self.heldout
-        for s in range(0, len(idx), self.max_batch):
-            part = idx[s:s + self.max_batch]
-            E.loss(part)
-            self.stream.synchronize()
-            total += float(E.loss_sum.item())
-        return total / (len(idx) * self.obj.frames)
+        return E.heldout_mean(self.heldout)
 
     def weights(self, w) -> np.ndarray:
         src = w.theta if isinstance(w, Learner) else w

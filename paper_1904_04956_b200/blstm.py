@@ -298,6 +298,27 @@ class Learner:
         _lib.check(lib.ds_blstm_loss(self.handle, self.idx.data_ptr(), B, self.loss_sum.data_ptr(),
                                      self.flag.data_ptr(), self.stream.cuda_stream), "ds_blstm_loss")
 
+    def heldout_mean(self, idx: np.ndarray) -> float:
+        """Mean CE over the sequences `idx` (held-out evaluation,
+        objectives.py:286-291), forward only: the per-chunk loss sums are
+        accumulated on the device and read back once."""
+        import torch
+
+        idx = np.asarray(idx)
+        if len(idx) == 0:
+            raise ValueError("empty held-out split")
+        if getattr(self, "_held_acc", None) is None:
+            self._held_acc = torch.zeros(1, dtype=torch.float64, device=self.theta.device)
+        acc = self._held_acc
+        with torch.cuda.stream(self.stream):
+            acc.zero_()
+        for s in range(0, len(idx), self.max_batch):
+            self.loss(idx[s:s + self.max_batch])
+            with torch.cuda.stream(self.stream):
+                acc.add_(self.loss_sum)
+        self.stream.synchronize()
+        return float(acc.item()) / (len(idx) * self.obj.frames)
+
     def sgd_step(self, lr: float) -> None:
         """sgd_step (optim.py:109-121) fused with the operand snapshot (K9+K2)."""
         if lr <= 0:
@@ -317,6 +338,12 @@ class Learner:
         if int(self.flag.item()) & 2:
             self.flag.zero_()
             raise ValueError("minibatch index outside the dataset")
+        if int(self.flag.item()) & 4:
+            self.flag.zero_()
+            raise ValueError("class label outside [0, classes)")
+        if int(self.flag.item()) & 8:
+            self.flag.zero_()
+            raise _lib.DsError("recurrent kernel flag wait timed out (CTAs not co-resident?)")
 
     def loss_async(self):
         """Queue the read-back of the last step's loss on the learner stream and

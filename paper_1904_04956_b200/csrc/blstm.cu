@@ -299,6 +299,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     TRY(gemm_launch(&gb, s));
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], nullptr, nullptr,
                      h->counters};
+    la.err = flag;
     MARK(PH_LSTM_FWD);
     TRY(lstm_forward(la, s));
     nl += 2 + (B - 1) / (128 * lstm_max_tiles());
@@ -504,6 +505,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   for (int l = Lh - 1; l >= 0; --l) {
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], h->dy,
                      h->dg, h->counters, nullptr, h->biaspart};
+    la.err = flag;
     MARK(PH_LSTM_BWD);
     TRY(lstm_backward(la, s));
     nl += 1 + (B - 1) / (128 * lstm_max_tiles());

@@ -60,11 +60,38 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* v) {
   return w;
 }
 
+// Flag words count up forever (never reset, see below), so comparisons are
+// wrap-safe: v has reached target when (int32)(v - target) >= 0.
+__device__ __forceinline__ bool reached(uint32_t v, uint32_t target) { return (int32_t)(v - target) >= 0; }
+
+// Spin guard: a peer CTA that never publishes (a co-residency failure, a
+// killed launch) must not hang the GPU.  After ~2 s of polling the waiter
+// sets bit 8 of the step's error flag (raised by the host as RuntimeError)
+// and gives up; the step's results are then garbage but the stream drains.
+constexpr uint64_t kSpinTimeoutNs = 2000000000ull;
+struct SpinGuard {
+  uint32_t n = 0;
+  uint64_t t0 = 0;
+};
+__device__ __forceinline__ bool spin_expired(SpinGuard& g, int* err) {
+  if ((++g.n & 1023u) != 0) return false;
+  const uint64_t now = globaltimer();
+  if (g.t0 == 0) {
+    g.t0 = now;
+    return false;
+  }
+  if (now - g.t0 < kSpinTimeoutNs) return false;
+  if (err) atomicOr(err, 8);
+  return true;
+}
+
 // spin (relaxed, L1-bypassing) until *flag >= target, then acquire and make
 // the released generic-proxy writes visible to our async-proxy (TMA) reads.
-__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target) {
-  if (ld_relaxed_gpu(flag) < target) {
-    while (ld_relaxed_gpu(flag) < target) {
+__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target, int* err) {
+  if (!reached(ld_relaxed_gpu(flag), target)) {
+    SpinGuard g;
+    while (!reached(ld_relaxed_gpu(flag), target)) {
+      if (spin_expired(g, err)) return;
     }
   }
 }
@@ -92,10 +119,12 @@ __device__ __forceinline__ uint32_t* bwd_flag(uint32_t* base, int c) { return ba
 
 // wait until all four consecutive flags (16-byte aligned) reach `target`,
 // polling them with one acquire vector load per round trip
-__device__ __forceinline__ void wait_flags4(const uint32_t* flags4, uint32_t target) {
+__device__ __forceinline__ void wait_flags4(const uint32_t* flags4, uint32_t target, int* err) {
+  SpinGuard g;
   while (true) {
     const uint4 v = ld_acquire_gpu_v4(flags4);
-    if (min(min(v.x, v.y), min(v.z, v.w)) >= target) break;
+    if (reached(v.x, target) && reached(v.y, target) && reached(v.z, target) && reached(v.w, target)) break;
+    if (spin_expired(g, err)) return;
   }
 }
 // segment cache for an issuer walking the flags of one 32-byte segment
@@ -104,12 +133,13 @@ struct FlagSeg {
 };
 // wait until flags [pos, pos + n) of the segment reach `target` (n = 1 or 4)
 template <int n>
-__device__ __forceinline__ void wait_seg(FlagSeg& c, const uint32_t* seg, int pos, uint32_t target) {
+__device__ __forceinline__ void wait_seg(FlagSeg& c, const uint32_t* seg, int pos, uint32_t target, int* err) {
+  SpinGuard g;
   while (true) {
-    uint32_t m = c.v[pos];
+    bool ok = reached(c.v[pos], target);
 #pragma unroll
-    for (int i = 1; i < n; ++i) m = min(m, c.v[pos + i]);
-    if (m >= target) return;
+    for (int i = 1; i < n; ++i) ok = ok && reached(c.v[pos + i], target);
+    if (ok || spin_expired(g, err)) return;
     ld_acquire_gpu_v8(seg, c.v);
   }
 }
@@ -239,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
           uint64_t* fb = &full[buf * 8 + k];
           if (leader) mbar_arrive_expect_tx(fb, 2 * kChunkB);
           if (s > 0) {  // chunk k of h_{t-1} = both CTAs of pair k (flags 2k, 2k+1)
-            wait_seg<2>(seg[k >> 2], flags + (k >> 2) * 8, (k & 3) * 2, base + (uint32_t)s);
+            wait_seg<2>(seg[k >> 2], flags + (k >> 2) * 8, (k & 3) * 2, base + (uint32_t)s, P.err);
             fence_proxy_async_global();
           }
           tma_load_2d_pair(sB + buf * kBufB + k * kChunkB, &P.tmA, full_c + (uint32_t)(buf * 8 + k) * 8,
@@ -533,20 +563,20 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(const __grid_cons
           mbar_arrive_expect_tx(&full[stage], kTileA);
           if (kMulticastB) {  // the pair alternates chunks; multicast to both
             if ((j & 1) == upair) {
-              wait_flag(bwd_flag(flags, chunk), base + (uint32_t)s);
+              wait_flag(bwd_flag(flags, chunk), base + (uint32_t)s, P.err);
               acquire_for_tma(bwd_flag(flags, chunk), P.variant);
               tma_load_2d_mc(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow,
                              pair_mask);
             }
           } else {
             if (P.variant & 256) {  // experiment: relaxed polls, one acquire load once satisfied
-              if (seg.v[j] < base + (uint32_t)s) {
+              if (!reached(seg.v[j], base + (uint32_t)s)) {
                 do ld_relaxed_gpu_v8(myseg, seg.v);
-                while (seg.v[j] < base + (uint32_t)s);
+                while (!reached(seg.v[j], base + (uint32_t)s));
                 ld_acquire_gpu_v8(myseg, seg.v);
               }
             } else {
-              wait_seg<1>(seg, myseg, j, base + (uint32_t)s);  // one 32-byte acquire poll covers the step's 8 chunks
+              wait_seg<1>(seg, myseg, j, base + (uint32_t)s, P.err);  // one 32-byte acquire poll covers the step's 8 chunks
             }
             if (!(P.variant & 128)) fence_proxy_async_global();
             tma_load_2d(sA + stage * kTileA, &P.tmA, &full[stage], dir * 4 * kH + chunk * 64, arow);
@@ -823,6 +853,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.cstate = a.cstate;
     P.y = a.y_full;
     P.trace = a.trace;
+    P.err = a.err;
     P.B = B;
     P.T = T;
     const int chunk_rows = max_blocks * fwd2::kNB;
@@ -853,6 +884,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   P.dg = a.dg;
   P.trace = a.trace;
   P.dbpart = a.dbpart;
+  P.err = a.err;
   P.variant = 7;  // acquire by ld.acquire, no writer-side fences
   {  // fp16 exchange scale: power of two ~ frames / 2 (dh ~ 1/frames for a mean loss)
     float sc = 1.f;

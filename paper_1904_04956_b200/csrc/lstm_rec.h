@@ -21,6 +21,7 @@ struct LstmParams {
   int B, T, b0, nb, n_btile;
   int variant;  // debug: bit0 skip writer proxy fence, bit1 skip release fence
   float xscale; // BPTT: fp16 scale of the exchanged partial dh (power of two)
+  int* err;     // optional: |= 8 when a flag wait times out (a peer CTA never published)
 };
 
 struct LstmLayerArgs {
@@ -34,6 +35,7 @@ struct LstmLayerArgs {
   uint32_t* counters;       // >= lstm_counter_words(B)
   uint64_t* trace = nullptr;
   float* dbpart = nullptr;  // backward: per-(batch tile, lane quadrant) column sums of dG
+  int* err = nullptr;       // step error flag: |= 8 on a flag-wait timeout
 };
 
 int lstm_max_tiles();

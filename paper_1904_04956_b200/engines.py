@@ -126,8 +126,8 @@ def run_single(objective, dataset, schedule, *, epochs: int, batch_size: int, se
                     d = compute_delay()
                     if d > 0:
                         clock.sleep(d)
-                    be.gradient(L, batch)
-                    be.sgd_step(L, learning_rate(schedule, epoch, k, len(batches)))
+                    # gradient + sgd_step (single.py:53-55) as one fused device step
+                    be.train_step(L, batch, learning_rate(schedule, epoch, k, len(batches)))
                     frames += _frames(dataset, batch)
                 be.check(L)
                 wall = clock.now() - t0

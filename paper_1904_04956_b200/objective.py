@@ -11,6 +11,7 @@ drop-in compatibility and tests; the engines keep weights on the device.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -50,6 +51,12 @@ def make_blstm_dataset(obj: BlstmObjective, n_seq: int, seed: int) -> Dataset:
 
 
 _cache: dict = {}
+# The reference calls gradient()/evaluate()/heldout_loss() from many learner
+# threads at once (RealClock actors, engines/adpsgd.py:138).  The shim keeps one
+# cached device learner, so every call holds this lock across its whole
+# set_weights -> compute -> read-back sequence: calls serialise (they share one
+# GPU stream anyway) and can never read another thread's weights or gradient.
+_call_lock = threading.RLock()
 
 
 def _learner(obj: BlstmObjective, data, batch_len: int):
@@ -73,20 +80,22 @@ def _check(obj, w):
 
 def gradient(obj: BlstmObjective, weights: np.ndarray, batch, data) -> np.ndarray:
     _check(obj, weights)
-    L = _learner(obj, data, len(batch))
-    L.set_weights(weights)
-    L.gradient(np.asarray(batch))
-    L.check_finite("gradient")
-    L.stream.synchronize()
-    return L.grad.double().cpu().numpy()
+    with _call_lock:
+        L = _learner(obj, data, len(batch))
+        L.set_weights(weights)
+        L.gradient(np.asarray(batch))
+        L.check_finite("gradient")
+        L.stream.synchronize()
+        return L.grad.double().cpu().numpy()
 
 
 def evaluate(obj: BlstmObjective, weights: np.ndarray, batch, data) -> float:
     _check(obj, weights)
-    L = _learner(obj, data, len(batch))
-    L.set_weights(weights)
-    L.loss(np.asarray(batch))
-    val = L.mean_loss()
+    with _call_lock:
+        L = _learner(obj, data, len(batch))
+        L.set_weights(weights)
+        L.loss(np.asarray(batch))
+        val = L.mean_loss()
     if not np.isfinite(val):
         raise ValueError(f"{obj.kind} loss is non-finite (weights diverged?)")
     return val
@@ -95,11 +104,7 @@ def evaluate(obj: BlstmObjective, weights: np.ndarray, batch, data) -> float:
 def heldout_loss(obj: BlstmObjective, weights: np.ndarray, data) -> float:
     _check(obj, weights)
     idx = np.asarray(data.heldout_indices)
-    L = _learner(obj, data, min(len(idx), 256))
-    L.set_weights(weights)
-    total = 0.0
-    for s in range(0, len(idx), L.max_batch):
-        L.loss(idx[s:s + L.max_batch])
-        L.stream.synchronize()
-        total += float(L.loss_sum.item())
-    return total / (len(idx) * obj.frames)
+    with _call_lock:
+        L = _learner(obj, data, min(len(idx), 256))
+        L.set_weights(weights)
+        return L.heldout_mean(idx)

@@ -44,6 +44,10 @@ class NumpyBackend:
             g = g * (len(batch) * per / frames_total)
         L.g = g
 
+    def train_step(self, L, batch, lr):
+        self.gradient(L, batch)
+        self.sgd_step(L, lr)
+
     def zero_grad(self, L):
         L.g = np.zeros(self.param_dim)
 
