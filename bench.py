@@ -240,7 +240,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             red_dev = "cpu"
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    obj = BlstmObjective()
+    obj = BlstmObjective(layers=args.layers, classes=args.classes)
     B = args.batch
     T = obj.frames
     x, y, train = make_data(obj, args.n_seq, seed=0)
@@ -264,6 +264,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         from paper_1904_04956_b200.p2p import PeerGroup
 
         group = PeerGroup(L, rank, world)
+        if strategy == "ssgd" and args.ssgd_mode == "overlap":
+            group.attach_fused_ssgd()
     from paper_1904_04956_b200.p2p import adpsgd_partner, hadpsgd_layout
 
     ngroups = args.groups if strategy == "hadpsgd" else 1
@@ -280,46 +282,83 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             L.theta.add_(peer_buf).mul_(0.5)
         L.snapshot()
 
-    def sync(k: int, lr: float):
-        """the strategy's exchange after this rank's gradient of step k"""
-        if strategy == "single":
-            L.sgd_step(lr)
-        elif strategy == "ssgd":
-            if group is not None:
-                group.ssgd_step(lr)
-            else:
+    from paper_1904_04956_b200.schedule import SENDER, Topology
+
+    if strategy == "hadpsgd":
+        gid, mi = hadpsgd_layout(rank, ngroups, gsize)
+        members = list(range(gid * gsize, (gid + 1) * gsize))
+        is_sender = Topology(ngroups).role(gid + 1) == SENDER
+    else:
+        gid, mi, members = rank, 0, None
+        is_sender = strategy == "adpsgd" and Topology(world).role(rank + 1) == SENDER
+    straggle = args.straggler_sleep if rank == args.straggler_rank else 0.0
+
+    def step(k: int, host: bool = False):
+        """One learner iteration of the strategy (k = this rank's update count - 1);
+        host=True: the minibatch indices come from host memory (public API, e2e)."""
+        j = k % q
+        lr = learning_rate(sched, 1, j, q)
+
+        def grad():
+            L.gradient(mine[j]) if host else L.gradient_device(idx_dev[j], B)
+
+        def fused(lr):
+            L.train_step(mine[j], lr) if host else L.train_step(idx_dev[j], lr, device_idx=True)
+
+        if args.base_sleep > 0 or straggle > 0:  # injected compute time / slowdown on the real clock
+            time.sleep(args.base_sleep + straggle)  # (DelayModel base_compute_s / slowdowns, runtime.py:47-91)
+        if strategy == "single":  # gradient + momentum SGD fused in one graph
+            fused(lr)
+            return
+        if strategy == "adpsgd" and args.adpsgd_mode == "lockstep" or group is None:
+            if strategy == "ssgd":
+                grad()
                 with torch.cuda.stream(stream):
                     dist.all_reduce(L.grad)
                     L.grad.div_(world)
                 L.sgd_step(lr)
-        elif strategy == "adpsgd":
-            L.sgd_step(lr)
+                return
+            if strategy == "hadpsgd":
+                raise SystemExit("hadpsgd is implemented on the p2p transport only")
+            fused(lr)  # lock-step comparison: pair barriers every step
             peer = adpsgd_partner(rank, world, k + 1)
             group.mix(peer) if group is not None else nccl_mix(peer)
-        else:  # hadpsgd
-            gid, mi = hadpsgd_layout(rank, ngroups, gsize)
-            members = list(range(gid * gsize, (gid + 1) * gsize))
-            if group is not None:
-                group.ssgd_step(lr, members=members)
-            else:
-                raise SystemExit("hadpsgd is implemented on the p2p transport only")
-            peer = adpsgd_partner(gid, ngroups, k + 1) * gsize + mi
-            group.mix(peer)
-
-    def step(k: int):
-        j = k % q
-        lr = learning_rate(sched, 1, j, q)
-        if strategy in ("single", "adpsgd"):  # gradient + local momentum SGD fused in one graph
-            L.train_step(idx_dev[j], lr, device_idx=True)
-            if strategy == "adpsgd":
-                peer = adpsgd_partner(rank, world, k + 1)
-                group.mix(peer) if group is not None else nccl_mix(peer)
             return
-        L.gradient_device(idx_dev[j], B)
-        sync(k, lr)
+        if strategy == "ssgd":
+            if args.ssgd_mode == "overlap":  # per-layer group sync inside the fused step (ds_blstm_set_group)
+                fused(lr)
+            else:
+                grad()
+                group.ssgd_step(lr)
+            return
+        grad()
+        # asynchronous ADPSGD / H-ADPSGD (engines/adpsgd.py:115-288): senders initiate
+        if strategy == "adpsgd":
+            peer = adpsgd_partner(rank, world, k + 1)
+        else:
+            peer = adpsgd_partner(gid, ngroups, k + 1) * gsize + mi
+        if is_sender:
+            group.ack_gate()  # the previous exchange was acknowledged
+            if strategy == "hadpsgd":
+                group.ssgd_step(lr, members=members)
+            elif args.adpsgd_mode == "fused":
+                group.update_exchange_async(peer, lr)
+                return
+            else:
+                L.sgd_step(lr)
+            group.exchange_async(peer)
+        elif strategy == "hadpsgd":
+            group.ssgd_step(lr, members=members, locked=True)
+        else:
+            group.locked_update(lr)
+
+    def drain():
+        if group is not None:
+            group.ack_gate()  # the learner stream waits for the last exchange
 
     for k in range(args.warmup):
         step(k)
+    drain()
     L.check_finite()
     torch.cuda.synchronize()
     if dist is not None:
@@ -330,13 +369,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ev0.record(stream)
         for k in range(args.steps):
             step(args.warmup + k)
+        drain()
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
+    per_rank_ms = [ms]
     if dist is not None:
-        t = torch.tensor([ms], device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        t = torch.zeros(world, device=red_dev)
+        t[rank] = ms
+        dist.all_reduce(t)  # every rank's device time (straggler analysis); the bench uses the max
+        per_rank_ms = [round(float(v), 3) for v in t.tolist()]
+        ms = max(per_rank_ms)
         dist.barrier()
     L.check_finite()
     if group is not None:
@@ -344,8 +387,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     frames = args.steps * B * T * world
     value = frames / (ms / 1e3)
     # fwd/bwd kernels + the strategy's sync kernels (sgd+aux / barriers + shard step or mix + aux)
+    # per step: ssgd barrier + shard + barrier + aux; adpsgd sender sgd + lock + mix + unlock (receiver
+    # lock + sgd + unlock); hadpsgd the group step (+ locks) and the sender's exchange
     sync_launches = {"single": 0, "ssgd": 4 if group is not None else 2, "adpsgd": 4 if group is not None else 2,
-                     "hadpsgd": 10}[strategy]  # fused train steps count their SGD launches in kernel_count()
+                     "hadpsgd": 8}[strategy]  # fused train steps count their SGD launches in kernel_count()
     launches_per_step = L.kernel_count() + sync_launches
 
     # ---- end to end through the public Learner API (host indices in, loss out)
@@ -356,20 +401,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     t0 = time.perf_counter()
     pending = None  # every step's loss is read back; the host issues step k+1 before reading step k's
     for k in range(e2e_steps):
-        j = k % q
-        lr = learning_rate(sched, 1, j, q)
-        if strategy in ("single", "adpsgd"):
-            L.train_step(mine[j], lr)
-            if strategy == "adpsgd":
-                peer = adpsgd_partner(rank, world, args.warmup + args.steps + k + 1)
-                group.mix(peer) if group is not None else nccl_mix(peer)
-        else:
-            L.gradient(mine[j])
-            sync(args.warmup + args.steps + k, lr)
+        step(args.warmup + args.steps + k, host=True)
         fut = L.loss_async()
         if pending is not None:
             _ = pending()
         pending = fut
+    drain()
     _ = pending()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -435,8 +472,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "layers": obj.layers, "cells": 1024, "bottleneck": obj.bottleneck, "classes": obj.classes,
                    "input_dim": obj.input_dim, "frames": T, "batch_per_learner": B, "global_batch": B * world,
                    "strategy": strategy, "transport": args.transport if world > 1 else None,
+                   "mode": (args.ssgd_mode if strategy == "ssgd" else args.adpsgd_mode
+                            if strategy in ("adpsgd", "hadpsgd") else None),
+                   "straggler": ({"rank": args.straggler_rank, "extra_sleep_s": args.straggler_sleep}
+                                 if args.straggler_sleep > 0 else None),
                    "l2_policy": "per-step working set ~1.2 GB (activations, 344 MB dlogits) >> 126 MB L2; no flush",
                    "parallelism": f"dp{world}"},
+        "per_rank_ms": per_rank_ms,
         "roofline": roof, "cpu_baseline": cpu, "library_baseline": lib_base, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
     }
@@ -448,6 +490,32 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         L.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` without torchrun: launch the N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1 and relay rank 0's
+    line.  Fails loudly when fewer than N GPUs are visible (unless
+    --same-device)."""
+    import socket
+
+    try:
+        import torch
+
+        ndev = torch.cuda.device_count()
+    except Exception:  # pragma: no cover
+        ndev = 0
+    if ndev < args.gpus and not args.same_device:
+        print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "error": f"--gpus {args.gpus} but only {ndev} "
+                          "CUDA device(s) visible (use --same-device for a functional one-GPU run)"}), flush=True)
+        return 2
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -466,7 +534,20 @@ def main():
     ap.add_argument("--groups", type=int, default=2)
     ap.add_argument("--same-device", action="store_true",
                     help="all ranks on cuda:0 with gloo plumbing (functional check only; p2p transport)")
+    ap.add_argument("--adpsgd-mode", default="async", choices=["async", "fused", "lockstep"],
+                    help="async: the reference protocol (sender-initiated, ack-gated, receiver lock); fused: "
+                         "sender update+mix in one kernel (ds_update_mix); lockstep: pair barriers every step")
+    ap.add_argument("--ssgd-mode", default="overlap", choices=["overlap", "after"],
+                    help="overlap: each layer's allreduce+SGD runs beside the BPTT of the layers below; after: "
+                         "one sharded step after the whole backward")
+    ap.add_argument("--straggler-rank", type=int, default=-1, help="rank that sleeps --straggler-sleep s per step")
+    ap.add_argument("--straggler-sleep", type=float, default=0.0)
+    ap.add_argument("--base-sleep", type=float, default=0.0, help="host sleep per step on every rank (simulated compute)")
+    ap.add_argument("--layers", type=int, default=6, help="(tests) smaller models; the bench config is 6")
+    ap.add_argument("--classes", type=int, default=32000, help="(tests) smaller output layer; bench config 32000")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -189,12 +189,67 @@ void* ds_blstm_snapshot_ptr(ds_blstm* h);
 int ds_blstm_snapshot_aux(ds_blstm* h, const float* theta, ds_stream_t stream);
 
 /* Device-side barrier of n members: flag word member_flags[m][my_rank] is set
- * to `epoch` for every member m, then the call waits on the stream until
- * own_flags[member_ranks[m]] >= epoch for all m.  Epochs must increase
- * monotonically per process (SPMD call order).  After timeout_s the wait
- * gives up and sets *err (checked by the host): a lost peer never hangs. */
+ * to e_m = ++pair_epochs[member_ranks[m]] for every member m, then the call
+ * waits on the stream until own_flags[member_ranks[m]] >= e_m (wrap-safe).
+ * pair_epochs is a device array [64] of this rank's per-pair barrier counts
+ * (incremented by the kernel, so ranks may take part in different subsets of
+ * barriers and the barrier can be replayed inside a CUDA graph).  After
+ * timeout_s the wait gives up and sets *err |= 1 (checked by the host): a
+ * lost peer never hangs. */
 int ds_peer_barrier(int32_t n, uint32_t* const* member_flags, const int32_t* member_ranks, int32_t my_rank,
-                    uint32_t* own_flags, uint32_t epoch, int32_t* err, double timeout_s, ds_stream_t stream);
+                    uint32_t* own_flags, uint32_t* pair_epochs, int32_t* err, double timeout_s, ds_stream_t stream);
+
+/* SSGD group of the fused training step (engines/ssgd.py:80-90 with the
+ * allreduce of collective.py:122-163 overlapped with the backward): when set,
+ * ds_blstm_train_step replaces each layer's local momentum update by
+ *   barrier -> reduce the owned chunks of that layer's gradient block in the
+ *   canonical owner-first order, / divisor, momentum SGD, store theta and its
+ *   bf16 snapshot into every member -> barrier
+ * on the side stream as soon as the layer's gradient is final (while the
+ * BPTT of the layer below runs).  Results are bit-identical to the
+ * whole-vector ds_shard_step.  Member buffers are peer-mapped pointers. */
+#define DS_MAX_GROUP 16
+typedef struct {
+  int32_t n;          /* members (learners of the group)                       */
+  int32_t me;         /* this learner's member index = chunk owner id           */
+  int32_t my_rank;    /* this process's world rank (barrier flag slot)          */
+  int32_t nchunks;    /* make_chunk_plan(param_dim, n, nchunks), >= n           */
+  float divisor;      /* g_mean = sum / divisor; <= 0 selects n                 */
+  int32_t max_blocks; /* grid cap of the per-layer sync kernels (0: default 64) */
+  int32_t ranks[DS_MAX_GROUP];
+  float* thetas[DS_MAX_GROUP];
+  const float* grads[DS_MAX_GROUP];
+  void* snaps[DS_MAX_GROUP];
+  uint32_t* flags[DS_MAX_GROUP];
+  uint32_t* own_flags;
+  uint32_t* pair_epochs;
+  int32_t* err;
+  double timeout_s;
+} ds_group_desc;
+/* NULL clears (back to the local momentum update). */
+int ds_blstm_set_group(ds_blstm* h, const ds_group_desc* g);
+
+/* Exclusive access to one learner's weights across devices (the receiver's
+ * atomic region of engines/adpsgd.py:280-285 without a receiver thread): a
+ * system-scope CAS on a lock word in the owner's memory (peer pointer
+ * allowed) by one thread on `stream`; owner != 0 identifies the holder.
+ * Timeout sets *err |= 2.  Every work item ordered between ds_peer_lock and
+ * ds_peer_unlock on the stream runs while the lock is held. */
+int ds_peer_lock(uint32_t* word, uint32_t owner, int32_t* err, double timeout_s, ds_stream_t stream);
+int ds_peer_unlock(uint32_t* word, ds_stream_t stream);
+
+/* N1, ADPSGD throughput mode: the sender's sgd_step (optim.py:109-121) and
+ * its pairwise average (adpsgd_mix, engines/adpsgd.py:36-43) in one pass:
+ * v <- mu v + g; t' = theta - lr v; snap <- bf16(t') (nullable: the next
+ * gradient's operands, pre-mix as in the reference); m = (t' + peer) / 2
+ * stored to theta and peer (peer pointer: one NVLink read + write). */
+int ds_update_mix(float* theta, float* vel, const float* grad, float* theta_peer, void* snap, float lr, float mu,
+                  int64_t n, int32_t* nonfinite, ds_stream_t stream);
+
+/* Debug payload digest replacing the reference's blake2b WeightMessage
+ * checksum (engines/common.py:78-104): 128 bits over the buffer's 32-bit
+ * words written to out2[0..1] (device) on `stream`. */
+int ds_digest(const void* data, int64_t nbytes, unsigned long long* out2, ds_stream_t stream);
 
 /* Sharded group step of rank `rank` (RingAllreduceGroup.allreduce + /world +
  * sgd_step, engines/ssgd.py:84-87): for the chunks this rank owns
@@ -205,6 +260,14 @@ int ds_peer_barrier(int32_t n, uint32_t* const* member_flags, const int32_t* mem
 int ds_shard_step(int32_t world, int32_t rank, const float* const* grads, float* const* thetas,
                   void* const* snaps, float* v_own, int64_t n, int32_t nchunks, float lr, float mu, int32_t mode,
                   float divisor, ds_stream_t stream);
+/* The same restricted to elements [range_lo, range_hi) (range_lo % 4 == 0):
+ * one parameter block (a layer) synchronised as soon as its gradient is
+ * final, with the chunk ownership and summation order of the whole-vector
+ * plan (bit-identical results); max_blocks > 0 caps the grid (side stream). */
+int ds_shard_step_range(int32_t world, int32_t rank, const float* const* grads, float* const* thetas,
+                        void* const* snaps, float* v_own, int64_t n, int32_t nchunks, float lr, float mu,
+                        int32_t mode, float divisor, int64_t range_lo, int64_t range_hi, int32_t max_blocks,
+                        ds_stream_t stream);
 
 /* ADPSGD pairwise average (adpsgd_mix) over P2P: m = (self + peer) / 2 on
  * half 0 ([0, n/2)), half 1 ([n/2, n)) or -1 (all), stored to both sides and

@@ -56,12 +56,19 @@ SIGNATURES = {
     "ds_enable_peer_access": (_I32, [_I32, _I32]),
     "ds_blstm_snapshot_ptr": (_VP, [_VP]),
     "ds_blstm_snapshot_aux": (_I32, [_VP, _VP, _VP]),
-    "ds_peer_barrier": (_I32, [_I32, _VP, _VP, _I32, _VP, ctypes.c_uint32, _VP, ctypes.c_double, _VP]),
+    "ds_peer_barrier": (_I32, [_I32, _VP, _VP, _I32, _VP, _VP, _VP, ctypes.c_double, _VP]),
+    "ds_peer_lock": (_I32, [_VP, ctypes.c_uint32, _VP, ctypes.c_double, _VP]),
+    "ds_peer_unlock": (_I32, [_VP, _VP]),
+    "ds_update_mix": (_I32, [_VP, _VP, _VP, _VP, _VP, _F32, _F32, _I64, _VP, _VP]),
+    "ds_digest": (_I32, [_VP, _I64, _VP, _VP]),
+    "ds_shard_step_range": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _I64, _I32, _F32, _F32, _I32, _F32, _I64, _I64,
+                                   _I32, _VP]),
     "ds_shard_step": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _I64, _I32, _F32, _F32, _I32, _F32, _VP]),
     "ds_pair_mix": (_I32, [_VP, _VP, _VP, _VP, _I64, _I32, _VP]),
     "ds_blstm_set_precision": (_I32, [_VP, _I32]),
     "ds_blstm_get_precision": (_I32, [_VP]),
     "ds_debug_gemm_tf32x3": (_I32, [_VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _I32, _VP]),
+    "ds_blstm_set_group": (_I32, [_VP, _VP]),
     "ds_last_error": (ctypes.c_char_p, []),
 }
 
@@ -78,6 +85,21 @@ class DsCfg(ctypes.Structure):
         ("classes", _I32),
         ("frames", _I32),
         ("max_batch", _I32),
+    ]
+
+
+DS_MAX_GROUP = 16
+
+
+class DsGroupDesc(ctypes.Structure):
+    """ds_group_desc of include/ds_blstm.h (fused SSGD group step)."""
+
+    _fields_ = [
+        ("n", _I32), ("me", _I32), ("my_rank", _I32), ("nchunks", _I32), ("divisor", _F32), ("max_blocks", _I32),
+        ("ranks", _I32 * DS_MAX_GROUP),
+        ("thetas", _VP * DS_MAX_GROUP), ("grads", _VP * DS_MAX_GROUP), ("snaps", _VP * DS_MAX_GROUP),
+        ("flags", _VP * DS_MAX_GROUP),
+        ("own_flags", _VP), ("pair_epochs", _VP), ("err", _VP), ("timeout_s", ctypes.c_double),
     ]
 
 

@@ -11,6 +11,7 @@
 #include "layout.h"
 #include "lstm_rec.h"
 #include "ops.h"
+#include "p2p.h"
 #include "parity.h"
 #include "softmax_dz.h"
 
@@ -72,9 +73,10 @@ struct ds_blstm {
     float* theta;
     float* vel;
     float mu;
+    const void* grp;
     bool operator==(const Key& o) const {
       return B == o.B && idx == o.idx && grad == o.grad && loss == o.loss && flag == o.flag && bwd == o.bwd &&
-             gscale == o.gscale && theta == o.theta && vel == o.vel && mu == o.mu;
+             gscale == o.gscale && theta == o.theta && vel == o.vel && mu == o.mu && grp == o.grp;
     }
   };
   struct Entry {
@@ -92,6 +94,9 @@ struct ds_blstm {
   // precision mode: 0 = BF16 perf path, 1 = FP32 parity (3xTF32 tcgen05, parity.cu)
   int prec = 0;
   ParityWs* par = nullptr;
+  // SSGD peer group of the fused training step (ds_blstm_set_group)
+  GroupSync grp;
+  bool grp_on = false;
 };
 
 namespace {
@@ -241,9 +246,27 @@ struct SgdCtx {
   float* vel = nullptr;
   float mu = 0.f;
   int nfork = 0;
+  const GroupSync* grp = nullptr;  // SSGD: per-layer group sync instead of the local update
 };
+// SSGD group update of [off, off + n): barrier, sharded reduce + SGD + all-gather, barrier
+int group_segment(ds_blstm* h, SgdCtx& c, int64_t off, int64_t n, cudaStream_t s) {
+  int rc = group_barrier(*c.grp, s);
+  if (!rc) rc = group_shard_range(*c.grp, h->L.total, off, off + n, c.vel, h->d_lr, c.mu, s);
+  if (!rc) rc = group_barrier(*c.grp, s);
+  return rc;
+}
 int sgd_segment(ds_blstm* h, SgdCtx& c, float* grad, int* flag, int64_t off, int64_t n, bool side, cudaStream_t s) {
   if (!c.theta) return DS_OK;
+  if (c.grp) {
+    if (!side) return group_segment(h, c, off, n, s);
+    const int k = c.nfork++;
+    DS_CUDA_TRY(cudaEventRecord(h->ev_fork[k], s));
+    DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork[k], 0));
+    int rc = group_segment(h, c, off, n, h->side);
+    if (rc) return rc;
+    DS_CUDA_TRY(cudaEventRecord(h->ev_join[k], h->side));
+    return DS_OK;
+  }
   if (!side)
     return op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, 0, s);
   const int k = c.nfork++;
@@ -606,7 +629,7 @@ int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, i
   DS_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
   if (!use_graphs() || h->profile || cs != cudaStreamCaptureStatusNone)
     return issue_step(h, idx, B, grad, loss, flag, s, sg);
-  ds_blstm::Key key{B, idx, grad, loss, flag, grad != nullptr, h->grad_frames, sg.theta, sg.vel, sg.mu};
+  ds_blstm::Key key{B, idx, grad, loss, flag, grad != nullptr, h->grad_frames, sg.theta, sg.vel, sg.mu, sg.grp};
   for (auto& e : h->graphs)
     if (e.key == key) {
       DS_CUDA_TRY(cudaGraphLaunch(e.exec, s));
@@ -743,6 +766,44 @@ int ds_blstm_set_precision(ds_blstm* h, int32_t mode) {
 
 int32_t ds_blstm_get_precision(ds_blstm* h) { return h ? h->prec : -1; }
 
+int ds_blstm_set_group(ds_blstm* h, const ds_group_desc* g) {
+  if (!h) return fail_arg("null handle");
+  for (auto& e : h->graphs) cudaGraphExecDestroy(e.exec);  // graphs bake the update path
+  h->graphs.clear();
+  if (!g) {
+    h->grp_on = false;
+    return DS_OK;
+  }
+  if (g->n < 1 || g->n > kMaxGroupPeers || g->me < 0 || g->me >= g->n) return fail_arg("group: bad member count / index");
+  if (g->nchunks < g->n) return fail_arg("group: chunk_count must be >= members");
+  if (!g->own_flags || !g->pair_epochs || !g->err) return fail_arg("group: null flag / epoch / error buffer");
+  GroupSync gs;
+  gs.n = g->n;
+  gs.me = g->me;
+  gs.my_rank = g->my_rank;
+  gs.nchunks = g->nchunks;
+  gs.divisor = g->divisor;
+  gs.max_blocks = g->max_blocks > 0 ? g->max_blocks : 64;
+  for (int m = 0; m < g->n; ++m) {
+    if (!g->thetas[m] || !g->grads[m] || !g->snaps[m] || !g->flags[m] || g->ranks[m] < 0 || g->ranks[m] >= 64)
+      return fail_arg("group: null member buffer");
+    if ((reinterpret_cast<uintptr_t>(g->thetas[m]) | reinterpret_cast<uintptr_t>(g->grads[m])) & 15)
+      return fail_arg("group: buffers must be 16-byte aligned");
+    gs.ranks[m] = g->ranks[m];
+    gs.thetas[m] = g->thetas[m];
+    gs.grads[m] = g->grads[m];
+    gs.snaps[m] = g->snaps[m];
+    gs.flags[m] = g->flags[m];
+  }
+  gs.own_flags = g->own_flags;
+  gs.pair_epochs = g->pair_epochs;
+  gs.err = g->err;
+  gs.timeout_s = g->timeout_s;
+  h->grp = gs;
+  h->grp_on = true;
+  return DS_OK;
+}
+
 int ds_blstm_snapshot_aux(ds_blstm* h, const float* theta, ds_stream_t stream) {
   if (!h || !theta) return fail_arg("null argument");
   DS_CUDA_TRY(cudaSetDevice(h->device));
@@ -777,6 +838,12 @@ int ds_blstm_train_step(ds_blstm* h, const int64_t* idx, int32_t B, float* theta
   sg.theta = theta;
   sg.vel = vel;
   sg.mu = mu;
+  if (h->grp_on) {
+    if (h->prec != 0) return fail_arg("the fused SSGD group step runs in BF16 mode only");
+    if (h->grp.thetas[h->grp.me] != theta || h->grp.grads[h->grp.me] != grad)
+      return fail_arg("group step: theta / grad differ from this member's buffers in the group");
+    sg.grp = &h->grp;
+  }
   return run_step(h, idx, B, grad, loss_sum, nonfinite, s, sg);
 }
 
