@@ -393,6 +393,47 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "hadpsgd": 8}[strategy]  # fused train steps count their SGD launches in kernel_count()
     launches_per_step = L.kernel_count() + sync_launches
 
+    # ---- the sync step alone (NVLink roofline of the sync kernels, SURVEY §8d bytes per unit)
+    sync_meas = None
+    if group is not None and world > 1:
+        reps = 5
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        P4 = 4 * obj.param_dim
+        timed = True
+        if strategy in ("ssgd", "hadpsgd"):
+            mem = members if strategy == "hadpsgd" else list(range(world))
+            lam = len(mem)
+            t0e.record(stream)
+            for _ in range(reps):
+                group.ssgd_step(1e-6, members=mem)
+            t1e.record(stream)
+            kern = "ds_shard_step between two ds_peer_barrier (whole vector, %d members)" % lam
+            rx, tx = (lam - 1) / lam * P4, (lam - 1) / lam * (P4 + P4 // 2)  # gradients in; theta + bf16 snapshot out
+        else:
+            kern = "ds_pair_mix under the receiver's lock (sender side, whole vector)"
+            rx, tx = P4, P4
+            if is_sender:
+                t0e.record(group.comm)
+                for _ in range(reps):
+                    group.exchange_async(adpsgd_partner(rank, world, 1))
+                t1e.record(group.comm)
+                group.ack_gate()
+            else:
+                timed = False
+        torch.cuda.synchronize()
+        sms = t0e.elapsed_time(t1e) / reps if timed else 0.0
+        t = torch.tensor([sms], device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sms = float(t.item())
+        gbs = max(rx, tx) / (sms * 1e-3) / 1e9 if sms > 0 else None
+        sync_meas = {"kernel": kern, "ms": round(sms, 4), "rx_bytes": int(rx), "tx_bytes": int(tx),
+                     "achieved_gbs_per_direction": round(gbs, 1) if gbs else None,
+                     "peak_gbs_per_direction": 900.0, "peak_kind": "NVLink 5 nominal per direction (spec)",
+                     "frac": round(gbs / 900.0, 4) if gbs else None,
+                     "path": "same-device IPC (HBM, functional only)" if args.same_device else "NVLink P2P"}
+
     # ---- end to end through the public Learner API (host indices in, loss out)
     e2e_steps = max(3, min(args.steps, 60))
     torch.cuda.synchronize()
@@ -479,6 +520,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "l2_policy": "per-step working set ~1.2 GB (activations, 344 MB dlogits) >> 126 MB L2; no flush",
                    "parallelism": f"dp{world}"},
         "per_rank_ms": per_rank_ms,
+        "sync": sync_meas,
         "roofline": roof, "cpu_baseline": cpu, "library_baseline": lib_base, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
     }

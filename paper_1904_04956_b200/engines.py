@@ -62,18 +62,33 @@ class RunResult:
 
 @dataclass(frozen=True)
 class WeightMessage:
-    """Timestamped weight payload.  On the device path the payload is a
-    reference to the sender's learner (the mix kernel reads it over
-    NVLink/HBM); the reference's blake2b digest (common.py:78-104) is
-    replaced by stream/lock ordering."""
+    """Timestamped weight payload (common.py:78-104).  On the device path the
+    payload is a reference to the sender's learner (the mix kernel reads it
+    over NVLink/HBM), so no copy is shipped.  With `checksum=True` runs
+    (debug mode) the message carries a 128-bit device digest of the weights
+    it stands for (ds_digest) and `validate` recomputes it on the live
+    buffer: a request proves the sender's weights were not touched between
+    shipping and the receiver's mix (no torn snapshot), a reply proves both
+    learners hold the identical mean.  Mismatch -> ChecksumError, as in the
+    reference.  Without checksums ordering is structural (streams, locks)."""
 
     origin: int
     timestamp: int
     payload: object
     checksum: str = ""
+    digest_fn: object = None
 
-    def validate(self) -> None:
-        return None
+    @classmethod
+    def snapshot(cls, origin: int, timestamp: int, payload, digest_fn=None) -> "WeightMessage":
+        return cls(origin, timestamp, payload, digest_fn(payload) if digest_fn else "", digest_fn)
+
+    def validate(self, against=None) -> None:
+        if not self.checksum:
+            return None
+        live = self.digest_fn(self.payload if against is None else against)
+        if live != self.checksum:
+            raise ChecksumError(f"weights from learner {self.origin} (ts {self.timestamp}) changed in flight: "
+                                f"{live} != {self.checksum}")
 
 
 def _make_backend(objective, dataset, batch_size: int, backend):
@@ -352,7 +367,7 @@ class _Unit:
 
 def _run_gossip(objective, dataset, schedule, *, units: int, epochs: int, batch_size: int, seed: int,
                 momentum: float, delays, clock, record_trace: bool, init_weights, backend, group_size: int,
-                chunk_count=None, strategy: str = "adpsgd") -> RunResult:
+                chunk_count=None, strategy: str = "adpsgd", checksum: bool = False) -> RunResult:
     topo = Topology(units)
     _check_epochs(epochs, schedule)
     clock = clock or VirtualClock()
@@ -375,6 +390,11 @@ def _run_gossip(objective, dataset, schedule, *, units: int, epochs: int, batch_
     staleness = StalenessRecord(strategy)
     exchange_log: list = []
     staleness_by_learner = {i: [] for i in range(1, units + 1)}
+
+    def unit_digest(unit: "_Unit") -> str:
+        return "".join(be.digest(m) for m in unit.members)
+
+    digest = unit_digest if checksum else None
 
     def draw_snapshot(st: _State):
         # caller holds st.lock: weights as of this DRAW (adpsgd.py:132-134)
@@ -417,7 +437,7 @@ def _run_gossip(objective, dataset, schedule, *, units: int, epochs: int, batch_
                             pending = False
                         with st.lock:
                             local_update(st, epoch, k, pool_size, mut0)
-                            msg = WeightMessage(i, st.iteration, st.dev)
+                            msg = WeightMessage.snapshot(i, st.iteration, st.dev, digest)
                             partner = topo.partner(i, st.iteration)
                         job[i].put(("exchange", msg, partner))
                         pending = True
@@ -454,7 +474,7 @@ def _run_gossip(objective, dataset, schedule, *, units: int, epochs: int, batch_
                     continue
                 inbox[partner].put(("exchange", msg))
                 resp: WeightMessage = reply[i].get()
-                resp.validate()
+                resp.validate(against=st.dev)  # the receiver wrote the identical mean into both
                 if resp.timestamp < last_ts.get(resp.origin, -1):
                     raise RuntimeError(f"non-monotone timestamp from learner {resp.origin}: "
                                        f"{resp.timestamp} after {last_ts[resp.origin]}")
@@ -532,8 +552,8 @@ def _run_gossip(objective, dataset, schedule, *, units: int, epochs: int, batch_
                                        f"{msg.timestamp} after {last_ts[msg.origin]}")
                 last_ts[msg.origin] = msg.timestamp
                 with st.lock:
-                    mine = WeightMessage(j, st.iteration, st.dev)
                     st.dev.mix(msg.payload)  # identical mean into both sides (K10)
+                    mine = WeightMessage.snapshot(j, st.iteration, st.dev, digest)
                     st.mutations += 1
                     st.exchanges += 1
                 reply[msg.origin].put(mine)
@@ -587,12 +607,14 @@ def _run_gossip(objective, dataset, schedule, *, units: int, epochs: int, batch_
 
 def run_adpsgd(objective, dataset, schedule, *, learners: int, epochs: int, batch_size: int, seed: int,
                momentum: float = 0.9, delays: DelayModel | None = None, clock=None, record_trace: bool = False,
-               init_weights=None, backend=None) -> RunResult:
+               init_weights=None, backend=None, checksum: bool = False) -> RunResult:
     """Asynchronous decentralized parallel SGD on the bipartite ring
-    (engines/adpsgd.py:65-346); returns the uniform average of all learners."""
+    (engines/adpsgd.py:65-346); returns the uniform average of all learners.
+    checksum=True validates every exchanged payload with a device digest
+    (debug mode of the reference's WeightMessage checksum)."""
     return _run_gossip(objective, dataset, schedule, units=learners, epochs=epochs, batch_size=batch_size, seed=seed,
                        momentum=momentum, delays=delays, clock=clock, record_trace=record_trace,
-                       init_weights=init_weights, backend=backend, group_size=1)
+                       init_weights=init_weights, backend=backend, group_size=1, checksum=checksum)
 
 
 def run_hadpsgd(objective, dataset, schedule, *, groups: int, group_size: int, epochs: int, batch_size: int,

@@ -96,6 +96,11 @@ class NumpyBackend:
     def average(self, members):
         return np.mean(np.stack([m.w for m in members]), axis=0)
 
+    def digest(self, L):
+        import hashlib
+
+        return hashlib.blake2b(np.ascontiguousarray(L.w).tobytes(), digest_size=16).hexdigest()
+
     def heldout_loss(self, w):
         return self.heldout_fn(self.obj, w.w if isinstance(w, _L) else w, self.data)
 

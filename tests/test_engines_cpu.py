@@ -153,3 +153,32 @@ def test_validation_errors(ref):
         E.run_ssgd(obj, data, sched, learners=1, epochs=1, batch_size=8, seed=0, backend=be)
     with pytest.raises(ValueError):
         E.run_single(obj, data, sched, epochs=5, batch_size=8, seed=0, backend=be)
+
+
+def test_adpsgd_checksum_mode(ref):
+    """Debug payload checksums (WeightMessage, common.py:78-104): identical
+    results with checksums on, and a mix that leaves the two learners with
+    different weights is caught as ChecksumError."""
+    obj, data = _problem(ref, "logistic")
+    sched = ref.baseline_schedule(0.1, total_epochs=2)
+    _, md = _delays(ref)
+    kw = dict(learners=4, epochs=2, batch_size=16, seed=2, clock=VirtualClock())
+    a = E.run_adpsgd(obj, data, sched, delays=md, backend=_backend(ref, obj, data), **kw)
+    _, md2 = _delays(ref)
+    kw["clock"] = VirtualClock()
+    b = E.run_adpsgd(obj, data, sched, delays=md2, backend=_backend(ref, obj, data), checksum=True, **kw)
+    assert np.array_equal(a.weights, b.weights)
+    _same_records(a.records, b.records)
+
+    class Torn(NumpyBackend):
+        def mix(self, x, y):
+            super().mix(x, y)
+            y.w = y.w + 1e-12  # the two sides no longer hold the identical mean
+
+    _, md3 = _delays(ref)
+    kw["clock"] = VirtualClock()
+    with pytest.raises(E.ChecksumError):
+        import distsgd.objectives as ro
+
+        E.run_adpsgd(obj, data, sched, delays=md3, backend=Torn(obj, data, ro.gradient, ro.heldout_loss),
+                     checksum=True, **kw)

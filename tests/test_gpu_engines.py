@@ -86,3 +86,39 @@ def test_hadpsgd_gpu_vs_oracle():
 
 def test_hybrid_gpu_vs_oracle():
     _compare(E.run_hybrid, learners=2, epochs=1, batch_size=8)
+
+
+def _gpu_run(run, be, **kw):
+    w0 = O.initial_weights(SPEC, 4)
+    sched = baseline_schedule(0.05, total_epochs=2)
+    res = run(OBJ, DATA, sched, seed=4, init_weights=w0, delays=_delays(), clock=VirtualClock(), backend=be, **kw)
+    be.close()
+    return res
+
+
+@pytest.mark.parametrize("run,kw", [(E.run_adpsgd, dict(learners=4, epochs=2, batch_size=8)),
+                                    (E.run_ssgd, dict(learners=2, epochs=1, batch_size=8)),
+                                    (E.run_hadpsgd, dict(groups=2, group_size=2, epochs=1, batch_size=4)),
+                                    (E.run_hybrid, dict(learners=2, epochs=1, batch_size=8))])
+def test_per_learner_streams_bit_identical(run, kw):
+    """Learners on their own CUDA streams (and devices, when the box has
+    several) with event-ordered dependencies replay the schedule
+    bit-identically to the single-stream layout."""
+    ref = _gpu_run(run, GpuBackend(OBJ, DATA, max_batch=16), **kw)
+    layouts = [dict(streams="per_learner")]
+    if torch.cuda.device_count() >= 2:
+        layouts.append(dict(devices=list(range(min(4, torch.cuda.device_count())))))
+    for lay in layouts:
+        got = _gpu_run(run, GpuBackend(OBJ, DATA, max_batch=16, **lay), **kw)
+        assert np.array_equal(ref.weights, got.weights), lay
+        for a, b in zip(ref.records, got.records):
+            assert a == b, lay
+
+
+def test_adpsgd_device_checksums():
+    """checksum=True: every exchange validated with the device digest
+    (ds_digest); results unchanged."""
+    ref = _gpu_run(E.run_adpsgd, GpuBackend(OBJ, DATA, max_batch=16), learners=4, epochs=1, batch_size=8)
+    got = _gpu_run(E.run_adpsgd, GpuBackend(OBJ, DATA, max_batch=16, streams="per_learner"), learners=4, epochs=1,
+                   batch_size=8, checksum=True)
+    assert np.array_equal(ref.weights, got.weights)
