@@ -4,7 +4,7 @@ the ones the P2P path runs with peer pointers, where NVLink instead of HBM is
 the bound).  Prints one JSON object; bytes are algorithmic (each parameter
 array element read / written once).
 
-  python tools/sync_bench.py > profiles/r1_sync_kernels.json
+  python tools/sync_bench.py > profiles/r2_sync_kernels.json
 """
 import ctypes
 import json
@@ -25,6 +25,9 @@ v = [torch.zeros(P, device=dev) for _ in range(2)]
 g = [torch.randn(P, device=dev) * 1e-3 for _ in range(2)]
 snap = [torch.zeros(P, device=dev, dtype=torch.bfloat16) for _ in range(2)]
 flag = torch.zeros(1, device=dev, dtype=torch.int32)
+err = torch.zeros(1, device=dev, dtype=torch.int32)
+ctl = torch.zeros(16, device=dev, dtype=torch.int32)
+dig = torch.zeros(2, device=dev, dtype=torch.int64)
 s = torch.cuda.current_stream().cuda_stream
 
 
@@ -58,6 +61,18 @@ cases = {
     "shard_step world 2, both ranks (SSGD reduce-scatter + SGD + all-gather)": (
         lambda: [_lib.check(lib.ds_shard_step(2, r, arr(g), arr(th), arr(snap), v[r].data_ptr(), P, 2, 0.01, 0.9, 0,
                                                0.0, s)) for r in (0, 1)], 32 * P),
+    "update_mix (N1: sgd_step + pair average in one pass; theta,v rw + g r + snapshot w + peer rw)": (
+        lambda: _lib.check(lib.ds_update_mix(th[0].data_ptr(), v[0].data_ptr(), g[0].data_ptr(), th[1].data_ptr(),
+                                             snap[0].data_ptr(), 0.01, 0.9, P, flag.data_ptr(), s)), 30 * P),
+    "sgd_momentum + adpsgd_mix unfused (the N1 baseline)": (
+        lambda: (_lib.check(lib.ds_sgd_momentum(th[0].data_ptr(), v[0].data_ptr(), g[0].data_ptr(), 0.01, 0.9, P,
+                                                None, flag.data_ptr(), s)),
+                 _lib.check(lib.ds_adpsgd_mix(th[0].data_ptr(), th[1].data_ptr(), P, s))), 30 * P),
+    "digest (debug WeightMessage checksum, theta read)": (
+        lambda: _lib.check(lib.ds_digest(th[0].data_ptr(), 4 * P, dig.data_ptr(), s)), 4 * P),
+    "peer lock + unlock (empty critical section)": (
+        lambda: (_lib.check(lib.ds_peer_lock(ctl.data_ptr(), 1, err.data_ptr(), 5.0, s)),
+                 _lib.check(lib.ds_peer_unlock(ctl.data_ptr(), s))), 0),
     "group_reduce world 2, both owners (single-process SSGD)": (
         lambda: [_lib.check(lib.ds_group_reduce(2, r, arr(g), arr(th), arr(v), None, P, 2, 0.01, 0.9, 0, 0.0, s))
                  for r in (0, 1)], 36 * P),
@@ -72,5 +87,5 @@ for name, (fn, nbytes) in cases.items():
     ms = timed(fn)
     gbs = nbytes / (ms * 1e-3) / 1e9
     out["kernels"][name] = {"ms": round(ms, 4), "bytes": nbytes, "GB/s": round(gbs, 1),
-                            "frac_of_hbm": round(gbs / peak, 3) if peak else None}
+                            "frac_of_hbm": round(gbs / peak, 3) if peak and nbytes else None}
 print(json.dumps(out, indent=1))
