@@ -277,10 +277,10 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
-__global__ void digest_kernel(const uint32_t* __restrict__ w, int64_t n, unsigned long long* out) {
+__global__ void digest_kernel(const uint32_t* __restrict__ words, int64_t n, unsigned long long* out) {
   uint64_t a = 0, b = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = ((uint64_t)i << 32) | w[i];
+    const uint64_t key = ((uint64_t)i << 32) | words[i];
     a += mix64(key);
     b += mix64(key ^ 0xD6E8FEB86659FD93ull);
   }
@@ -288,7 +288,18 @@ __global__ void digest_kernel(const uint32_t* __restrict__ w, int64_t n, unsigne
     a += __shfl_xor_sync(0xffffffffu, a, o);
     b += __shfl_xor_sync(0xffffffffu, b, o);
   }
+  __shared__ unsigned long long red[2][32];  // per-warp partials, one atomic pair per block
+  const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    red[0][w] = a;
+    red[1][w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+      a += red[0][i];
+      b += red[1][i];
+    }
     atomicAdd(out, (unsigned long long)a);
     atomicAdd(out + 1, (unsigned long long)b);
   }

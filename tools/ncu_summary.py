@@ -13,6 +13,11 @@ METRICS = [
     ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
      "tensor pipe active % (of elapsed)"),
     ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor memory (TMEM) active %"),
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed", "TC (tcgen05 UTC) pipe active %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (sm__pipe_tensor)"),
+    ("sm__sass_inst_executed_op_utcmma.sum", "UTC*MMA instructions"),
+    ("sm__inst_executed_pipe_tc.sum", "tc-pipe instructions"),
+    ("sm__cycles_elapsed.max", "cycles elapsed (max SM)"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("dram__bytes_read.sum", "DRAM read"),
