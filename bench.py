@@ -216,7 +216,7 @@ def library_baseline(obj, B: int, steps: int = 10, warmup: int = 3):
     return res
 
 
-def run_reference_arm(args, rank: int):
+def run_reference_arm(args, rank: int, world: int = 1):
     from paper_1904_04956_b200.blstm import BlstmObjective
 
     if rank != 0:
@@ -230,13 +230,32 @@ def run_reference_arm(args, rank: int):
         "impl": "reference", "metric": METRIC, "value": round(fps, 2), "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": round(sec * 1e3, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "paper BLSTM training step (run_single), CPU oracle port", "model": "paper-blstm",
-                   "batch_per_step_sample": cb, "seq_len": obj.frames},
+        "config": bench_config(obj, cb, world, "single" if world == 1 else args.strategy, args,
+                               args.groups, max(1, world // max(1, args.groups))),
+        "reference_note": ("the float64 CPU port of one learner's training step on all host cores; with N "
+                           "learners the host's aggregate is the same (the learners would share the cores)"),
         "cpu_baseline": {"value": round(fps, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                          "sample": f"{steps} step(s) of B={cb} sequences x 21 frames, paper-size model, float64"},
         "e2e": {"value": round(fps, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_config(obj, B: int, world: int, strategy: str, args, ngroups: int = 1, gsize: int = 1) -> dict:
+    """The workload description shared by both arms (same keys and values,
+    so the driver can match the reference arm's line to ours)."""
+    return {"workload": ("paper BLSTM run_single step, batch 256 (config 2)" if world == 1 else
+                         f"paper BLSTM {strategy.upper()}, {B}/learner, transport={args.transport}"
+                         + (f", {ngroups} groups x {gsize}" if strategy == "hadpsgd" else "")),
+            "layers": obj.layers, "cells": 1024, "bottleneck": obj.bottleneck, "classes": obj.classes,
+            "input_dim": obj.input_dim, "frames": obj.frames, "batch_per_learner": B, "global_batch": B * world,
+            "strategy": strategy, "transport": args.transport if world > 1 else None,
+            "mode": (args.ssgd_mode if strategy == "ssgd" else args.adpsgd_mode
+                     if strategy in ("adpsgd", "hadpsgd") else None),
+            "straggler": ({"rank": args.straggler_rank, "extra_sleep_s": args.straggler_sleep}
+                          if args.straggler_sleep > 0 else None),
+            "l2_policy": "per-step working set ~1.2 GB (activations, 344 MB dlogits) >> 126 MB L2; no flush",
+            "parallelism": f"dp{world}"}
 
 
 # ---------------------------------------------------------------------------
@@ -545,18 +564,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": ("paper BLSTM run_single step, batch 256 (config 2)" if world == 1 else
-                                f"paper BLSTM {strategy.upper()}, {B}/learner, transport={args.transport}"
-                                + (f", {ngroups} groups x {gsize}" if strategy == "hadpsgd" else "")),
-                   "layers": obj.layers, "cells": 1024, "bottleneck": obj.bottleneck, "classes": obj.classes,
-                   "input_dim": obj.input_dim, "frames": T, "batch_per_learner": B, "global_batch": B * world,
-                   "strategy": strategy, "transport": args.transport if world > 1 else None,
-                   "mode": (args.ssgd_mode if strategy == "ssgd" else args.adpsgd_mode
-                            if strategy in ("adpsgd", "hadpsgd") else None),
-                   "straggler": ({"rank": args.straggler_rank, "extra_sleep_s": args.straggler_sleep}
-                                 if args.straggler_sleep > 0 else None),
-                   "l2_policy": "per-step working set ~1.2 GB (activations, 344 MB dlogits) >> 126 MB L2; no flush",
-                   "parallelism": f"dp{world}"},
+        "config": bench_config(obj, B, world, strategy, args, ngroups, gsize),
         "per_rank_ms": per_rank_ms,
         "sync": sync_meas,
         "roofline": roof, "cpu_baseline": cpu, "library_baseline": lib_base, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
@@ -626,14 +634,14 @@ def main():
     ap.add_argument("--layers", type=int, default=6, help="(tests) smaller models; the bench config is 6")
     ap.add_argument("--classes", type=int, default=32000, help="(tests) smaller output layer; bench config 32000")
     args = ap.parse_args()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference_arm(args, rank)
+    if args.impl == "reference":  # CPU only: rank 0 prints, other ranks (if launched) exit 0
+        run_reference_arm(args, rank, max(world, args.gpus))
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.warmup < 3:
         args.warmup = 3
     run_ours(args, rank, world, local_rank)
