@@ -305,7 +305,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         group = PeerGroup(L, rank, world)
         if strategy == "ssgd" and args.ssgd_mode == "overlap":
             group.attach_fused_ssgd()
-    from paper_1904_04956_b200.p2p import adpsgd_partner, hadpsgd_layout
+    from paper_1904_04956_b200.p2p import adpsgd_partner
 
     ngroups = args.groups if strategy == "hadpsgd" else 1
     gsize = world // max(1, ngroups)
@@ -321,15 +321,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             L.theta.add_(peer_buf).mul_(0.5)
         L.snapshot()
 
-    from paper_1904_04956_b200.schedule import SENDER, Topology
+    from paper_1904_04956_b200.distributed import step_plan
 
-    if strategy == "hadpsgd":
-        gid, mi = hadpsgd_layout(rank, ngroups, gsize)
-        members = list(range(gid * gsize, (gid + 1) * gsize))
-        is_sender = Topology(ngroups).role(gid + 1) == SENDER
-    else:
-        gid, mi, members = rank, 0, None
-        is_sender = strategy == "adpsgd" and Topology(world).role(rank + 1) == SENDER
+    plan1 = step_plan(strategy, rank, world, 1, ngroups)
+    members, is_sender = list(plan1.members), plan1.initiates
     straggle = args.straggler_sleep if rank == args.straggler_rank else 0.0
 
     def step(k: int, host: bool = False):
@@ -372,22 +367,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             return
         grad()
         # asynchronous ADPSGD / H-ADPSGD (engines/adpsgd.py:115-288): senders initiate
-        if strategy == "adpsgd":
-            peer = adpsgd_partner(rank, world, k + 1)
-        else:
-            peer = adpsgd_partner(gid, ngroups, k + 1) * gsize + mi
-        if is_sender:
+        plan = step_plan(strategy, rank, world, k + 1, ngroups)
+        if plan.initiates:
             group.ack_gate()  # the previous exchange was acknowledged
             if strategy == "hadpsgd":
-                group.ssgd_step(lr, members=members)
+                group.ssgd_step(lr, members=list(plan.members))
             elif args.adpsgd_mode == "fused":
-                group.update_exchange_async(peer, lr)
+                group.update_exchange_async(plan.partner, lr)
                 return
             else:
                 L.sgd_step(lr)
-            group.exchange_async(peer)
+            group.exchange_async(plan.partner)
         elif strategy == "hadpsgd":
-            group.ssgd_step(lr, members=members, locked=True)
+            group.ssgd_step(lr, members=list(plan.members), locked=plan.locked)
         else:
             group.locked_update(lr)
 

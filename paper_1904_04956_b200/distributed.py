@@ -1,26 +1,21 @@
-"""Multi-process (one process per GPU, torchrun) data-parallel plumbing.
+"""Host-side plan of the one-process-per-GPU strategies (each rank is one
+learner; bench.py and p2p.PeerGroup execute it).
 
-Each rank is one learner.  The batch sharding is the reference's
-static_partition (engines/ssgd.py:16-25): rank r takes batches k*world + r of
-the epoch pool, so a multi-process SSGD epoch consumes exactly the batches
-the reference's SSGD learners would.  The gradient exchange uses
-torch.distributed (NCCL on GPUs, gloo on CPU) — the comparison transport of
-the north star; the single-process multi-device path uses the fused
-canonical-order reduce kernel (ds_group_reduce) instead.
+* Batch sharding: rank r takes batches k*world + r of the epoch pool — the
+  reference's static_partition (engines/ssgd.py:16-25) — so a multi-process
+  SSGD epoch consumes exactly the batches the reference's SSGD learners would.
+* Per-iteration roles: `step_plan` says what rank r does at its k-th update
+  under each strategy — who initiates an ADPSGD exchange and with whom
+  (Topology, engines/common.py:38-75), which group an H-ADPSGD member
+  synchronises with, whether its update must hold its own
+  weight lock (the receiver's atomic region, engines/adpsgd.py:280-285).
 """
 
 from __future__ import annotations
 
-import os
+from dataclasses import dataclass
 
-import numpy as np
-
-from .schedule import epoch_minibatches, learning_rate, static_partition
-
-
-def env_rank_world() -> tuple[int, int, int]:
-    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
-            int(os.environ.get("LOCAL_RANK", "0")))
+from .schedule import SENDER, Topology, epoch_minibatches, static_partition
 
 
 def rank_batches(train_indices, batch_size: int, seed: int, epoch: int, rank: int, world: int) -> list:
@@ -31,25 +26,62 @@ def rank_batches(train_indices, batch_size: int, seed: int, epoch: int, rank: in
     return static_partition(pool, world)[rank]
 
 
-def allreduce_mean_(t, world: int, group=None) -> None:
-    """In-place mean of a gradient tensor over the process group
-    (engines/ssgd.py:85: allreduce / learners)."""
-    import torch.distributed as dist
+@dataclass(frozen=True)
+class StepPlan:
+    """What one rank does at one update.
 
-    if world > 1:
-        dist.all_reduce(t, group=group)
-        t.div_(world)
+    members     ranks of its synchronous group (SSGD: everyone; H-ADPSGD: its
+                group; ADPSGD: itself)
+    initiates   it starts a pairwise exchange after its update (a sender)
+    partner     the rank it exchanges with this iteration (None: none)
+    locked      its own update (or group step) holds its weight lock, because
+                exchanges from other learners may land concurrently
+    """
 
-
-def ssgd_lr(schedule, epoch: int, k: int, q: int) -> float:
-    """Learning rate of local iteration k of q (engines/ssgd.py:86)."""
-    return learning_rate(schedule, epoch, k, q)
-
-
-def shard_sizes(n_train: int, batch_size: int, world: int) -> list[int]:
-    """Per-rank batch counts of one epoch (all equal: q = len(pool) // world)."""
-    n_batches = -(-n_train // batch_size)
-    return [n_batches // world] * world
+    members: tuple
+    initiates: bool
+    partner: int | None
+    locked: bool
 
 
-__all__ = ["env_rank_world", "rank_batches", "allreduce_mean_", "ssgd_lr", "shard_sizes", "np"]
+def step_plan(strategy: str, rank: int, world: int, k: int, groups: int = 2) -> StepPlan:
+    """Plan of rank `rank` (0-based) at its k-th update (1-based iteration
+    count, as Topology.partner uses it, engines/adpsgd.py:147-149)."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside 0..{world - 1}")
+    if k < 1:
+        raise ValueError("iterations are 1-based")
+    if strategy in ("single", "ssgd", "hybrid"):
+        return StepPlan(tuple(range(world)), False, None, False)
+    if strategy == "adpsgd":
+        if world < 2 or world % 2:
+            raise ValueError("adpsgd needs an even number of learners >= 2")
+        topo = Topology(world)
+        me = rank + 1
+        if topo.role(me) == SENDER:
+            return StepPlan((rank,), True, topo.partner(me, k) - 1, False)
+        return StepPlan((rank,), False, None, True)
+    if strategy == "hadpsgd":
+        if groups < 2 or groups % 2 or world % groups:
+            raise ValueError("hadpsgd needs an even group count dividing the learner count")
+        size = world // groups
+        gid, member = divmod(rank, size)
+        topo = Topology(groups)
+        mem = tuple(range(gid * size, (gid + 1) * size))
+        if topo.role(gid + 1) == SENDER:
+            return StepPlan(mem, True, (topo.partner(gid + 1, k) - 1) * size + member, False)
+        return StepPlan(mem, False, None, True)
+    raise ValueError(f"unknown strategy {strategy!r}")
+
+
+def exchanges_at(strategy: str, world: int, k: int, groups: int = 2) -> list:
+    """All (initiator, partner) pairs of iteration k (the edges in flight)."""
+    out = []
+    for r in range(world):
+        p = step_plan(strategy, r, world, k, groups)
+        if p.initiates:
+            out.append((r, p.partner))
+    return out
+
+
+__all__ = ["rank_batches", "StepPlan", "step_plan", "exchanges_at"]

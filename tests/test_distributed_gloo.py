@@ -1,6 +1,11 @@
-"""world_size-2 multi-process path on CPU (gloo): each rank takes its
-static_partition shard and the averaged update is identical on both ranks
-and equal to the single-process SSGD restatement."""
+"""The one-process-per-GPU host plan (paper_1904_04956_b200/distributed.py)
+across a real world-4 process group (gloo on CPU): every rank computes its
+own batches and per-iteration roles; gathered, they must form the
+reference's schedule — SSGD shards disjoint and covering the truncated pool
+(static_partition, engines/ssgd.py:16-25); ADPSGD exchanges a matching of
+senders onto receivers with the Topology partners (engines/common.py:38-75),
+receivers locked; H-ADPSGD groups partitioning the ranks with member r of
+partner groups paired."""
 
 import os
 import socket
@@ -24,35 +29,51 @@ def _free_port():
 def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1904_04956_b200.distributed import allreduce_mean_, rank_batches
-    from paper_1904_04956_b200.schedule import baseline_schedule, learning_rate
+    from paper_1904_04956_b200.distributed import rank_batches, step_plan
 
-    rng = np.random.default_rng(0)
-    X = rng.standard_normal((100, 4))
-    w = torch.zeros(4, dtype=torch.float64)
-    v = torch.zeros(4, dtype=torch.float64)
-    sched = baseline_schedule(0.1, total_epochs=2)
-    mine = rank_batches(np.arange(90), 16, 3, 1, rank, world)
-    for k, b in enumerate(mine):
-        g = torch.from_numpy(X[b].mean(0)) + w  # grad of 0.5||w||^2 - mean(x).w ... any deterministic fn
-        allreduce_mean_(g, world)
-        lr = learning_rate(sched, 1, k, len(mine))
-        v.mul_(0.9).add_(g)
-        w = w - lr * v
-    out[rank] = (w.numpy().copy(), [b.tolist() for b in mine])
+    mine = {"batches": [b.tolist() for b in rank_batches(np.arange(1000), 32, 3, 2, rank, world)],
+            "adpsgd": [step_plan("adpsgd", rank, world, k) for k in range(1, 9)],
+            "hadpsgd": [step_plan("hadpsgd", rank, world, k, groups=2) for k in range(1, 9)],
+            "ssgd": step_plan("ssgd", rank, world, 1)}
+    got = [None] * world
+    dist.all_gather_object(got, mine)
+    if rank == 0:
+        out["plans"] = got
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_gloo_world2_ssgd_step():
-    from paper_1904_04956_b200.schedule import epoch_minibatches, static_partition
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_world_host_plan(world):
+    from paper_1904_04956_b200.schedule import SENDER, Topology, epoch_minibatches
 
-    port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
-    w0, b0 = out[0]
-    w1, b1 = out[1]
-    assert np.array_equal(w0, w1)  # replicas identical after every step
-    parts = static_partition(epoch_minibatches(np.arange(90), 16, 3, 1), 2)
-    assert b0 == [b.tolist() for b in parts[0]] and b1 == [b.tolist() for b in parts[1]]
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    plans = out["plans"]
+    # SSGD: shards disjoint, covering the pool truncated to q*world, in static_partition order
+    pool = epoch_minibatches(np.arange(1000), 32, 3, 2)
+    q = len(pool) // world
+    for r in range(world):
+        assert plans[r]["batches"] == [pool[k * world + r].tolist() for k in range(q)]
+        assert plans[r]["ssgd"].members == tuple(range(world)) and not plans[r]["ssgd"].initiates
+    # ADPSGD: senders (odd ids) initiate to their Topology partner; receivers locked; a matching per step
+    topo = Topology(world)
+    for k in range(8):
+        edges = [(r, plans[r]["adpsgd"][k].partner) for r in range(world) if plans[r]["adpsgd"][k].initiates]
+        assert [r + 1 for r, _ in edges] == topo.senders()
+        assert all(p + 1 == topo.partner(r + 1, k + 1) for r, p in edges)
+        assert len({p for _, p in edges}) == len(edges)  # each receiver mixes with one sender at a time
+        for r in range(world):
+            assert plans[r]["adpsgd"][k].locked == (topo.role(r + 1) != SENDER)
+    # H-ADPSGD (2 groups): groups partition the ranks; member r of the sender group pairs member r of the other
+    size = world // 2
+    for k in range(8):
+        groups = {plans[r]["hadpsgd"][k].members for r in range(world)}
+        assert sorted(x for g in groups for x in g) == list(range(world)) and len(groups) == 2
+        for r in range(world):
+            p = plans[r]["hadpsgd"][k]
+            if p.initiates:
+                assert r < size and p.partner == size + r and not p.locked
+            else:
+                assert r >= size and p.locked and p.partner is None
