@@ -823,24 +823,71 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
 // clusters of 4 (cluster placement leaves some SMs unusable: keep <= 128)
 // <= 128 CTAs per launch: forward 32 CTAs per 64-row batch block, backward
 // 64 CTAs per 128-row batch tile in clusters of 4
-int lstm_max_tiles() { return (num_sms() >= 132 ? 128 : num_sms()) / 64; }
-static int lstm_bwd_max_tiles() { return lstm_max_tiles(); }
+//
+// The recurrent grids synchronise through flags, so every CTA of a launch
+// must be co-resident.  The per-launch batch is capped by what the device
+// can actually co-schedule in clusters of 2 (forward) / 4 (backward) at the
+// kernels' shared-memory size (cudaOccupancyMaxActiveClusters on an idle
+// device), not just by the SM count: cluster placement inside GPCs leaves
+// SMs unusable.  A larger batch runs as several launches.
+struct RecCaps {
+  int fwd_ctas = 0, bwd_ctas = 0;  // co-resident CTAs in recurrent-kernel clusters
+  int err = 0;
+};
+static int cluster_cap(const void* fn, size_t smem, int cluster) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster * 64);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cluster;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return n * cluster;
+}
+static const RecCaps& rec_caps() {
+  static RecCaps caps;
+  static bool done = false;
+  if (!done) {
+    done = true;
+    if (cudaFuncSetAttribute(lstm_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd2::kSmem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmem) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      caps.err = 1;
+      return caps;
+    }
+    const int sm = num_sms() >= 132 ? 128 : num_sms();
+    const int f = cluster_cap((const void*)lstm_fwd2_kernel, fwd2::kSmem, 2);
+    const int b = cluster_cap((const void*)lstm_bwd_kernel, bwd::kSmem, 4);
+    caps.fwd_ctas = f < 0 ? sm : (f < sm ? f : sm);
+    caps.bwd_ctas = b < 0 ? sm : (b < sm ? b : sm);
+  }
+  return caps;
+}
+int lstm_max_tiles() {
+  const RecCaps& c = rec_caps();
+  const int t = (c.bwd_ctas < c.fwd_ctas ? c.bwd_ctas : c.fwd_ctas) / 64;
+  return t > 0 ? t : 0;
+}
+static int lstm_bwd_max_tiles() { return rec_caps().bwd_ctas / 64; }
 int lstm_counter_words(int B) { return kFlagWords128 * ((B + 127) / 128); }
 
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    DS_CUDA_TRY(
-        cudaFuncSetAttribute(lstm_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd2::kSmem));
-    DS_CUDA_TRY(
-        cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmem));
-
-    attr_set = true;
-  }
+  if (rec_caps().err) return fail_arg("recurrent kernels: cannot set the shared-memory attribute");
   const int B = a.B, T = a.T;
   if (fwd) {
     // 32 CTAs (2 directions x 8 pairs x 2) per 64-row batch block
-    const int max_blocks = num_sms() / (2 * fwd2::kCtas);
+    const int max_blocks = rec_caps().fwd_ctas / (2 * fwd2::kCtas);
     if (max_blocks < 1) return fail_arg("device too small for the recurrent kernel");
     LstmParams P;
     memset(&P, 0, sizeof(P));
