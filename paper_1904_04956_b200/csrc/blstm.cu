@@ -4,6 +4,7 @@
 // include/ds_blstm.h.
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "../../include/ds_blstm.h"
@@ -47,6 +48,7 @@ struct ds_blstm {
   __nv_bfloat16* dz = nullptr;
   __nv_bfloat16* dy = nullptr;
   __nv_bfloat16* dg = nullptr;
+  __nv_bfloat16* dg2 = nullptr;  // dG of odd layers while dW of the layer above still reads dg
   float* colpart = nullptr;
   float* biaspart = nullptr;  // fused bias-gradient partials (CE grad epilogue / BPTT kernel)
   float* splitk = nullptr;    // split-K fp32 partials of dZ
@@ -61,6 +63,10 @@ struct ds_blstm {
   // per-layer bias-gradient row sums beside the layer's weight-gradient GEMMs
   cudaStream_t side2 = nullptr;
   cudaEvent_t ev_rs[kMaxLayers][2] = {};
+  // weight-gradient GEMMs of layer l beside BPTT_{l-1} (narrow BPTT only): low-priority stream
+  cudaStream_t side3 = nullptr;
+  cudaEvent_t ev_dw[kMaxLayers][2] = {};  // [0] BPTT_l done, [1] dW_l done
+  int prio_hi = 0, prio_lo = 0;
   // graph cache
   struct Key {
     int B;
@@ -86,6 +92,10 @@ struct ds_blstm {
   std::vector<Entry> graphs;
   // phase profiling (tests / bench only; bypasses the graph)
   int profile = 0;
+  // debug timeline (DS_TIMELINE=1): timing events recorded inside the step graph on every stream
+  unsigned long long* tl_buf = nullptr;  // device globaltimer stamps (graph-safe, unlike event timing)
+  std::vector<std::string> tl_name;
+  int tl_n = 0;
   std::vector<cudaEvent_t> ev;
   std::vector<int> ev_kind;
   int launches = 0;  // kernel launches issued by the last step
@@ -147,6 +157,7 @@ bool fused_ce_dz(const ds_blstm* h) {
 }
 // the soft-max combine's last-block ticket: a word of the zeroed slack after the recurrent flags
 unsigned* ce_ticket(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax); }
+uint32_t* seq_words(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax) + 32; }
 int fused_dz_splits(const ds_blstm* h, int N) {
   // h->splitk holds kDzPartMax x N x bottleneck floats
   return ce_grad_dz_splits(N, h->L.classes, kDzPartMax);
@@ -192,6 +203,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   h->dz = a.take<__nv_bfloat16>(base, (size_t)N * L.bottleneck);
   h->dy = a.take<__nv_bfloat16>(base, (size_t)N * kLayerOut);
   h->dg = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
+  h->dg2 = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
   {  // bottleneck bias colsum partials / CE loss partials
     const int64_t c1 = op_colsum_scratch(N, L.bottleneck), c2 = (N + 31) / 32 + 64;
     h->colpart = a.take<float>(base, c1 > c2 ? c1 : c2);
@@ -226,6 +238,29 @@ int validate_cfg(const ds_blstm_cfg* c) {
 // phase kinds for profiling
 enum { PH_GEMM = 0, PH_LSTM_FWD = 1, PH_LSTM_BWD = 2, PH_OTHER = 3, PH_END = 4 };
 
+bool use_timeline() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_TIMELINE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+__global__ void tl_stamp_kernel(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+int tl_mark(ds_blstm* h, const std::string& name, cudaStream_t s) {
+  if (!use_timeline()) return DS_OK;
+  if (!h->tl_buf || h->tl_n >= 256) return DS_OK;
+  if (h->tl_n >= (int)h->tl_name.size()) h->tl_name.push_back(name);
+  h->tl_name[h->tl_n] = name;
+  tl_stamp_kernel<<<1, 1, 0, s>>>(h->tl_buf + h->tl_n++);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
 int mark(ds_blstm* h, int kind, cudaStream_t s) {
   if (!h->profile) return DS_OK;
   cudaEvent_t e;
@@ -255,6 +290,23 @@ int group_segment(ds_blstm* h, SgdCtx& c, int64_t off, int64_t n, cudaStream_t s
   if (!rc) rc = group_barrier(*c.grp, s);
   return rc;
 }
+bool use_dw_overlap() {  // DS_DW_OVERLAP=0: weight gradients after each BPTT on the main stream
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_DW_OVERLAP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+int dw_pair_margin() {  // CTA pairs kept free beside the BPTT for the side-stream SGD (DS_DW_MARGIN)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_DW_MARGIN");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 int sgd_segment(ds_blstm* h, SgdCtx& c, float* grad, int* flag, int64_t off, int64_t n, bool side, cudaStream_t s) {
   if (!c.theta) return DS_OK;
   if (c.grp) {
@@ -274,6 +326,7 @@ int sgd_segment(ds_blstm* h, SgdCtx& c, float* grad, int* flag, int64_t off, int
   DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork[k], 0));
   int rc = op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, 16, h->side);
   if (rc) return rc;
+  if ((rc = tl_mark(h, "sgd" + std::to_string(k), h->side))) return rc;
   DS_CUDA_TRY(cudaEventRecord(h->ev_join[k], h->side));
   return DS_OK;
 }
@@ -294,9 +347,13 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     if ((rc = (x))) return rc; \
   } while (0)
 #define MARK(k) TRY(mark(h, k, s))
+#define TL(name, st) TRY(tl_mark(h, name, st))
   int& nl = h->launches;
   nl = 0;
+  h->tl_n = 0;
+  TL("start", s);
   bool aux_join = false;
+  bool out_side_done = false;  // ev_dw[0][1] recorded: the output-layer weight gradients ran beside BPTT_{L-1}
 
   MARK(PH_OTHER);
   TRY(op_gather(idx, B, T, h->feats, h->labels, h->n_seq, h->x0, h->lab, flag, s));
@@ -320,11 +377,13 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     TRY(gemm_bf16_output(&p));
     MARK(PH_GEMM);
     TRY(gemm_launch(&gb, s));
+    TL("proj" + std::to_string(l), s);
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], nullptr, nullptr,
                      h->counters};
     la.err = flag;
     MARK(PH_LSTM_FWD);
     TRY(lstm_forward(la, s));
+    TL("fwd" + std::to_string(l), s);
     nl += 2 + (B - 1) / (128 * lstm_max_tiles());
   }
   {
@@ -381,10 +440,18 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
                       ce_ticket(h), loss, flag, s));
     nl += 3;  // gather, ce stats gemm, combine
   }
+  TL("ce", s);
   if (!grad) {
     MARK(PH_END);
     return DS_OK;
   }
+  // Weight gradients beside the recurrence (narrow 64-CTA BPTT only): dW_o / dW_b beside BPTT_{L-1},
+  // layer l's dW_ih / dW_hh beside BPTT_{l-1}, on a low-priority stream, each gated on the BPTT's
+  // start and capped to the SMs it leaves free; only dY / dX stay between two BPTTs.
+  const int narrow = lstm_bwd_narrow_ctas(B);
+  const bool ovl = narrow > 0 && !h->profile && use_dw_overlap();
+  int dw_pairs = (num_sms() - narrow) / 2 - dw_pair_margin();
+  if (dw_pairs < 1) dw_pairs = 1;
 
   // ---- backward ----
   GemmProblem pwo;  // fused path: dW_o joins the dW_b / dY launch below
@@ -495,6 +562,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     const int q0 = have_wo ? 1 : 0;
     if (have_wo) gb.p[0] = pwo;
     gb.nprob = q0 + 2;
+    const bool out_side = ovl && have_wo;  // dW_o + dW_b beside BPTT_{L-1}, dY alone here
     GemmProblem& p0 = gb.p[q0];  // dW_b = dZ^T Y (alone: split-K fp32 partials, reduced below in split order)
     TRY(gemm_problem(&p0, h->dz, bott, 1, Y(Lh - 1), kLayerOut, 1, bott, kLayerOut, N));
     p0.epi = EPI_F32;
@@ -510,7 +578,28 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     p1.ldo = kLayerOut;
     TRY(gemm_bf16_output(&p1));
     MARK(PH_GEMM);
-    TRY(gemm_launch(&gb, s));
+    if (out_side) {
+      GemmBatch gy;
+      memset(&gy, 0, sizeof(gy));
+      gy.nprob = 1;
+      gy.p[0] = p1;
+      gy.prio = h->prio_hi;
+      gb.nprob = q0 + 1;
+      // dW_o streams the 344 MB dlogits: beyond ~24 pairs its HBM traffic slows the BPTT it hides behind
+      static const int wo_pairs = getenv("DS_WO_PAIRS") ? atoi(getenv("DS_WO_PAIRS")) : 24;
+      gb.max_pairs = wo_pairs > 0 && wo_pairs < dw_pairs ? wo_pairs : dw_pairs;
+      gb.prio = h->prio_lo;
+      DS_CUDA_TRY(cudaEventRecord(h->ev_aux[3], s));
+      TRY(gemm_launch(&gy, s));
+      TL("dY", s);
+      DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_aux[3], 0));
+      TRY(lstm_wait_started(seq_words(h), 0, flag, h->side3));
+      TRY(gemm_launch(&gb, h->side3));
+      TL("dWo", h->side3);
+      nl += 2;
+    } else {
+      TRY(gemm_launch(&gb, s));
+    }
     MARK(PH_OTHER);
     if (Sb > 1) TRY(op_splitk_f32(h->splitk, Sb, (int64_t)bott * kLayerOut, grad + L.off_wb, s));
     if (aux_join) {  // db_b (column sums of dZ) on the side stream too; the output SGD follows it there
@@ -523,25 +612,41 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     }
     nl += Sb > 1 ? 4 : 3;
     // bottleneck + output layer gradients are final: update them beside BPTT_{L-1}
-    TRY(sgd_segment(h, sg, grad, flag, L.off_wb, L.total - L.off_wb, true, s));
+    TRY(sgd_segment(h, sg, grad, flag, L.off_wb, L.total - L.off_wb, true, out_side ? h->side3 : s));
+    if (out_side) {
+      DS_CUDA_TRY(cudaEventRecord(h->ev_dw[0][1], h->side3));
+      out_side_done = true;
+    }
   }
+  // Weight gradients beside the recurrence: with the narrow (64-CTA) BPTT, layer l's dW_ih / dW_hh
+  // GEMMs run on the SMs BPTT_{l-1} leaves free (low-priority stream, grid capped to those SMs) and
+  // only dX = dG W_ih stays between two BPTTs.  dG alternates between two buffers by layer parity.
   for (int l = Lh - 1; l >= 0; --l) {
+    __nv_bfloat16* dgl = (ovl && (l & 1)) ? h->dg2 : h->dg;
+    if (ovl && l + 2 < Lh) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l + 2][1], 0));  // dW_{l+2} read dgl
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], h->dy,
-                     h->dg, h->counters, nullptr, h->biaspart};
+                     dgl, h->counters, nullptr, h->biaspart};
     la.err = flag;
+    if (ovl) {
+      la.prio = h->prio_hi;
+      la.seq = seq_words(h);
+      la.tag = Lh - 1 - l;
+    }
+    TL("pre-bptt" + std::to_string(l), s);
     MARK(PH_LSTM_BWD);
     TRY(lstm_backward(la, s));
+    TL("bptt" + std::to_string(l), s);
     nl += 1 + (B - 1) / (128 * lstm_max_tiles());
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
     gb.b_early = 1;  // B = X / Y / W_ih (forward pass, snapshot); the predecessor (BPTT l) writes only A = dG
     GemmProblem& p0 = gb.p[0];  // dW_ih = dG^T X
     if (l == 0) {
-      TRY(gemm_problem(&p0, h->dg, kGates2, 1, h->x0, kInPad, 1, kGates2, kInPad, N));
+      TRY(gemm_problem(&p0, dgl, kGates2, 1, h->x0, kInPad, 1, kGates2, kInPad, N));
       p0.n_valid = L.input_dim;
       p0.ldo = L.input_dim;
     } else {
-      TRY(gemm_problem(&p0, h->dg, kGates2, 1, Y(l - 1), kLayerOut, 1, kGates2, kLayerOut, N));
+      TRY(gemm_problem(&p0, dgl, kGates2, 1, Y(l - 1), kLayerOut, 1, kGates2, kLayerOut, N));
       p0.ldo = kLayerOut;
     }
     p0.epi = EPI_F32;
@@ -549,20 +654,24 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     for (int d = 0; d < 2; ++d) {  // dW_hh[dir] = dG_dir^T H_prev_dir
       GemmProblem& p = gb.p[1 + d];
       const __nv_bfloat16* hp = d == 0 ? h->yfull[l] : h->yfull[l] + (size_t)2 * B * kLayerOut + kHidden;
-      TRY(gemm_problem(&p, h->dg + d * kGates, kGates2, 1, hp, kLayerOut, 1, kGates, kHidden, N));
+      TRY(gemm_problem(&p, dgl + d * kGates, kGates2, 1, hp, kLayerOut, 1, kGates, kHidden, N));
       p.epi = EPI_F32;
       p.out = grad + L.off_whh[l] + (size_t)d * kGates * kHidden;
       p.ldo = kHidden;
     }
     gb.nprob = 3;
-    if (l > 0) {  // dY_{l-1} = dG W_ih
-      GemmProblem& p3 = gb.p[3];
-      TRY(gemm_problem(&p3, h->dg, kGates2, 0, h->snap + L.off_wih[l], kLayerOut, 1, N, kLayerOut, kGates2));
+    GemmBatch gx;  // dY_{l-1} = dG W_ih (the critical path)
+    memset(&gx, 0, sizeof(gx));
+    if (l > 0) {
+      GemmBatch& gt = ovl ? gx : gb;
+      GemmProblem& p3 = gt.p[gt.nprob];
+      TRY(gemm_problem(&p3, dgl, kGates2, 0, h->snap + L.off_wih[l], kLayerOut, 1, N, kLayerOut, kGates2));
       p3.epi = EPI_BF16;
       p3.out = h->dy;
       p3.ldo = kLayerOut;
       TRY(gemm_bf16_output(&p3));
-      gb.nprob = 4;
+      ++gt.nprob;
+      gx.b_early = 1;
     }
     // db = row sums of the BPTT's bias partials: off the critical path, beside the GEMMs; joined
     // before the layer's update and before BPTT_{l-1} reuses biaspart
@@ -575,19 +684,45 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     TRY(op_rowsum(h->biaspart, ((B + 127) / 128) * 4, kGates2, grad + L.off_b[l], rs_side ? h->side2 : s));
     if (rs_side) DS_CUDA_TRY(cudaEventRecord(h->ev_rs[l][1], h->side2));
     MARK(PH_GEMM);
+    if (ovl && l > 0) {
+      DS_CUDA_TRY(cudaEventRecord(h->ev_dw[l][0], s));
+      DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_dw[l][0], 0));
+      gb.max_pairs = dw_pairs;
+      gb.prio = h->prio_lo;
+      gb.b_early = 0;  // its stream predecessor is the previous layer's dW, not BPTT_l
+      gx.prio = h->prio_hi;  // dX first: it is the critical path between the two BPTTs
+      // dW_l only once BPTT_{l-1} holds its SMs (dX_l runs alone on the machine first)
+      TRY(lstm_wait_started(seq_words(h), Lh - l, flag, h->side3));
+      TRY(gemm_launch(&gb, h->side3));
+      TL("dW" + std::to_string(l), h->side3);
+      TRY(gemm_launch(&gx, s));
+      TL("dX" + std::to_string(l), s);
+      DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l][1], 0));
+      DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_rs[l][1], 0));
+      DS_CUDA_TRY(cudaEventRecord(h->ev_dw[l][1], h->side3));
+      nl += 3;
+      // layer l's gradients are final once dW_l is: update them beside BPTT_{l-1}
+      TRY(sgd_segment(h, sg, grad, flag, L.off_wih[l], L.off_b[l] + kGates2 - L.off_wih[l], true, h->side3));
+      continue;
+    }
     TRY(gemm_launch(&gb, s));
+    TL("grp" + std::to_string(l), s);
     if (rs_side) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l][1], 0));
     nl += 2;
     // layer l's gradients are final: update them beside BPTT_{l-1} (layer 0 on the critical path)
     TRY(sgd_segment(h, sg, grad, flag, L.off_wih[l], L.off_b[l] + kGates2 - L.off_wih[l], l > 0, s));
   }
+  if (ovl)  // every weight gradient is complete when the step ends (also without an update)
+    for (int l = out_side_done ? 0 : 1; l < Lh; ++l) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l][1], 0));
   if (sg.theta) {
     MARK(PH_OTHER);
     for (int k = 0; k < sg.nfork; ++k) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_join[k], 0));
     TRY(op_snapshot_aux(sg.theta, L, h->wih0pad, h->bias_snap, s));
     nl += L.layers + 2;
   }
+  TL("end", s);
   MARK(PH_END);
+#undef TL
 #undef MARK
 #undef TRY
   return DS_OK;
@@ -648,7 +783,7 @@ int run_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss, i
   }
   if (ce != cudaSuccess) return fail_cuda(ce, "cudaStreamEndCapture");
   cudaGraphExec_t ex;
-  ce = cudaGraphInstantiate(&ex, g, 0);
+  ce = cudaGraphInstantiate(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
   cudaGraphDestroy(g);
   if (ce != cudaSuccess) return fail_cuda(ce, "cudaGraphInstantiate");
   if (h->graphs.size() >= 16) {
@@ -702,6 +837,11 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side2, cudaStreamNonBlocking);
   for (int k = 0; k < kMaxLayers * 2 && e == cudaSuccess; ++k)
     e = cudaEventCreateWithFlags(&h->ev_rs[k / 2][k % 2], cudaEventDisableTiming);
+  if (e == cudaSuccess && use_timeline()) e = cudaMalloc(&h->tl_buf, 256 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&h->prio_lo, &h->prio_hi);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->side3, cudaStreamNonBlocking, h->prio_lo);
+  for (int k = 0; k < kMaxLayers * 2 && e == cudaSuccess; ++k)
+    e = cudaEventCreateWithFlags(&h->ev_dw[k / 2][k % 2], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     cudaFree(h->arena);
     delete h;
@@ -721,9 +861,13 @@ int ds_blstm_destroy(ds_blstm* h) {
   }
   for (int k = 0; k < 4; ++k)
     if (h->ev_aux[k]) cudaEventDestroy(h->ev_aux[k]);
-  for (int k = 0; k < kMaxLayers * 2; ++k)
+  for (int k = 0; k < kMaxLayers * 2; ++k) {
     if (h->ev_rs[k / 2][k % 2]) cudaEventDestroy(h->ev_rs[k / 2][k % 2]);
+    if (h->ev_dw[k / 2][k % 2]) cudaEventDestroy(h->ev_dw[k / 2][k % 2]);
+  }
   if (h->side2) cudaStreamDestroy(h->side2);
+  if (h->side3) cudaStreamDestroy(h->side3);
+  if (h->tl_buf) cudaFree(h->tl_buf);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->loss_pinned) cudaFreeHost(h->loss_pinned);
   parity_destroy(h->par);
@@ -950,6 +1094,19 @@ int ds_blstm_profile_list(ds_blstm* h, float* ms, int32_t* kinds, int32_t max_n,
     kinds[n] = h->ev_kind[i];
   }
   *n_out = n;
+  return DS_OK;
+}
+
+// debug: "name ms" lines of the last step's timeline (DS_TIMELINE=1), relative to its start
+int ds_debug_timeline(ds_blstm* h, char* buf, int32_t len) {
+  if (!h || !buf || len < 1) return fail_arg("ds_debug_timeline: bad arguments");
+  DS_CUDA_TRY(cudaDeviceSynchronize());
+  std::string out;
+  std::vector<unsigned long long> t(h->tl_n > 0 ? h->tl_n : 1);
+  if (h->tl_n > 0)
+    DS_CUDA_TRY(cudaMemcpy(t.data(), h->tl_buf, sizeof(unsigned long long) * h->tl_n, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < h->tl_n; ++i) out += h->tl_name[i] + " " + std::to_string((double)(t[i] - t[0]) * 1e-6) + "\n";
+  snprintf(buf, (size_t)len, "%s", out.c_str());
   return DS_OK;
 }
 

@@ -109,6 +109,9 @@ struct GemmBatch {
   int sched;                            // 1: use order/pstart
   int b_early;                          // B of every problem is not written by the predecessor kernel:
                                         // prefetch it before griddep_wait (PDL)
+  int max_pairs;                        // > 0: at most this many CTA pairs (a GEMM running beside a
+                                        // recurrent kernel on the SMs it leaves free)
+  int prio;                             // != 0: launch priority (cudaLaunchAttributePriority)
   uint16_t pstart[kMaxPairs + 1];       // pair p runs order[pstart[p] .. pstart[p+1])
   uint16_t order[kMaxSched];
   // debug: per-CTA per-tile timeline (tools/gemm_trace.py), null in production

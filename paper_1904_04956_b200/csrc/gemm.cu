@@ -693,7 +693,8 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   }
   b->total_tiles = total;
   if (total == 0) return DS_OK;
-  const int max_pairs = num_sms() / 2 < kMaxPairs ? num_sms() / 2 : kMaxPairs;
+  int max_pairs = num_sms() / 2 < kMaxPairs ? num_sms() / 2 : kMaxPairs;
+  if (b->max_pairs > 0 && b->max_pairs < max_pairs) max_pairs = b->max_pairs;
   const int pairs = total < max_pairs ? total : max_pairs;
   schedule_tiles(b, pairs);
   cudaLaunchConfig_t cfg = {};
@@ -701,15 +702,25 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[3];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = 2;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (use_pdl()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (b->prio) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na].val.priority = b->prio;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = use_pdl() ? 2 : 1;
+  cfg.numAttrs = na;
   DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_kernel, *b));
   return DS_OK;
 }

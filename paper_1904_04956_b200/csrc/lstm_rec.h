@@ -10,6 +10,7 @@ namespace ds {
 struct LstmParams {
   CUtensorMap tmA;  // forward: Y_full; backward: dG
   CUtensorMap tmW;  // W_hh [4096, 512] bf16 (forward: K-major B; backward: MN-major B)
+  CUtensorMap tmG, tmC, tmDY;  // transposed BPTT: per-step cell inputs (gates, c_{t-1}, dY) staged by TMA
   __nv_bfloat16* gates;
   float* cstate;
   __nv_bfloat16* y;
@@ -22,6 +23,8 @@ struct LstmParams {
   int variant;  // debug: bit0 skip writer proxy fence, bit1 skip release fence
   float xscale; // BPTT: fp16 scale of the exchanged partial dh (power of two)
   int* err;     // optional: |= 8 when a flag wait times out (a peer CTA never published)
+  uint32_t* seq;  // transposed BPTT: [0] step epoch, [1] last started launch (epoch*16 + tag)
+  int tag;        // position of this backward launch in the step (0 = first: bumps the epoch)
 };
 
 struct LstmLayerArgs {
@@ -36,9 +39,18 @@ struct LstmLayerArgs {
   uint64_t* trace = nullptr;
   float* dbpart = nullptr;  // backward: per-(batch tile, lane quadrant) column sums of dG
   int* err = nullptr;       // step error flag: |= 8 on a flag-wait timeout
+  int prio = 0;             // != 0: launch priority (ahead of GEMMs issued beside the recurrence)
+  uint32_t* seq = nullptr;  // start signal for GEMMs gated on this launch (lstm_wait_started)
+  int tag = 0;
 };
+// Block `stream` until the backward launch with `tag` of the current step has started (its grid is
+// placed), so a GEMM issued next on `stream` only takes the SMs the recurrence left free.
+int lstm_wait_started(uint32_t* seq, int tag, int* err, cudaStream_t stream);
 
 int lstm_max_tiles();
+// CTAs of the first backward launch for a batch of B (the SMs a concurrent GEMM must leave free),
+// 0 when the backward kernel is the 128-CTA split-K variant (nothing to overlap)
+int lstm_bwd_narrow_ctas(int B);
 int lstm_counter_words(int B);
 int lstm_forward(const LstmLayerArgs& a, cudaStream_t stream);
 int lstm_backward(const LstmLayerArgs& a, cudaStream_t stream);
