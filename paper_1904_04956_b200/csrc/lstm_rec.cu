@@ -1056,6 +1056,13 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
     const bool issuer = (cg & 1) == 0;                            // copies the (q, half) block
     const uint32_t pbar = 4 + q * 2 + half;                       // named barrier of the two warps of a block
     const bool kEpiLead = threadIdx.x == 0;
+    uint32_t okmask = 0;  // my rows inside the batch and this launch
+#pragma unroll
+    for (int i = 0; i < kCellRows; ++i)
+      okmask |= (row0 + i + btile * kRows < P.nb && brow0 + row0 + i < B ? 1u : 0u) << i;
+    const uint32_t cg_in = smem_u32(in_g) + row0 * 256 + lane * 8;  // staged inputs of my (unit, first row)
+    const uint32_t cc_in = smem_u32(in_c) + row0 * 128 + lane * 4;
+    const uint32_t cdy_in = smem_u32(in_dy) + row0 * 64 + lane * 2;
     float dcc[kCellRows], cc[kCellRows], db[4];  // cc: c_t of my rows (c_{t-1} becomes the next step's c_t)
 #pragma unroll
     for (int i = 0; i < kCellRows; ++i) dcc[i] = 0.f;
@@ -1154,16 +1161,15 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
       mbar_wait(inbar, (uint32_t)s & 1);
       if (P.trace && blockIdx.x == 0 && threadIdx.x == 0)
         P.trace[(size_t)gridDim.x * T * kTraceSlots + (size_t)T * 18 + 2 * s + 1] = globaltimer();
+      uint2* dgp = reinterpret_cast<uint2*>(P.dg + ((size_t)t * B + brow0 + row0) * (8 * kH) + col_g);
 #pragma unroll
       for (int i = 0; i < kCellRows; ++i) {
-        const int rw = row0 + i, b = brow0 + rw;
-        const bool ok = rw + btile * kRows < P.nb && b < B;
-        const uint2 actw = *reinterpret_cast<const uint2*>(in_g + rw * 256 + lane * 8);
-        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&actw);
-        const float2 a01 = __bfloat1622float2(a2[0]), a23 = __bfloat1622float2(a2[1]);
-        const float ig = a01.x, fg = a01.y, gg = a23.x, og = a23.y;
-        const float dyv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(in_dy + rw * 64 + lane * 2));
-        const float cpv = has_cprev ? *reinterpret_cast<const float*>(in_c + rw * 128 + lane * 4) : 0.f;
+        const bool ok = (okmask >> i) & 1u;
+        const uint2 actw = ld_shared_v2(cg_in + i * 256);
+        const float ig = __uint_as_float(actw.x << 16), fg = __uint_as_float(actw.x & 0xffff0000u);
+        const float gg = __uint_as_float(actw.y << 16), og = __uint_as_float(actw.y & 0xffff0000u);
+        const float dyv = __uint_as_float(ld_shared_u16(cdy_in + i * 64) << 16);
+        const float cpv = has_cprev ? ld_shared_f32(cc_in + i * 128) : 0.f;
         const float dht = dh[i] + dyv;
         const float tcn = tanh_fast(cc[i]);
         const float dct = fmaf(dht * og, 1.f - tcn * tcn, dcc[i]);
@@ -1179,7 +1185,7 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
           uint2 w;
           w.x = *reinterpret_cast<uint32_t*>(&p0);
           w.y = *reinterpret_cast<uint32_t*>(&p1);
-          *reinterpret_cast<uint2*>(P.dg + ((size_t)t * B + b) * (8 * kH) + col_g) = w;
+          dgp[(size_t)i * (8 * kH / 4)] = w;
 #pragma unroll
           for (int g = 0; g < 4; ++g) db[g] += dgv[g];
         }
