@@ -51,6 +51,7 @@ struct ds_blstm {
   __nv_bfloat16* dg2 = nullptr;  // dG of odd layers while dW of the layer above still reads dg
   float* colpart = nullptr;
   float* biaspart = nullptr;  // fused bias-gradient partials (CE grad epilogue / BPTT kernel)
+  float* biaspart2 = nullptr;  // BPTT partials of odd layers (the row sums of layer l+1 may still read biaspart)
   float* splitk = nullptr;    // split-K fp32 partials of dZ
   uint32_t* counters = nullptr;
   float* d_lr = nullptr;  // fused training step: learning rate read by the SGD kernels
@@ -213,6 +214,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
     const int64_t a1 = tiles_m * 4 * L.classes;
     const int64_t a2 = (int64_t)((h->Bmax + 127) / 128) * 4 * kGates2;
     h->biaspart = a.take<float>(base, a1 > a2 ? a1 : a2);
+    h->biaspart2 = a.take<float>(base, a2);
   }
   {  // split-K fp32 partials: dZ (K = classes) and dW_b (K = frames)
     const int64_t s1 = (int64_t)kDzPartMax * N * L.bottleneck, s2 = (int64_t)kWbSplit * L.bottleneck * kLayerOut;
@@ -606,7 +608,8 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       DS_CUDA_TRY(cudaEventRecord(h->ev_aux[2], s));
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_aux[2], 0));
       TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, h->side));
-      DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_aux[1], 0));  // biaspart free for the BPTT
+      if (!(ovl && ((Lh - 1) & 1)))  // biaspart free for the BPTT (unless it uses biaspart2)
+        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_aux[1], 0));
     } else {
       TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, s));
     }
@@ -622,10 +625,13 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   // GEMMs run on the SMs BPTT_{l-1} leaves free (low-priority stream, grid capped to those SMs) and
   // only dX = dG W_ih stays between two BPTTs.  dG alternates between two buffers by layer parity.
   for (int l = Lh - 1; l >= 0; --l) {
+    // overlap: dG and the bias partials alternate between two buffers by layer parity; the waits for
+    // their readers (dW_{l+2}, row sums of l+2) sit before dX_{l+1}, so BPTT_l follows dX_{l+1}
+    // directly (programmatic launch: its W_hh^T setup overlaps dX on the SMs dX leaves free)
     __nv_bfloat16* dgl = (ovl && (l & 1)) ? h->dg2 : h->dg;
-    if (ovl && l + 2 < Lh) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l + 2][1], 0));  // dW_{l+2} read dgl
+    float* bpl = (ovl && (l & 1)) ? h->biaspart2 : h->biaspart;
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], h->dy,
-                     dgl, h->counters, nullptr, h->biaspart};
+                     dgl, h->counters, nullptr, bpl};
     la.err = flag;
     if (ovl) {
       la.prio = h->prio_hi;
@@ -681,7 +687,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       DS_CUDA_TRY(cudaEventRecord(h->ev_rs[l][0], s));
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev_rs[l][0], 0));
     }
-    TRY(op_rowsum(h->biaspart, ((B + 127) / 128) * 4, kGates2, grad + L.off_b[l], rs_side ? h->side2 : s));
+    TRY(op_rowsum(bpl, ((B + 127) / 128) * 4, kGates2, grad + L.off_b[l], rs_side ? h->side2 : s));
     if (rs_side) DS_CUDA_TRY(cudaEventRecord(h->ev_rs[l][1], h->side2));
     MARK(PH_GEMM);
     if (ovl && l > 0) {
@@ -695,9 +701,14 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       TRY(lstm_wait_started(seq_words(h), Lh - l, flag, h->side3));
       TRY(gemm_launch(&gb, h->side3));
       TL("dW" + std::to_string(l), h->side3);
+      if (l + 1 < Lh) {  // BPTT_{l-1} overwrites the dG / bias-partial buffers of layer l+1
+        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l + 1][1], 0));
+        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l + 1][1], 0));
+      }
+      static const bool dx_full = getenv("DS_DX_FULL") != nullptr;
+      if (!dx_full) gx.max_pairs = dw_pairs;  // same two tile waves; the next BPTT's CTAs set up beside it
       TRY(gemm_launch(&gx, s));
       TL("dX" + std::to_string(l), s);
-      DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l][1], 0));
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_rs[l][1], 0));
       DS_CUDA_TRY(cudaEventRecord(h->ev_dw[l][1], h->side3));
       nl += 3;

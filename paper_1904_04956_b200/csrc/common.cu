@@ -50,13 +50,15 @@ static EncodeTiledFn get_encode() {
 
 // Programmatic dependent launch for the big kernels (GEMM, recurrences, fused
 // soft-max/dZ); DS_NO_PDL=1 turns it off (A/B measurements).
-bool use_pdl() {
+// DS_NO_PDL: bit 0 all launches, bit 1 + kind: one launch class (1 GEMMs, 2 forward recurrence,
+// 3 backward recurrence, 4 soft-max kernels) without programmatic dependent launch
+bool use_pdl(int kind) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DS_NO_PDL");
-    v = (e && e[0] == '1') ? 0 : 1;
+    v = e ? atoi(e) : 0;
   }
-  return v == 1;
+  return !(v & 1) && !(v & (1 << kind));
 }
 
 int make_tmap_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t outer,

@@ -34,7 +34,7 @@ int num_sms();
 // 2D row-major tensor [outer][inner] of `elem_bytes` elements, row pitch in
 // bytes; box = box_inner x box_outer elements; SWIZZLE_128B (box_inner *
 // elem_bytes must be 128).
-bool use_pdl();  // programmatic dependent launch on (DS_NO_PDL=1: off)
+bool use_pdl(int kind = 0);  // programmatic dependent launch on (DS_NO_PDL=1: off; see common.cu)
 int make_tmap_2d(CUtensorMap* out, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t outer,
                  uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
                  CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B);

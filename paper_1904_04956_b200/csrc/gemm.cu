@@ -674,7 +674,7 @@ void gemm_set_trace(unsigned long long* buf, int launch) {
 int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   b->trace = nullptr;
   static const bool no_bearly = getenv("DS_NO_BEARLY") != nullptr;  // A/B switch
-  if (no_bearly || !use_pdl()) b->b_early = 0;
+  if (no_bearly || !use_pdl(1)) b->b_early = 0;
   if (g_trace_countdown >= 0 && g_trace_countdown-- == 0) b->trace = g_trace;
   static bool attr_set = false;
   if (!attr_set) {
@@ -709,7 +709,7 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   attr[na].val.clusterDim.y = 1;
   attr[na].val.clusterDim.z = 1;
   ++na;
-  if (use_pdl()) {
+  if (use_pdl(1)) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;

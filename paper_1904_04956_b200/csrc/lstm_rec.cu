@@ -1245,7 +1245,7 @@ int lstm_wait_started(uint32_t* seq, int tag, int* err, cudaStream_t stream) {
 }
 
 static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream_t stream, size_t smem,
-                       int cluster, int threads = kThreads, int prio = 0) {
+                       int cluster, int threads = kThreads, int prio = 0, int pdl_kind = 2) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -1269,7 +1269,7 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
     attr[na].val.cooperative = 1;
     ++na;
   }
-  if (use_pdl()) {
+  if (pdl_kind >= 0 && use_pdl(pdl_kind)) {  // the transposed BPTT measured faster without (kind -1)
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
@@ -1452,8 +1452,8 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.n_btile = (nb + 127) / 128;
     P.counters = a.counters;
     rc = v3 ? launch_coop((const void*)lstm_bwd3_kernel, 32 * P.n_btile, P, stream, bwd3::kSmem, 8, bwd3::kThreads3,
-                          a.prio)
-            : launch_coop((const void*)lstm_bwd_kernel, 64 * P.n_btile, P, stream, bwd::kSmem, bwd::kClB);
+                          a.prio, -1)
+            : launch_coop((const void*)lstm_bwd_kernel, 64 * P.n_btile, P, stream, bwd::kSmem, bwd::kClB, kThreads, 0, 3);
     if (rc) return rc;
     P.trace = nullptr;  // trace only the first chunk
   }

@@ -676,7 +676,7 @@ int ce_grad_dz_launch(const CeGradDzArgs& a, cudaStream_t stream) {
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = use_pdl() ? 2 : 1;
+  cfg.numAttrs = use_pdl(4) ? 2 : 1;
   DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, ce_grad_dz_kernel, P));
   return DS_OK;
 }
@@ -724,7 +724,7 @@ int ce_stats_launch(const CeStatsArgs& a, cudaStream_t stream) {
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = use_pdl() ? 2 : 1;
+  cfg.numAttrs = use_pdl(4) ? 2 : 1;
   DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, ce_stats_kernel, P));
   return DS_OK;
 }
