@@ -2,6 +2,7 @@
 // training-step schedule of the paper BLSTM issued as one CUDA
 // graph per (batch, buffer) binding.  Implements the C ABI of
 // include/ds_blstm.h.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -67,6 +68,8 @@ struct ds_blstm {
   // weight-gradient GEMMs of layer l beside BPTT_{l-1} (narrow BPTT only): low-priority stream
   cudaStream_t side3 = nullptr;
   cudaEvent_t ev_dw[kMaxLayers][2] = {};  // [0] BPTT_l done, [1] dW_l done
+  cudaEvent_t ev_x[kMaxLayers] = {};      // dX_l (streamed behind BPTT_l on side3) done
+  cudaEvent_t ev_gz[2] = {};              // gate counters zeroed (fork / join)
   int prio_hi = 0, prio_lo = 0;
   // graph cache
   struct Key {
@@ -159,6 +162,27 @@ bool fused_ce_dz(const ds_blstm* h) {
 // the soft-max combine's last-block ticket: a word of the zeroed slack after the recurrent flags
 unsigned* ce_ticket(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax); }
 uint32_t* seq_words(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax) + 32; }
+// per-(layer, time step) BPTT completion counters gating the dX GEMM that streams behind it (zeroed per step)
+uint32_t* gate_words(const ds_blstm* h, int l) { return h->counters + lstm_counter_words(h->Bmax) + 64 + (size_t)l * h->T; }
+// row tiles of a time-major [T*B] operand in the order a bidirectional recurrence completes them
+// (frame t is final after step max(t, T-1-t)); false when there are too many row tiles to gate
+bool fill_m_order(GemmProblem& p, int B, int T) {
+  if (p.tiles_m > 64) return false;
+  const int N = T * B;
+  std::vector<std::pair<int, int>> key(p.tiles_m);
+  for (int m = 0; m < p.tiles_m; ++m) {
+    const int r0 = m * 2 * kGemmBM, r1 = (r0 + 2 * kGemmBM < N ? r0 + 2 * kGemmBM : N) - 1;
+    int avail = 0;
+    for (int t = r0 / B; t <= r1 / B; ++t) {
+      const int a = t > T - 1 - t ? t : T - 1 - t;
+      if (a > avail) avail = a;
+    }
+    key[m] = {avail, m};
+  }
+  std::stable_sort(key.begin(), key.end());
+  for (int m = 0; m < p.tiles_m; ++m) p.m_order[m] = (uint8_t)key[m].second;
+  return true;
+}
 int fused_dz_splits(const ds_blstm* h, int N) {
   // h->splitk holds kDzPartMax x N x bottleneck floats
   return ce_grad_dz_splits(N, h->L.classes, kDzPartMax);
@@ -220,7 +244,7 @@ int carve(ds_blstm* h, char* base, size_t* total) {
     const int64_t s1 = (int64_t)kDzPartMax * N * L.bottleneck, s2 = (int64_t)kWbSplit * L.bottleneck * kLayerOut;
     h->splitk = a.take<float>(base, s1 > s2 ? s1 : s2);
   }
-  h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64);
+  h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64 + (size_t)kMaxLayers * h->T);
   h->d_lr = a.take<float>(base, 4);
   *total = a.off + 256;
   return DS_OK;
@@ -296,6 +320,14 @@ bool use_dw_overlap() {  // DS_DW_OVERLAP=0: weight gradients after each BPTT on
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DS_DW_OVERLAP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+bool use_dx_stream() {  // DS_DX_STREAM=0: dX after each BPTT instead of streaming behind it
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_DX_STREAM");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -454,6 +486,14 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   const bool ovl = narrow > 0 && !h->profile && use_dw_overlap();
   int dw_pairs = (num_sms() - narrow) / 2 - dw_pair_margin();
   if (dw_pairs < 1) dw_pairs = 1;
+  // per-time-step BPTT completion counters for the streamed dX: zeroed on side2 beside the output layer
+  const bool gated = ovl && use_dx_stream();
+  if (gated) {
+    DS_CUDA_TRY(cudaEventRecord(h->ev_gz[0], s));
+    DS_CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev_gz[0], 0));
+    DS_CUDA_TRY(cudaMemsetAsync(gate_words(h, 0), 0, sizeof(uint32_t) * (size_t)Lh * T, h->side2));
+    DS_CUDA_TRY(cudaEventRecord(h->ev_gz[1], h->side2));
+  }
 
   // ---- backward ----
   GemmProblem pwo;  // fused path: dW_o joins the dW_b / dY launch below
@@ -630,6 +670,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     // directly (programmatic launch: its W_hh^T setup overlaps dX on the SMs dX leaves free)
     __nv_bfloat16* dgl = (ovl && (l & 1)) ? h->dg2 : h->dg;
     float* bpl = (ovl && (l & 1)) ? h->biaspart2 : h->biaspart;
+    if (gated && l == Lh - 1) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_gz[1], 0));  // counters zeroed
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], h->dy,
                      dgl, h->counters, nullptr, bpl};
     la.err = flag;
@@ -637,6 +678,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       la.prio = h->prio_hi;
       la.seq = seq_words(h);
       la.tag = Lh - 1 - l;
+      if (gated) la.gate = gate_words(h, l);
     }
     TL("pre-bptt" + std::to_string(l), s);
     MARK(PH_LSTM_BWD);
@@ -692,6 +734,27 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     if (ovl && l > 0) {
       DS_CUDA_TRY(cudaEventRecord(h->ev_dw[l][0], s));
+      // dX_l streams behind BPTT_l (row tiles gated on its per-time-step counters) on side3 after
+      // dW_{l+1}, so only the last frames' tiles trail the recurrence; the first BPTT's dX (side3
+      // busy with dW_o there) stays on the main stream
+      bool stream_dx = gated && l + 1 < Lh;
+      if (stream_dx) {
+        GemmProblem& px = gx.p[0];
+        stream_dx = fill_m_order(px, B, T);
+        if (stream_dx) {
+          px.gate = gate_words(h, l);
+          px.gate_target = (uint32_t)lstm_bwd_gate_target(B);
+          px.gate_rows = B;
+          px.gate_T = T;
+          px.gate_err = flag;
+          gx.b_early = 0;
+          gx.max_pairs = dw_pairs;
+          gx.prio = h->prio_lo;
+          TRY(gemm_launch(&gx, h->side3));
+          TL("dX" + std::to_string(l), h->side3);
+          DS_CUDA_TRY(cudaEventRecord(h->ev_x[l], h->side3));
+        }
+      }
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_dw[l][0], 0));
       gb.max_pairs = dw_pairs;
       gb.prio = h->prio_lo;
@@ -701,14 +764,16 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       TRY(lstm_wait_started(seq_words(h), Lh - l, flag, h->side3));
       TRY(gemm_launch(&gb, h->side3));
       TL("dW" + std::to_string(l), h->side3);
+      if (stream_dx) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_x[l], 0));
       if (l + 1 < Lh) {  // BPTT_{l-1} overwrites the dG / bias-partial buffers of layer l+1
         DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l + 1][1], 0));
         DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l + 1][1], 0));
       }
-      static const bool dx_full = getenv("DS_DX_FULL") != nullptr;
-      if (!dx_full) gx.max_pairs = dw_pairs;  // same two tile waves; the next BPTT's CTAs set up beside it
-      TRY(gemm_launch(&gx, s));
-      TL("dX" + std::to_string(l), s);
+      if (!stream_dx) {
+        gx.max_pairs = dw_pairs;  // same two tile waves; the next BPTT's CTAs set up beside it
+        TRY(gemm_launch(&gx, s));
+        TL("dX" + std::to_string(l), s);
+      }
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_rs[l][1], 0));
       DS_CUDA_TRY(cudaEventRecord(h->ev_dw[l][1], h->side3));
       nl += 3;
@@ -838,7 +903,7 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
   }
   carve(h, reinterpret_cast<char*>(h->arena), &total);
   // recurrent-kernel flags count up across launches: zero once
-  e = cudaMemset(h->counters, 0, sizeof(uint32_t) * (lstm_counter_words(h->Bmax) + 64));
+  e = cudaMemset(h->counters, 0, sizeof(uint32_t) * (lstm_counter_words(h->Bmax) + 64 + (size_t)kMaxLayers * h->T));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
   for (int k = 0; k < kMaxLayers + 2 && e == cudaSuccess; ++k) {
     e = cudaEventCreateWithFlags(&h->ev_fork[k], cudaEventDisableTiming);
@@ -853,6 +918,8 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->side3, cudaStreamNonBlocking, h->prio_lo);
   for (int k = 0; k < kMaxLayers * 2 && e == cudaSuccess; ++k)
     e = cudaEventCreateWithFlags(&h->ev_dw[k / 2][k % 2], cudaEventDisableTiming);
+  for (int k = 0; k < kMaxLayers && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_x[k], cudaEventDisableTiming);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_gz[k], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     cudaFree(h->arena);
     delete h;
@@ -876,6 +943,10 @@ int ds_blstm_destroy(ds_blstm* h) {
     if (h->ev_rs[k / 2][k % 2]) cudaEventDestroy(h->ev_rs[k / 2][k % 2]);
     if (h->ev_dw[k / 2][k % 2]) cudaEventDestroy(h->ev_dw[k / 2][k % 2]);
   }
+  for (int k = 0; k < kMaxLayers; ++k)
+    if (h->ev_x[k]) cudaEventDestroy(h->ev_x[k]);
+  for (int k = 0; k < 2; ++k)
+    if (h->ev_gz[k]) cudaEventDestroy(h->ev_gz[k]);
   if (h->side2) cudaStreamDestroy(h->side2);
   if (h->side3) cudaStreamDestroy(h->side3);
   if (h->tl_buf) cudaFree(h->tl_buf);

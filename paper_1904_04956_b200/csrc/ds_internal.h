@@ -93,6 +93,14 @@ struct GemmProblem {
   int c_blk;
   int ksplit;             // split-K factor (EPI_F32 only): split s writes out + s*split_stride
   long long split_stride;
+  // Row gate (a GEMM streaming behind a recurrence): rows are time-major, gate_rows per time step;
+  // a tile's A rows are loaded once gate[t] >= gate_target for every time step t they cover.  Tiles
+  // are visited N-fastest in the m_order row-tile order (the order the recurrence completes them).
+  const uint32_t* gate;
+  uint32_t gate_target;
+  int gate_rows, gate_T;
+  int* gate_err;          // |= 8 when a gate wait times out
+  uint8_t m_order[64];
 };
 
 // Pair-tile schedule: when the tiles of a launch differ in length the host

@@ -66,6 +66,13 @@ __device__ __forceinline__ TileCoord locate(const GemmBatch& b, int tile) {
   int local = tile - b.p[p].tile_begin;
   TileCoord c;
   c.prob = p;
+  if (b.p[p].gate) {  // N-fastest in completion order of the row tiles
+    c.tn = local % b.p[p].tiles_n;
+    const int rest = local / b.p[p].tiles_n;
+    c.tm = b.p[p].m_order[rest % b.p[p].tiles_m];
+    c.ks = rest / b.p[p].tiles_m;
+    return c;
+  }
   c.tm = local % b.p[p].tiles_m;
   const int rest = local / b.p[p].tiles_m;
   c.tn = rest % b.p[p].tiles_n;
@@ -216,6 +223,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int m0 = tc.tm * kPairM + (int)crank * BM, n0 = tc.tn * BN + (int)crank * kBHalf;
         int kb0, kb1;
         kb_range(P, tc.ks, kb0, kb1);
+        if (P.gate) {  // this CTA's A rows: every time step they cover has completed upstream
+          const int t0 = m0 / P.gate_rows;
+          int t1 = (m0 + BM - 1) / P.gate_rows;
+          if (t1 > P.gate_T - 1) t1 = P.gate_T - 1;
+          for (int t = t0; t <= t1; ++t) {
+            uint32_t n = 0;
+            uint64_t g0 = 0;
+            while ((int32_t)(ld_acquire_gpu(P.gate + t) - P.gate_target) < 0) {
+              if ((++n & 1023u) == 0) {  // 2 s guard: a recurrence that never completes the step
+                const uint64_t now = globaltimer();
+                if (!g0) g0 = now;
+                else if (now - g0 > 2000000000ull) {
+                  if (P.gate_err) atomicOr(P.gate_err, 8);
+                  break;
+                }
+              }
+            }
+          }
+          fence_proxy_async_global();
+        }
         long long pst = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
           const bool early = ti == 0 && kb - kb0 < pre;

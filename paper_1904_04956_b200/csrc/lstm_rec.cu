@@ -1194,6 +1194,7 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
       named_bar_sync(3, kEpi * 32);  // dG of this step stored; staged inputs consumed
       if (kEpiLead) {
         st_release_gpu(myflag, base + (uint32_t)(s + 1));
+        if (P.gate) red_release_gpu_add(P.gate + t, 1u);  // dG of time t: this CTA's part stored
         trace_mark(P.trace, T, s, 4);
         if (s + 1 < T) {
           const int t1 = dir == 0 ? T - 2 - s : s + 1;
@@ -1351,6 +1352,7 @@ static const RecCaps& rec_caps() {
 }
 // 128-row batch tiles per launch: forward 64 CTAs per tile, backward 64 (split-K) or 32 (transposed)
 static int lstm_bwd_max_tiles() { return use_bwd3() ? rec_caps().bwd3_ctas / 32 : rec_caps().bwd_ctas / 64; }
+int lstm_bwd_gate_target(int B) { return 32 * ((B + 127) / 128); }
 int lstm_bwd_narrow_ctas(int B) {
   if (!use_bwd3()) return 0;
   const int tiles = (B + 127) / 128, cap = lstm_bwd_max_tiles();
@@ -1432,6 +1434,7 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   P.err = a.err;
   P.seq = a.seq;
   P.tag = a.tag;
+  P.gate = v3 ? a.gate : nullptr;
   P.variant = 7;  // acquire by ld.acquire, no writer-side fences
   if (v3) {
     const char* ev = getenv("DS_VARIANT");

@@ -25,6 +25,7 @@ struct LstmParams {
   int* err;     // optional: |= 8 when a flag wait times out (a peer CTA never published)
   uint32_t* seq;  // transposed BPTT: [0] step epoch, [1] last started launch (epoch*16 + tag)
   int tag;        // position of this backward launch in the step (0 = first: bumps the epoch)
+  uint32_t* gate; // transposed BPTT: per-time-step counters, +1 per CTA once its dG of that step is stored
 };
 
 struct LstmLayerArgs {
@@ -42,7 +43,10 @@ struct LstmLayerArgs {
   int prio = 0;             // != 0: launch priority (ahead of GEMMs issued beside the recurrence)
   uint32_t* seq = nullptr;  // start signal for GEMMs gated on this launch (lstm_wait_started)
   int tag = 0;
+  uint32_t* gate = nullptr;  // per-time-step completion counters (lstm_bwd_gate_target per step)
 };
+// value of a backward launch's per-time-step counter once every CTA stored its dG of that step
+int lstm_bwd_gate_target(int B);
 // Block `stream` until the backward launch with `tag` of the current step has started (its grid is
 // placed), so a GEMM issued next on `stream` only takes the SMs the recurrence left free.
 int lstm_wait_started(uint32_t* seq, int tag, int* err, cudaStream_t stream);
