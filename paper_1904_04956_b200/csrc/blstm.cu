@@ -358,7 +358,9 @@ int sgd_segment(ds_blstm* h, SgdCtx& c, float* grad, int* flag, int64_t off, int
   const int k = c.nfork++;
   DS_CUDA_TRY(cudaEventRecord(h->ev_fork[k], s));
   DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork[k], 0));
-  int rc = op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, 16, h->side);
+  static const int side_blocks = getenv("DS_SGD_BLOCKS") ? atoi(getenv("DS_SGD_BLOCKS")) : 48;  // 16 left the last layer's update on the critical path
+  int rc = op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, side_blocks,
+                     h->side);
   if (rc) return rc;
   if ((rc = tl_mark(h, "sgd" + std::to_string(k), h->side))) return rc;
   DS_CUDA_TRY(cudaEventRecord(h->ev_join[k], h->side));
@@ -787,12 +789,15 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     nl += 2;
     // layer l's gradients are final: update them beside BPTT_{l-1} (layer 0 on the critical path)
     TRY(sgd_segment(h, sg, grad, flag, L.off_wih[l], L.off_b[l] + kGates2 - L.off_wih[l], l > 0, s));
+    if (l == 0) TL("sgd-main", s);
   }
   if (ovl)  // every weight gradient is complete when the step ends (also without an update)
     for (int l = out_side_done ? 0 : 1; l < Lh; ++l) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l][1], 0));
+  TL("dW-joined", s);
   if (sg.theta) {
     MARK(PH_OTHER);
     for (int k = 0; k < sg.nfork; ++k) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_join[k], 0));
+    TL("sgd-joined", s);
     TRY(op_snapshot_aux(sg.theta, L, h->wih0pad, h->bias_snap, s));
     nl += L.layers + 2;
   }
