@@ -49,10 +49,12 @@ struct ds_blstm {
   __nv_bfloat16* dz = nullptr;
   __nv_bfloat16* dy = nullptr;
   __nv_bfloat16* dg = nullptr;
-  __nv_bfloat16* dg2 = nullptr;  // dG of odd layers while dW of the layer above still reads dg
+  __nv_bfloat16* dg2 = nullptr;  // overlapped backward: dG of layer l in buffer l % 3 (dg, dg2, dg3), so
+  __nv_bfloat16* dg3 = nullptr;  //   BPTT_{l-1} waits only for the readers of layer l+2's
   float* colpart = nullptr;
   float* biaspart = nullptr;  // fused bias-gradient partials (CE grad epilogue / BPTT kernel)
-  float* biaspart2 = nullptr;  // BPTT partials of odd layers (the row sums of layer l+1 may still read biaspart)
+  float* biaspart2 = nullptr;  // BPTT bias partials of layer l in buffer l % 3 (biaspart, biaspart2, biaspart3)
+  float* biaspart3 = nullptr;
   float* splitk = nullptr;    // split-K fp32 partials of dZ
   uint32_t* counters = nullptr;
   float* d_lr = nullptr;  // fused training step: learning rate read by the SGD kernels
@@ -68,7 +70,12 @@ struct ds_blstm {
   // weight-gradient GEMMs of layer l beside BPTT_{l-1} (narrow BPTT only): low-priority stream
   cudaStream_t side3 = nullptr;
   cudaEvent_t ev_dw[kMaxLayers][2] = {};  // [0] BPTT_l done, [1] dW_l done
-  cudaEvent_t ev_x[kMaxLayers] = {};      // dX_l (streamed behind BPTT_l on side3) done
+  cudaEvent_t ev_x[kMaxLayers] = {};      // dX_l (streamed behind BPTT_l on side4) done
+  // dX_l = dG_l W_ih_l streamed behind BPTT_l in direction-split units (high-priority stream)
+  cudaStream_t side4 = nullptr;
+  // its outputs: dY_{l-1} = dyx[l & 1][0] (direction-0 dG) + dyx[l & 1][1] (direction-1 dG); by layer
+  // parity, since a half gated on one BPTT direction must not overwrite rows the other still reads
+  __nv_bfloat16* dyx[2][2] = {};
   cudaEvent_t ev_gz[2] = {};              // gate counters zeroed (fork / join)
   int prio_hi = 0, prio_lo = 0;
   // graph cache
@@ -162,26 +169,64 @@ bool fused_ce_dz(const ds_blstm* h) {
 // the soft-max combine's last-block ticket: a word of the zeroed slack after the recurrent flags
 unsigned* ce_ticket(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax); }
 uint32_t* seq_words(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax) + 32; }
-// per-(layer, time step) BPTT completion counters gating the dX GEMM that streams behind it (zeroed per step)
-uint32_t* gate_words(const ds_blstm* h, int l) { return h->counters + lstm_counter_words(h->Bmax) + 64 + (size_t)l * h->T; }
-// row tiles of a time-major [T*B] operand in the order a bidirectional recurrence completes them
-// (frame t is final after step max(t, T-1-t)); false when there are too many row tiles to gate
-bool fill_m_order(GemmProblem& p, int B, int T) {
-  if (p.tiles_m > 64) return false;
-  const int N = T * B;
-  std::vector<std::pair<int, int>> key(p.tiles_m);
-  for (int m = 0; m < p.tiles_m; ++m) {
-    const int r0 = m * 2 * kGemmBM, r1 = (r0 + 2 * kGemmBM < N ? r0 + 2 * kGemmBM : N) - 1;
-    int avail = 0;
-    for (int t = r0 / B; t <= r1 / B; ++t) {
-      const int a = t > T - 1 - t ? t : T - 1 - t;
-      if (a > avail) avail = a;
-    }
-    key[m] = {avail, m};
+int dx_pairs() {  // CTA pairs the streamed dX holds beside the BPTT (DS_DX_PAIRS)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_DX_PAIRS");
+    v = e ? atoi(e) : 16;
+    if (v < 1) v = 1;
   }
-  std::stable_sort(key.begin(), key.end());
-  for (int m = 0; m < p.tiles_m; ++m) p.m_order[m] = (uint8_t)key[m].second;
-  return true;
+  return v;
+}
+// Per-step counters after the recurrent flags (zeroed per step, one memset), per layer: [2][T] BPTT
+// completion counters (per direction and time step, gating dX_l) and [T][2][2] dY completion counters
+// (dX_{l+1}'s two per-direction outputs, per frame and unit direction, gating BPTT_l)
+uint32_t* gate_words(const ds_blstm* h, int l) { return h->counters + lstm_counter_words(h->Bmax) + 64 + (size_t)l * 6 * h->T; }
+uint32_t* ready_words(const ds_blstm* h, int l) { return gate_words(h, l) + 2 * h->T; }
+size_t counter_words_total(const ds_blstm* h) { return lstm_counter_words(h->Bmax) + 64 + (size_t)kMaxLayers * 6 * h->T; }
+// Host list schedule of the streamed dX: a unit (direction d's problem, row tile, column tile) becomes
+// available when direction d of the BPTT has finished all its frames (direction 0 finishes frame t at
+// step T-1-t, direction 1 at step t); units go, in order of availability, to the CTA pair that frees
+// up first under a simple cost model (a BPTT step ~ 14 k-blocks of a pair tile).
+int dx_schedule(GemmBatch& g, int pairs, int B, int T) {
+  struct Unit {
+    int avail, tile;
+    double dur;
+  };
+  std::vector<Unit> us;
+  int begin = 0;
+  for (int d = 0; d < g.nprob; ++d) {
+    const GemmProblem& P = g.p[d];
+    const int n = P.tiles_m * P.tiles_n;
+    for (int local = 0; local < n; ++local) {  // the kernel's mapping: row tile fastest
+      const int tm = local % P.tiles_m;
+      const int r0 = tm * 2 * kGemmBM, r1 = std::min(r0 + 2 * kGemmBM, P.M) - 1;
+      int avail = 0;
+      for (int t = r0 / B; t <= r1 / B; ++t) avail = std::max(avail, d == 0 ? T - 1 - t : t);
+      us.push_back({avail, begin + local, (P.K + kGemmBK - 1) / kGemmBK + 3.0});
+    }
+    begin += n;
+  }
+  if ((int)us.size() > kMaxSched || pairs > kMaxPairs) return fail_arg("streamed dX: too many units");
+  std::stable_sort(us.begin(), us.end(), [](const Unit& a, const Unit& b) { return a.avail < b.avail; });
+  std::vector<double> fr(pairs, 0.0);
+  std::vector<std::vector<int>> lists(pairs);
+  for (const Unit& u : us) {
+    int best = 0;
+    for (int q = 1; q < pairs; ++q)
+      if (fr[q] < fr[best]) best = q;
+    fr[best] = std::max(fr[best], 14.0 * u.avail) + u.dur;
+    lists[best].push_back(u.tile);
+  }
+  int pos = 0;
+  for (int q = 0; q < pairs; ++q) {
+    g.pstart[q] = (uint16_t)pos;
+    for (int t : lists[q]) g.order[pos++] = (uint16_t)t;
+  }
+  g.pstart[pairs] = (uint16_t)pos;
+  g.sched = 1;
+  g.presched = pairs;
+  return DS_OK;
 }
 int fused_dz_splits(const ds_blstm* h, int N) {
   // h->splitk holds kDzPartMax x N x bottleneck floats
@@ -227,8 +272,10 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   }
   h->dz = a.take<__nv_bfloat16>(base, (size_t)N * L.bottleneck);
   h->dy = a.take<__nv_bfloat16>(base, (size_t)N * kLayerOut);
+  for (int i = 0; i < 4; ++i) h->dyx[i / 2][i % 2] = a.take<__nv_bfloat16>(base, (size_t)N * kLayerOut);
   h->dg = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
   h->dg2 = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
+  h->dg3 = a.take<__nv_bfloat16>(base, (size_t)N * kGates2);
   {  // bottleneck bias colsum partials / CE loss partials
     const int64_t c1 = op_colsum_scratch(N, L.bottleneck), c2 = (N + 31) / 32 + 64;
     h->colpart = a.take<float>(base, c1 > c2 ? c1 : c2);
@@ -239,12 +286,13 @@ int carve(ds_blstm* h, char* base, size_t* total) {
     const int64_t a2 = (int64_t)((h->Bmax + 127) / 128) * 4 * kGates2;
     h->biaspart = a.take<float>(base, a1 > a2 ? a1 : a2);
     h->biaspart2 = a.take<float>(base, a2);
+    h->biaspart3 = a.take<float>(base, a2);
   }
   {  // split-K fp32 partials: dZ (K = classes) and dW_b (K = frames)
     const int64_t s1 = (int64_t)kDzPartMax * N * L.bottleneck, s2 = (int64_t)kWbSplit * L.bottleneck * kLayerOut;
     h->splitk = a.take<float>(base, s1 > s2 ? s1 : s2);
   }
-  h->counters = a.take<uint32_t>(base, lstm_counter_words(h->Bmax) + 64 + (size_t)kMaxLayers * h->T);
+  h->counters = a.take<uint32_t>(base, counter_words_total(h));
   h->d_lr = a.take<float>(base, 4);
   *total = a.off + 256;
   return DS_OK;
@@ -392,7 +440,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   bool out_side_done = false;  // ev_dw[0][1] recorded: the output-layer weight gradients ran beside BPTT_{L-1}
 
   MARK(PH_OTHER);
-  TRY(op_gather(idx, B, T, h->feats, h->labels, h->n_seq, h->x0, h->lab, flag, s));
+  TRY(op_gather(idx, B, T, h->feats, h->labels, h->n_seq, h->x0, h->lab, flag, s, seq_words(h)));
   auto Y = [&](int l) { return h->yfull[l] + (size_t)B * kLayerOut; };
 
   // ---- forward ----
@@ -488,13 +536,16 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   const bool ovl = narrow > 0 && !h->profile && use_dw_overlap();
   int dw_pairs = (num_sms() - narrow) / 2 - dw_pair_margin();
   if (dw_pairs < 1) dw_pairs = 1;
-  // per-time-step BPTT completion counters for the streamed dX: zeroed on side2 beside the output layer
-  const bool gated = ovl && use_dx_stream();
-  if (gated) {
+  // dX_l streamed behind BPTT_l (side4, direction-split units finished in the kernel) and consumed by
+  // BPTT_{l-1} frame by frame: its per-step counters are zeroed on side2 beside the output layer
+  const bool xstream = ovl && use_dx_stream() && B % 32 == 0;
+  const int dxp = xstream ? std::min(dx_pairs(), dw_pairs - 1) : 0;
+  if (xstream) {
     DS_CUDA_TRY(cudaEventRecord(h->ev_gz[0], s));
     DS_CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev_gz[0], 0));
-    DS_CUDA_TRY(cudaMemsetAsync(gate_words(h, 0), 0, sizeof(uint32_t) * (size_t)Lh * T, h->side2));
+    DS_CUDA_TRY(cudaMemsetAsync(gate_words(h, 0), 0, sizeof(uint32_t) * (size_t)Lh * 6 * T, h->side2));
     DS_CUDA_TRY(cudaEventRecord(h->ev_gz[1], h->side2));
+    DS_CUDA_TRY(cudaStreamWaitEvent(h->side4, h->ev_gz[1], 0));
   }
 
   // ---- backward ----
@@ -631,7 +682,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       gb.nprob = q0 + 1;
       // dW_o streams the 344 MB dlogits: beyond ~24 pairs its HBM traffic slows the BPTT it hides behind
       static const int wo_pairs = getenv("DS_WO_PAIRS") ? atoi(getenv("DS_WO_PAIRS")) : 24;
-      gb.max_pairs = wo_pairs > 0 && wo_pairs < dw_pairs ? wo_pairs : dw_pairs;
+      gb.max_pairs = wo_pairs > 0 && wo_pairs < dw_pairs - dxp ? wo_pairs : dw_pairs - dxp;
       gb.prio = h->prio_lo;
       DS_CUDA_TRY(cudaEventRecord(h->ev_aux[3], s));
       TRY(gemm_launch(&gy, s));
@@ -650,8 +701,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       DS_CUDA_TRY(cudaEventRecord(h->ev_aux[2], s));
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_aux[2], 0));
       TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, h->side));
-      if (!(ovl && ((Lh - 1) & 1)))  // biaspart free for the BPTT (unless it uses biaspart2)
-        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_aux[1], 0));
+      // (biaspart is read there: the first BPTT writing it waits below)
     } else {
       TRY(op_colsum(h->dz, N, bott, bott, h->colpart, grad + L.off_bb, s));
     }
@@ -670,17 +720,30 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     // overlap: dG and the bias partials alternate between two buffers by layer parity; the waits for
     // their readers (dW_{l+2}, row sums of l+2) sit before dX_{l+1}, so BPTT_l follows dX_{l+1}
     // directly (programmatic launch: its W_hh^T setup overlaps dX on the SMs dX leaves free)
-    __nv_bfloat16* dgl = (ovl && (l & 1)) ? h->dg2 : h->dg;
-    float* bpl = (ovl && (l & 1)) ? h->biaspart2 : h->biaspart;
-    if (gated && l == Lh - 1) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_gz[1], 0));  // counters zeroed
-    LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l], h->dy,
-                     dgl, h->counters, nullptr, bpl};
+    const int buf = ovl ? l % 3 : 0;
+    __nv_bfloat16* dgl = buf == 0 ? h->dg : buf == 1 ? h->dg2 : h->dg3;
+    float* bpl = buf == 0 ? h->biaspart : buf == 1 ? h->biaspart2 : h->biaspart3;
+    if (aux_join && buf == 0) {  // the output layer's bias row sums (side stream) have read biaspart
+      DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_aux[1], 0));
+      aux_join = false;
+    }
+    if (xstream && l == Lh - 1) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_gz[1], 0));  // counters zeroed
+    const bool dy_streamed = xstream && l + 1 < Lh;  // dY = the two halves of dX_{l+1}
+    LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l],
+                     dy_streamed ? h->dyx[(l + 1) & 1][0] : h->dy, dgl, h->counters, nullptr, bpl};
     la.err = flag;
     if (ovl) {
       la.prio = h->prio_hi;
       la.seq = seq_words(h);
       la.tag = Lh - 1 - l;
-      if (gated) la.gate = gate_words(h, l);
+      if (xstream) {
+        la.gate = gate_words(h, l);
+        if (dy_streamed) {  // still streaming: frame by frame
+          la.dy2 = h->dyx[(l + 1) & 1][1];
+          la.dyready = ready_words(h, l);
+          la.dyready_target = (uint32_t)((B / 32) * (kHidden / 64));
+        }
+      }
     }
     TL("pre-bptt" + std::to_string(l), s);
     MARK(PH_LSTM_BWD);
@@ -736,47 +799,63 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_GEMM);
     if (ovl && l > 0) {
       DS_CUDA_TRY(cudaEventRecord(h->ev_dw[l][0], s));
-      // dX_l streams behind BPTT_l (row tiles gated on its per-time-step counters) on side3 after
-      // dW_{l+1}, so only the last frames' tiles trail the recurrence; the first BPTT's dX (side3
-      // busy with dW_o there) stays on the main stream
-      bool stream_dx = gated && l + 1 < Lh;
-      if (stream_dx) {
-        GemmProblem& px = gx.p[0];
-        stream_dx = fill_m_order(px, B, T);
-        if (stream_dx) {
-          px.gate = gate_words(h, l);
+      if (xstream) {
+        // dX_l = dG_l W_ih_l behind BPTT_l on side4 as two problems, one per BPTT direction (K = its
+        // 2048 gate columns, rows gated on that direction's per-step counters, units list-scheduled in
+        // completion order), into dy / dy2; every stored block is counted per (frame, unit direction,
+        // half) and BPTT_{l-1} sums the halves frame by frame as they land
+        GemmBatch gd;
+        memset(&gd, 0, sizeof(gd));
+        gd.nprob = 2;
+        for (int d = 0; d < 2; ++d) {  // dY_d = dG[:, dir d] W_ih[dir d rows]: K = one direction's 2048 gates
+          GemmProblem& px = gd.p[d];
+          TRY(gemm_problem(&px, dgl + (size_t)d * kGates, kGates2, 0, h->snap + L.off_wih[l] + (size_t)d * kGates * kLayerOut,
+                           kLayerOut, 1, N, kLayerOut, kGates));
+          px.epi = EPI_BF16;
+          px.out = h->dyx[l & 1][d];
+          px.ldo = kLayerOut;
+          TRY(gemm_bf16_output(&px));
+          px.gate = gate_words(h, l) + (size_t)d * T;
           px.gate_target = (uint32_t)lstm_bwd_gate_target(B);
           px.gate_rows = B;
           px.gate_T = T;
           px.gate_err = flag;
-          gx.b_early = 0;
-          gx.max_pairs = dw_pairs;
-          gx.prio = h->prio_lo;
-          TRY(gemm_launch(&gx, h->side3));
-          TL("dX" + std::to_string(l), h->side3);
-          DS_CUDA_TRY(cudaEventRecord(h->ev_x[l], h->side3));
+          px.ready = ready_words(h, l - 1) + d;
+          px.ready_rows = B;
+          px.ready_cols = kHidden;
+          px.ready_stride = 2;
         }
+        TRY(dx_schedule(gd, dxp, B, T));
+        gd.prio = h->prio_hi;
+        gd.trace = gemm_layer_trace(l);
+        gd.trace_keep = gd.trace != nullptr;
+        TRY(lstm_wait_started(seq_words(h), Lh - 1 - l, flag, h->side4));  // BPTT_l holds its SMs
+        TRY(gemm_launch(&gd, h->side4));
+        TL("dX" + std::to_string(l), h->side4);
+        DS_CUDA_TRY(cudaEventRecord(h->ev_x[l], h->side4));
+        nl += 2;
       }
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_dw[l][0], 0));
-      gb.max_pairs = dw_pairs;
+      gb.max_pairs = dw_pairs - dxp;
       gb.prio = h->prio_lo;
       gb.b_early = 0;  // its stream predecessor is the previous layer's dW, not BPTT_l
-      gx.prio = h->prio_hi;  // dX first: it is the critical path between the two BPTTs
       // dW_l only once BPTT_{l-1} holds its SMs (dX_l runs alone on the machine first)
       TRY(lstm_wait_started(seq_words(h), Lh - l, flag, h->side3));
       TRY(gemm_launch(&gb, h->side3));
       TL("dW" + std::to_string(l), h->side3);
-      if (stream_dx) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_x[l], 0));
-      if (l + 1 < Lh) {  // BPTT_{l-1} overwrites the dG / bias-partial buffers of layer l+1
-        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l + 1][1], 0));
-        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l + 1][1], 0));
+      if (l + 2 < Lh) {  // BPTT_{l-1} overwrites the dG / bias-partial buffers of layer l+2
+        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l + 2][1], 0));
+        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l + 2][1], 0));
+        if (xstream) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_x[l + 2], 0));
       }
-      if (!stream_dx) {
+      if (!xstream) {
         gx.max_pairs = dw_pairs;  // same two tile waves; the next BPTT's CTAs set up beside it
         TRY(gemm_launch(&gx, s));
         TL("dX" + std::to_string(l), s);
       }
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_rs[l][1], 0));
+      // layer l's update rewrites the W_ih snapshot dX_l reads: after it (dX_l ends long before dW_l)
+      if (xstream) DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_x[l], 0));
       DS_CUDA_TRY(cudaEventRecord(h->ev_dw[l][1], h->side3));
       nl += 3;
       // layer l's gradients are final once dW_l is: update them beside BPTT_{l-1}
@@ -793,6 +872,7 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   }
   if (ovl)  // every weight gradient is complete when the step ends (also without an update)
     for (int l = out_side_done ? 0 : 1; l < Lh; ++l) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_dw[l][1], 0));
+  if (xstream && Lh > 1) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_x[1], 0));  // side4 joined (its last dX)
   TL("dW-joined", s);
   if (sg.theta) {
     MARK(PH_OTHER);
@@ -908,7 +988,7 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
   }
   carve(h, reinterpret_cast<char*>(h->arena), &total);
   // recurrent-kernel flags count up across launches: zero once
-  e = cudaMemset(h->counters, 0, sizeof(uint32_t) * (lstm_counter_words(h->Bmax) + 64 + (size_t)kMaxLayers * h->T));
+  e = cudaMemset(h->counters, 0, sizeof(uint32_t) * counter_words_total(h));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
   for (int k = 0; k < kMaxLayers + 2 && e == cudaSuccess; ++k) {
     e = cudaEventCreateWithFlags(&h->ev_fork[k], cudaEventDisableTiming);
@@ -921,6 +1001,7 @@ int ds_blstm_create(const ds_blstm_cfg* c, int device, ds_blstm** out) {
   if (e == cudaSuccess && use_timeline()) e = cudaMalloc(&h->tl_buf, 256 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&h->prio_lo, &h->prio_hi);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->side3, cudaStreamNonBlocking, h->prio_lo);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->side4, cudaStreamNonBlocking, h->prio_hi);
   for (int k = 0; k < kMaxLayers * 2 && e == cudaSuccess; ++k)
     e = cudaEventCreateWithFlags(&h->ev_dw[k / 2][k % 2], cudaEventDisableTiming);
   for (int k = 0; k < kMaxLayers && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&h->ev_x[k], cudaEventDisableTiming);
@@ -954,6 +1035,7 @@ int ds_blstm_destroy(ds_blstm* h) {
     if (h->ev_gz[k]) cudaEventDestroy(h->ev_gz[k]);
   if (h->side2) cudaStreamDestroy(h->side2);
   if (h->side3) cudaStreamDestroy(h->side3);
+  if (h->side4) cudaStreamDestroy(h->side4);
   if (h->tl_buf) cudaFree(h->tl_buf);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->loss_pinned) cudaFreeHost(h->loss_pinned);
@@ -1193,6 +1275,7 @@ int ds_debug_timeline(ds_blstm* h, char* buf, int32_t len) {
   if (h->tl_n > 0)
     DS_CUDA_TRY(cudaMemcpy(t.data(), h->tl_buf, sizeof(unsigned long long) * h->tl_n, cudaMemcpyDeviceToHost));
   for (int i = 0; i < h->tl_n; ++i) out += h->tl_name[i] + " " + std::to_string((double)(t[i] - t[0]) * 1e-6) + "\n";
+  if (h->tl_n > 0) out += "base_ns " + std::to_string(t[0]) + "\n";  // absolute globaltimer of "start"
   snprintf(buf, (size_t)len, "%s", out.c_str());
   return DS_OK;
 }
@@ -1202,7 +1285,9 @@ int ds_debug_gemm_trace(void* buf, int32_t launch) {
     ce_grad_dz_set_trace(static_cast<unsigned long long*>(buf));
     return DS_OK;
   }
-  if (buf && launch < 0) return fail_arg("launch index must be >= 0 (or -1: soft-max/dZ kernel)");
+  if (buf && launch < 0 && launch > -2 - kMaxLayers)  // -2 - l: the streamed dX of layer l (graph capture)
+    return gemm_set_trace(static_cast<unsigned long long*>(buf), launch), DS_OK;
+  if (buf && launch < 0) return fail_arg("launch index must be >= 0 (or -1: soft-max/dZ kernel, -2-l: dX of layer l)");
   gemm_set_trace(static_cast<unsigned long long*>(buf), launch);
   return DS_OK;
 }

@@ -94,14 +94,21 @@ struct GemmProblem {
   int ksplit;             // split-K factor (EPI_F32 only): split s writes out + s*split_stride
   long long split_stride;
   // Row gate (a GEMM streaming behind a recurrence): rows are time-major, gate_rows per time step;
-  // a tile's A rows are loaded once gate[t] >= gate_target for every time step t they cover.  Tiles
-  // are visited N-fastest in the m_order row-tile order (the order the recurrence completes them).
+  // a tile's A rows are loaded once gate[t] >= gate_target for every time step t < gate_T they
+  // cover.  A gated launch needs a host schedule (GemmBatch::presched: its units in the order the
+  // recurrence completes them).
   const uint32_t* gate;
   uint32_t gate_target;
   int gate_rows, gate_T;
   int* gate_err;          // |= 8 when a gate wait times out
-  uint8_t m_order[64];
+  // Completion counters of the bf16 output: +1 (release) per stored 32-row x 64-column warp block on
+  // ready[((row / ready_rows) * (N / ready_cols) + col / ready_cols) * ready_stride] (a recurrence
+  // consuming the rows of one time step and one column group waits for (ready_rows / 32) *
+  // (ready_cols / 64))
+  uint32_t* ready;
+  int ready_rows, ready_cols, ready_stride;
 };
+
 
 // Pair-tile schedule: when the tiles of a launch differ in length the host
 // assigns them to the persistent CTA pairs longest-first onto the least
@@ -115,6 +122,7 @@ struct GemmBatch {
   int nprob;
   int total_tiles;
   int sched;                            // 1: use order/pstart
+  int presched;                         // order/pstart/sched filled by the caller for `presched` pairs
   int b_early;                          // B of every problem is not written by the predecessor kernel:
                                         // prefetch it before griddep_wait (PDL)
   int max_pairs;                        // > 0: at most this many CTA pairs (a GEMM running beside a
@@ -122,11 +130,14 @@ struct GemmBatch {
   int prio;                             // != 0: launch priority (cudaLaunchAttributePriority)
   uint16_t pstart[kMaxPairs + 1];       // pair p runs order[pstart[p] .. pstart[p+1])
   uint16_t order[kMaxSched];
-  // debug: per-CTA per-tile timeline (tools/gemm_trace.py), null in production
+  // debug: per-CTA per-tile timeline (tools/gemm_trace.py, tools/dx_trace.py), null in production
   unsigned long long* trace;
+  int trace_keep;                       // the caller set `trace` (gemm_layer_trace)
 };
-// debug: trace the `launch`-th gemm_launch from now on into `buf` (null: off)
+// debug: trace the `launch`-th gemm_launch from now on into `buf` (null: off); launch <= -2: the
+// streamed dX of layer -launch-2 inside the step graph (gemm_layer_trace)
 void gemm_set_trace(unsigned long long* buf, int launch);
+unsigned long long* gemm_layer_trace(int layer);
 
 // Host helpers -------------------------------------------------------------
 // Describe one problem. A/B are device pointers with the given row pitches

@@ -51,8 +51,9 @@ constexpr int kEpiGroups = 1;  // epilogue warp groups taking alternate tiles (1
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + kEpiWarps * kStageC + 256;
 
 // trace record: [cta][tile < kTrTiles][kTrFields] (globaltimer ns / clock64 cycles)
-constexpr int kTrTiles = 8, kTrFields = 8;
-enum { TR_MMA_START, TR_MMA_FULLSTALL, TR_MMA_END, TR_EPI_START, TR_EPI_END, TR_EPI_LAST, TR_PROD_STALL, TR_CTA_START };
+constexpr int kTrTiles = 32, kTrFields = 11;
+enum { TR_MMA_START, TR_MMA_FULLSTALL, TR_MMA_END, TR_EPI_START, TR_EPI_END, TR_EPI_LAST, TR_PROD_STALL, TR_CTA_START,
+       TR_GATE0, TR_GATE1, TR_READY };
 
 struct TileCoord {
   int prob, tm, tn, ks;
@@ -66,13 +67,6 @@ __device__ __forceinline__ TileCoord locate(const GemmBatch& b, int tile) {
   int local = tile - b.p[p].tile_begin;
   TileCoord c;
   c.prob = p;
-  if (b.p[p].gate) {  // N-fastest in completion order of the row tiles
-    c.tn = local % b.p[p].tiles_n;
-    const int rest = local / b.p[p].tiles_n;
-    c.tm = b.p[p].m_order[rest % b.p[p].tiles_m];
-    c.ks = rest / b.p[p].tiles_m;
-    return c;
-  }
   c.tm = local % b.p[p].tiles_m;
   const int rest = local / b.p[p].tiles_m;
   c.tn = rest % b.p[p].tiles_n;
@@ -224,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         int kb0, kb1;
         kb_range(P, tc.ks, kb0, kb1);
         if (P.gate) {  // this CTA's A rows: every time step they cover has completed upstream
+          if (trace && ti < kTrTiles) trace[ti * kTrFields + TR_GATE0] = globaltimer();
           const int t0 = m0 / P.gate_rows;
           int t1 = (m0 + BM - 1) / P.gate_rows;
           if (t1 > P.gate_T - 1) t1 = P.gate_T - 1;
@@ -232,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             uint64_t g0 = 0;
             while ((int32_t)(ld_acquire_gpu(P.gate + t) - P.gate_target) < 0) {
               if ((++n & 1023u) == 0) {  // 2 s guard: a recurrence that never completes the step
+                if (P.gate_err && (*reinterpret_cast<volatile int*>(P.gate_err) & 8)) break;  // step failed
                 const uint64_t now = globaltimer();
                 if (!g0) g0 = now;
                 else if (now - g0 > 2000000000ull) {
@@ -242,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             }
           }
           fence_proxy_async_global();
+          if (trace && ti < kTrTiles) trace[ti * kTrFields + TR_GATE1] = globaltimer();
         }
         long long pst = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -516,6 +513,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             if (nb + 16 < n_valid) store_bf16x16(orow + nb + 16, v + 16);
           }
         }
+        if (P.ready && rt * BM + (int)q * 32 < P.m_valid) {  // output block stored: count it
+          __syncwarp();
+          if (lane == 0) {
+            if (P.c_tma) bulk_wait0();
+            fence_proxy_async_global();  // async-proxy (TMA) stores before the generic release
+            const int r0 = rt * BM + (int)q * 32;
+            red_release_gpu_add(P.ready + ((r0 / P.ready_rows) * (P.N / P.ready_cols) + n0 / P.ready_cols) * P.ready_stride,
+                                1u);
+            if (trace && ti < kTrTiles && e == 0) trace[ti * kTrFields + TR_READY] = globaltimer();
+          }
+        }
       } else {  // EPI_F32
         float* orow = reinterpret_cast<float*>(P.out) + (size_t)tc.ks * P.split_stride + (size_t)row * ldo;
         const int accumulate = P.accumulate;
@@ -693,13 +701,16 @@ static void schedule_tiles(GemmBatch* b, int pairs) {
 
 static unsigned long long* g_trace = nullptr;
 static int g_trace_countdown = -1;
+static int g_trace_layer = -1;
+unsigned long long* gemm_layer_trace(int layer) { return layer == g_trace_layer ? g_trace : nullptr; }
 void gemm_set_trace(unsigned long long* buf, int launch) {
   g_trace = buf;
-  g_trace_countdown = buf ? launch : -1;
+  g_trace_layer = buf && launch <= -2 ? -launch - 2 : -1;
+  g_trace_countdown = buf && launch >= 0 ? launch : -1;
 }
 
 int gemm_launch(GemmBatch* b, cudaStream_t stream) {
-  b->trace = nullptr;
+  if (!b->trace_keep) b->trace = nullptr;
   static const bool no_bearly = getenv("DS_NO_BEARLY") != nullptr;  // A/B switch
   if (no_bearly || !use_pdl(1)) b->b_early = 0;
   if (g_trace_countdown >= 0 && g_trace_countdown-- == 0) b->trace = g_trace;
@@ -715,6 +726,10 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
     const int nkb = (P.K + BK - 1) / BK;
     if (P.ksplit > 1 && (P.epi != EPI_F32 || P.accumulate || (P.ksplit - 1) * ((nkb + P.ksplit - 1) / P.ksplit) >= nkb))
       return fail_arg("split-K needs EPI_F32, no accumulate and no empty split");
+    if (P.gate && !b->presched) return fail_arg("gated GEMM: needs a host schedule (presched)");
+    if (P.ready && P.ready_stride < 1) P.ready_stride = 1;
+    if (P.ready && (P.epi != EPI_BF16 || P.ready_rows % 32 || P.ready_cols % 64 || P.ready_rows < 32 || P.N % P.ready_cols))
+      return fail_arg("output counters: 32-row / 64-column granularity");
     P.tile_begin = total;
     total += P.tiles_m * P.tiles_n * P.ksplit;
   }
@@ -722,8 +737,14 @@ int gemm_launch(GemmBatch* b, cudaStream_t stream) {
   if (total == 0) return DS_OK;
   int max_pairs = num_sms() / 2 < kMaxPairs ? num_sms() / 2 : kMaxPairs;
   if (b->max_pairs > 0 && b->max_pairs < max_pairs) max_pairs = b->max_pairs;
-  const int pairs = total < max_pairs ? total : max_pairs;
-  schedule_tiles(b, pairs);
+  int pairs = total < max_pairs ? total : max_pairs;
+  if (b->presched > 0) {
+    if (!b->sched || b->presched > kMaxPairs || b->pstart[b->presched] != total)
+      return fail_arg("gemm: bad host schedule");
+    pairs = b->presched;
+  } else {
+    schedule_tiles(b, pairs);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kThreads);

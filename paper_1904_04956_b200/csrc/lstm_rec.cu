@@ -75,6 +75,7 @@ struct SpinGuard {
 };
 __device__ __forceinline__ bool spin_expired(SpinGuard& g, int* err) {
   if ((++g.n & 1023u) != 0) return false;
+  if (err && (*reinterpret_cast<volatile int*>(err) & 8)) return true;  // the step already failed: drain
   const uint64_t now = globaltimer();
   if (g.t0 == 0) {
     g.t0 = now;
@@ -816,7 +817,7 @@ constexpr int kRows = 128;                 // batch rows per tile (MMA N)
 constexpr int kHalfRows = kRows / 2;       // staged per CTA (N split across the pair)
 constexpr int kChunk = kHalfRows * 128;    // 8 KB: 64 rows x 64 gate columns bf16, SWIZZLE_128B
 constexpr int kChunks = kSlice / 64;       // 8 B chunks per step
-constexpr int kStages = 8;
+constexpr int kStages = 7;                 // (8 measured no faster; the 8 KB pay for the second dY input)
 constexpr int kPitch = 144;                // bytes per unit row of an exchange block (64 fp16 + pad)
 constexpr int kBlock = kFin * kPitch;      // 4608: one (source slice, batch half) block
 constexpr int kRecvBuf = kKS * 2 * kBlock; // one step's incoming partials (own + 3 peers)
@@ -825,9 +826,10 @@ constexpr int kWBytes = kSlice * kUnits * 2;  // 128 KB W slice, staged once (al
 constexpr int kRingBytes = kStages * kChunk;
 constexpr int kInG = kRows * kFin * 4 * 2;  // 32 KB
 constexpr int kInC = kRows * kFin * 4;      // 16 KB
-constexpr int kInDY = kRows * kFin * 2;     // 8 KB
-constexpr size_t kSmem = 1024 + kRingBytes + 2 * kRecvBuf + kSendBytes + kInG + kInC + kInDY + 256;
-static_assert(kWBytes <= kRingBytes + 2 * kRecvBuf, "W staging must fit in the ring + recv region");
+constexpr int kInDY = kRows * kFin * 2;     // 8 KB per dY input (dY, or the two per-direction halves of a streamed dX)
+constexpr size_t kSmem = 1024 + kRingBytes + 2 * kRecvBuf + kSendBytes + kInG + kInC + 2 * kInDY + 256;
+static_assert(kWBytes <= kRingBytes + 2 * kRecvBuf + kSendBytes, "W staging must fit in the ring + recv + send region");
+static_assert(kSmem <= 232448, "shared memory");
 constexpr uint32_t kACol = 256;            // A = W^T slice at TMEM columns 256..511 (two bf16 per column)
 constexpr int kEpi = 16;                   // epilogue warps 0..15 (warp % 4 = TMEM lane quadrant)
 constexpr int kProdWarp = 16, kMmaWarp = 17;  // TMA producer, MMA issuer (+ TMEM allocation)
@@ -842,10 +844,22 @@ constexpr int kFlagLine0 = 4;
 __device__ __forceinline__ void issue_inputs(const LstmParams& P, uint64_t* bar, uint8_t* g, uint8_t* c, uint8_t* dy,
                                              int t, int tc, int brow0, int dir, int unit0) {
   const bool cprev = tc >= 0 && tc < P.T;
-  mbar_arrive_expect_tx(bar, bwd3::kInG + bwd3::kInDY + (cprev ? bwd3::kInC : 0));
+  mbar_arrive_expect_tx(bar, bwd3::kInG + (P.dy2 ? 2 : 1) * bwd3::kInDY + (cprev ? bwd3::kInC : 0));
   const int row = t * P.B + brow0;
   tma_load_2d(g, &P.tmG, bar, dir * 4 * kH + unit0 * 4, row);
+  if (P.dyready) {  // dY of (t, dir) written by the GEMM streaming behind the previous BPTT (both halves)
+    for (int src = 0; src < (P.dy2 ? 2 : 1); ++src) {
+      const uint32_t* w = P.dyready + (2 * t + dir) * 2 + src;
+      if (ld_acquire_gpu(w) < P.dyready_target) {
+        SpinGuard sg;
+        while (ld_acquire_gpu(w) < P.dyready_target)
+          if (spin_expired(sg, P.err)) break;
+      }
+    }
+    fence_proxy_async_global();
+  }
   tma_load_2d(dy, &P.tmDY, bar, dir * kH + unit0, row);
+  if (P.dy2) tma_load_2d(dy + bwd3::kInDY, &P.tmDY2, bar, dir * kH + unit0, row);
   if (cprev) tma_load_2d(c, &P.tmC, bar, dir * kH + unit0, tc * P.B + brow0);
 }
 
@@ -858,9 +872,9 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
   uint8_t* send = recv + 2 * kRecvBuf;      // [dst 3][batch half 2][32 units][kPitch]
   uint8_t* in_g = send + kSendBytes;        // next step's cell inputs: gates [128 rows][32 units x 4] bf16
   uint8_t* in_c = in_g + kInG;              //   c_{t-1} [128 rows][32] f32
-  uint8_t* in_dy = in_c + kInC;             //   dY [128 rows][32] bf16
+  uint8_t* in_dy = in_c + kInC;             //   dY [128 rows][32] bf16 (+ the second half at in_dy + kInDY)
   uint8_t* wstage = ring;                   // launch only: [unit half 2][512 gate rows][64 units] bf16
-  uint64_t* bars = reinterpret_cast<uint64_t*>(in_dy + kInDY);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(in_dy + 2 * kInDY);
   uint64_t* full = bars;                    // [kStages] leader only: both CTAs' chunk bytes
   uint64_t* empty = full + kStages;         // [kStages] per CTA: the pair's MMAs read the stage
   uint64_t* wbar = empty + kStages;
@@ -915,6 +929,7 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
     tma_prefetch_desc(&P.tmG);
     tma_prefetch_desc(&P.tmC);
     tma_prefetch_desc(&P.tmDY);
+    if (P.dy2) tma_prefetch_desc(&P.tmDY2);
     mbar_arrive_expect_tx(wbar, kWBytes);
     for (int uq = 0; uq < 2; ++uq)
       for (int kh = 0; kh < 2; ++kh)
@@ -945,8 +960,7 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
   griddep_wait();
   if (threadIdx.x == 0) s_base = ld_relaxed_gpu(myflag);
   if (threadIdx.x == 0 && blockIdx.x == 0 && P.seq) {  // started: release GEMMs gated on this launch
-    const uint32_t ep = P.tag == 0 ? atomicAdd(P.seq, 1u) + 1u : ld_relaxed_gpu(P.seq);
-    st_release_gpu(P.seq + 1, ep * 16u + (uint32_t)P.tag);
+    st_release_gpu(P.seq + 1, ld_relaxed_gpu(P.seq) * 16u + (uint32_t)P.tag);  // epoch: bumped by the step's gather
   }
   __syncthreads();
   const uint32_t base = s_base;  // flag value at launch start (same for every flag of the group)
@@ -1168,7 +1182,8 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
         const uint2 actw = ld_shared_v2(cg_in + i * 256);
         const float ig = __uint_as_float(actw.x << 16), fg = __uint_as_float(actw.x & 0xffff0000u);
         const float gg = __uint_as_float(actw.y << 16), og = __uint_as_float(actw.y & 0xffff0000u);
-        const float dyv = __uint_as_float(ld_shared_u16(cdy_in + i * 64) << 16);
+        float dyv = __uint_as_float(ld_shared_u16(cdy_in + i * 64) << 16);
+        if (P.dy2) dyv += __uint_as_float(ld_shared_u16(cdy_in + kInDY + i * 64) << 16);
         const float cpv = has_cprev ? ld_shared_f32(cc_in + i * 128) : 0.f;
         const float dht = dh[i] + dyv;
         const float tcn = tanh_fast(cc[i]);
@@ -1194,7 +1209,7 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
       named_bar_sync(3, kEpi * 32);  // dG of this step stored; staged inputs consumed
       if (kEpiLead) {
         st_release_gpu(myflag, base + (uint32_t)(s + 1));
-        if (P.gate) red_release_gpu_add(P.gate + t, 1u);  // dG of time t: this CTA's part stored
+        if (P.gate) red_release_gpu_add(P.gate + dir * T + t, 1u);  // dG of (dir, t): this CTA's part stored
         trace_mark(P.trace, T, s, 4);
         if (s + 1 < T) {
           const int t1 = dir == 0 ? T - 2 - s : s + 1;
@@ -1231,7 +1246,7 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
 }
 
 __global__ void wait_started_kernel(const uint32_t* seq, int tag, int* err) {
-  const uint32_t target = ld_relaxed_gpu(seq) * 16u + (uint32_t)tag;  // this step's epoch (already bumped)
+  const uint32_t target = ld_relaxed_gpu(seq) * 16u + (uint32_t)tag;  // this step's epoch (bumped by its gather)
   SpinGuard g;
   while (!reached(ld_acquire_gpu(seq + 1), target))
     if (spin_expired(g, err)) return;
@@ -1352,7 +1367,7 @@ static const RecCaps& rec_caps() {
 }
 // 128-row batch tiles per launch: forward 64 CTAs per tile, backward 64 (split-K) or 32 (transposed)
 static int lstm_bwd_max_tiles() { return use_bwd3() ? rec_caps().bwd3_ctas / 32 : rec_caps().bwd_ctas / 64; }
-int lstm_bwd_gate_target(int B) { return 32 * ((B + 127) / 128); }
+int lstm_bwd_gate_target(int B) { return 16 * ((B + 127) / 128); }
 int lstm_bwd_narrow_ctas(int B) {
   if (!use_bwd3()) return 0;
   const int tiles = (B + 127) / 128, cap = lstm_bwd_max_tiles();
@@ -1422,6 +1437,9 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     if (!rc)
       rc = make_tmap_2d(&P.tmDY, a.dy, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2 * kH, (uint64_t)T * B, 2 * kH * 2,
                         bwd3::kFin, bwd3::kRows, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!rc && a.dy2)
+      rc = make_tmap_2d(&P.tmDY2, a.dy2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2 * kH, (uint64_t)T * B, 2 * kH * 2,
+                        bwd3::kFin, bwd3::kRows, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
   }
   P.gates = a.gates;
@@ -1435,6 +1453,11 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   P.seq = a.seq;
   P.tag = a.tag;
   P.gate = v3 ? a.gate : nullptr;
+  P.dyready = v3 ? a.dyready : nullptr;
+  P.dy2 = v3 ? a.dy2 : nullptr;
+  if (a.dy2 && !v3) return fail_arg("a second dY input needs the transposed BPTT");
+  P.dyready_target = a.dyready_target;
+  if (a.dyready && !v3) return fail_arg("streamed dY needs the transposed BPTT");
   P.variant = 7;  // acquire by ld.acquire, no writer-side fences
   if (v3) {
     const char* ev = getenv("DS_VARIANT");

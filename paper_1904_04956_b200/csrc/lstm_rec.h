@@ -11,6 +11,7 @@ struct LstmParams {
   CUtensorMap tmA;  // forward: Y_full; backward: dG
   CUtensorMap tmW;  // W_hh [4096, 512] bf16 (forward: K-major B; backward: MN-major B)
   CUtensorMap tmG, tmC, tmDY;  // transposed BPTT: per-step cell inputs (gates, c_{t-1}, dY) staged by TMA
+  CUtensorMap tmDY2;           //   second dY input (dY = dy + dy2), when dy2 != null
   __nv_bfloat16* gates;
   float* cstate;
   __nv_bfloat16* y;
@@ -25,7 +26,10 @@ struct LstmParams {
   int* err;     // optional: |= 8 when a flag wait times out (a peer CTA never published)
   uint32_t* seq;  // transposed BPTT: [0] step epoch, [1] last started launch (epoch*16 + tag)
   int tag;        // position of this backward launch in the step (0 = first: bumps the epoch)
-  uint32_t* gate; // transposed BPTT: per-time-step counters, +1 per CTA once its dG of that step is stored
+  uint32_t* gate; // transposed BPTT: per-(direction, time step) counters, +1 per CTA once its dG of that step is stored
+  const __nv_bfloat16* dy2;  // transposed BPTT: optional second dY input
+  const uint32_t* dyready;  // transposed BPTT: per-(time step, direction, input) dY counters of the GEMM producing dY
+  uint32_t dyready_target;  //   (0 / null: dY is complete when the launch starts)
 };
 
 struct LstmLayerArgs {
@@ -43,9 +47,17 @@ struct LstmLayerArgs {
   int prio = 0;             // != 0: launch priority (ahead of GEMMs issued beside the recurrence)
   uint32_t* seq = nullptr;  // start signal for GEMMs gated on this launch (lstm_wait_started)
   int tag = 0;
-  uint32_t* gate = nullptr;  // per-time-step completion counters (lstm_bwd_gate_target per step)
+  uint32_t* gate = nullptr;  // [2][T] per-(direction, time step) completion counters (lstm_bwd_gate_target)
+  // backward: dY = dy + dy2 (the two per-direction halves of dX_{l+1}) when dy2 != null
+  const __nv_bfloat16* dy2 = nullptr;
+  // dY streamed in by a GEMM still running: frame t of direction d's units of input i is complete once
+  // dyready[(2t + d) * 2 + i] >= dyready_target (GemmProblem::ready with ready_rows = B, ready_cols = 512,
+  // ready_stride = 2)
+  const uint32_t* dyready = nullptr;
+  uint32_t dyready_target = 0;
 };
-// value of a backward launch's per-time-step counter once every CTA stored its dG of that step
+// value of a backward launch's per-(direction, time step) counter once every CTA of that direction
+// stored its dG of that step
 int lstm_bwd_gate_target(int B);
 // Block `stream` until the backward launch with `tag` of the current step has started (its grid is
 // placed), so a GEMM issued next on `stream` only takes the SMs the recurrence left free.

@@ -23,8 +23,9 @@ constexpr int kEW = 256;  // elementwise block size
 // K1: X0[t*B+b, :] = feats[idx[b], t, :]   (rows of kInPad bf16 = 34 x 16 B)
 __global__ void gather_kernel(const int64_t* __restrict__ idx, int B, int T, const uint4* __restrict__ feats,
                               const int32_t* __restrict__ labels, uint4* __restrict__ x0, int32_t* __restrict__ lab,
-                              int64_t n_seq, int* __restrict__ flag) {
+                              int64_t n_seq, int* __restrict__ flag, uint32_t* __restrict__ epoch) {
   constexpr int kVec = kInPad * 2 / 16;  // 34
+  if (epoch && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(epoch, 1u);  // new step (lstm_wait_started)
   const int64_t total = (int64_t)T * B * kVec;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / kVec;
@@ -494,9 +495,9 @@ inline int ew_grid(int64_t n) {
 }  // namespace
 
 int op_gather(const int64_t* idx, int B, int T, const __nv_bfloat16* feats, const int32_t* labels, int64_t n_seq,
-              __nv_bfloat16* x0, int32_t* lab, int* flag, cudaStream_t s) {
+              __nv_bfloat16* x0, int32_t* lab, int* flag, cudaStream_t s, uint32_t* epoch) {
   gather_kernel<<<ew_grid((int64_t)T * B * 34), kEW, 0, s>>>(idx, B, T, reinterpret_cast<const uint4*>(feats), labels,
-                                                            reinterpret_cast<uint4*>(x0), lab, n_seq, flag);
+                                                            reinterpret_cast<uint4*>(x0), lab, n_seq, flag, epoch);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }

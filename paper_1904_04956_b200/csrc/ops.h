@@ -10,7 +10,7 @@ namespace ds {
 constexpr int kMaxGroup = 16;
 
 int op_gather(const int64_t* idx, int B, int T, const __nv_bfloat16* feats, const int32_t* labels, int64_t n_seq,
-              __nv_bfloat16* x0, int32_t* lab, int* flag, cudaStream_t s);
+              __nv_bfloat16* x0, int32_t* lab, int* flag, cudaStream_t s, uint32_t* epoch = nullptr);
 int op_colsum(const __nv_bfloat16* x, int64_t rows, int ncols, int64_t ld, float* part, float* out, cudaStream_t s);
 int64_t op_colsum_scratch(int64_t rows, int ncols);
 int op_splitk_bf16(const float* part, int S, int64_t n, __nv_bfloat16* out, cudaStream_t s);

@@ -19,7 +19,7 @@ sys.path.insert(0, ".")
 from paper_1904_04956_b200 import _lib  # noqa: E402
 from paper_1904_04956_b200.blstm import BlstmObjective, DeviceDataset, Learner, initial_weights  # noqa: E402
 
-TILES, FIELDS = 8, 8
+TILES, FIELDS = 32, 11
 B = 256
 lib = _lib.load()
 obj = BlstmObjective()

@@ -32,5 +32,7 @@ _lib.check(lib.ds_debug_timeline(L.handle, buf, len(buf)), "ds_debug_timeline")
 prev = {}
 for line in buf.value.decode().splitlines():
     name, t = line.split()
+    if name == "base_ns":
+        continue
     t = float(t)
     print(f"{name:>12s} {t * 1e3:9.1f} us")
