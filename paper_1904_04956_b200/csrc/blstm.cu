@@ -169,6 +169,15 @@ bool fused_ce_dz(const ds_blstm* h) {
 // the soft-max combine's last-block ticket: a word of the zeroed slack after the recurrent flags
 unsigned* ce_ticket(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax); }
 uint32_t* seq_words(const ds_blstm* h) { return h->counters + lstm_counter_words(h->Bmax) + 32; }
+int dw0_early() {  // frames per direction of layer 0's weight gradients computed beside BPTT_0 (DS_DW0_EARLY)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_DW0_EARLY");
+    v = e ? atoi(e) : 10;
+    if (v < 0) v = 0;
+  }
+  return v;
+}
 int dx_pairs() {  // CTA pairs the streamed dX holds beside the BPTT (DS_DX_PAIRS)
   static int v = -1;
   if (v < 0) {
@@ -862,7 +871,51 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       TRY(sgd_segment(h, sg, grad, flag, L.off_wih[l], L.off_b[l] + kGates2 - L.off_wih[l], true, h->side3));
       continue;
     }
-    TRY(gemm_launch(&gb, s));
+    const int E = dw0_early();
+    if (xstream && l == 0 && E > 0 && E < T) {
+      // layer 0 (no dX): the frames BPTT_0 completes first (direction 0 from t = T-1 down, direction 1
+      // from t = 0 up) go into its weight gradients beside it, on the pairs dX left, once E frames of
+      // each direction are final; the rest after it, accumulated onto them (early + late, fixed order)
+      GemmBatch ge, gl;
+      memset(&ge, 0, sizeof(ge));
+      memset(&gl, 0, sizeof(gl));
+      for (int part = 0; part < 2; ++part) {
+        GemmBatch& g = part ? gl : ge;
+        for (int d = 0; d < 2; ++d) {
+          // frames: early dir 0 [T-E, T), dir 1 [0, E); late dir 0 [0, T-E), dir 1 [E, T)
+          const int nf = part == 0 ? E : T - E;
+          const int r0 = (d == 0 ? (part == 0 ? T - E : 0) : (part == 0 ? 0 : E)) * B;
+          GemmProblem& pi = g.p[g.nprob++];  // dW_ih0 rows of direction d = dG[:, dir d]^T X0
+          TRY(gemm_problem(&pi, dgl + (size_t)r0 * kGates2 + (size_t)d * kGates, kGates2, 1, h->x0 + (size_t)r0 * kInPad,
+                           kInPad, 1, kGates, kInPad, nf * B));
+          pi.n_valid = L.input_dim;
+          pi.ldo = L.input_dim;
+          pi.epi = EPI_F32;
+          pi.out = grad + L.off_wih[0] + (size_t)d * kGates * L.input_dim;
+          pi.accumulate = part;
+          GemmProblem& ph = g.p[g.nprob++];  // dW_hh0[d] = dG[:, dir d]^T H_prev[d]
+          const __nv_bfloat16* hp = d == 0 ? h->yfull[0] : h->yfull[0] + (size_t)2 * B * kLayerOut + kHidden;
+          TRY(gemm_problem(&ph, dgl + (size_t)r0 * kGates2 + (size_t)d * kGates, kGates2, 1, hp + (size_t)r0 * kLayerOut,
+                           kLayerOut, 1, kGates, kHidden, nf * B));
+          ph.epi = EPI_F32;
+          ph.out = grad + L.off_whh[0] + (size_t)d * kGates * kHidden;
+          ph.ldo = kHidden;
+          ph.accumulate = part;
+        }
+      }
+      const uint32_t* g0 = gate_words(h, 0);
+      TRY(lstm_wait_counters(g0 + (T - E), g0 + T + (E - 1), (uint32_t)lstm_bwd_gate_target(B), flag, h->side4));
+      ge.max_pairs = dxp;
+      ge.prio = h->prio_hi;
+      TRY(gemm_launch(&ge, h->side4));
+      TL("dW0-early", h->side4);
+      DS_CUDA_TRY(cudaEventRecord(h->ev_x[0], h->side4));
+      DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_x[0], 0));
+      TRY(gemm_launch(&gl, s));
+      nl += 3;
+    } else {
+      TRY(gemm_launch(&gb, s));
+    }
     TL("grp" + std::to_string(l), s);
     if (rs_side) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_rs[l][1], 0));
     nl += 2;

@@ -534,8 +534,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           tmem_ld_wait();
           const int nb = n0 + c;
           if (!row_ok || nb >= n_valid) continue;
-          const bool vec = (nb + 32 <= n_valid) && ((ldo & 3) == 0) && !accumulate;
-          if (vec) {
+          const bool vec = (nb + 32 <= n_valid) && ((ldo & 3) == 0);
+          if (vec && accumulate) {  // this tile's rows were written earlier (a preceding K range): add onto them
+            float4 o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = *reinterpret_cast<const float4*>(orow + nb + 4 * i);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              *reinterpret_cast<float4*>(orow + nb + 4 * i) =
+                  make_float4(fmaf(v[4 * i], scale, o[i].x), fmaf(v[4 * i + 1], scale, o[i].y),
+                              fmaf(v[4 * i + 2], scale, o[i].z), fmaf(v[4 * i + 3], scale, o[i].w));
+          } else if (vec) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4)
               *reinterpret_cast<float4*>(orow + nb + i) =
@@ -546,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               const int n = nb + i;
               if (n < n_valid) {
                 float x = v[i] * scale;
-                if (accumulate) x += orow[n];
+                if (accumulate) x = fmaf(v[i], scale, orow[n]);
                 orow[n] = x;
               }
             }

@@ -441,6 +441,296 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
 }
 
 // ============================================================================
+// Forward, narrow (DS_FWD=3): 64 CTAs at B = 256 instead of 128, so that the next layer's input
+// projection could stream beside the recurrence on the SMs it leaves free.  Measured 5.4 us per
+// step (cell 1.4 us: twice fwd2's cell work per SM, MUFU / issue bound) against fwd2's 4.5.
+//   CTA pair (cta_group::2) = (dir, batch block of 128, 64 units = 256 gate rows).  Rank r
+//   holds W_hh rows [r*128, +128) of the pair's 256 as the MMA's A operand in tensor memory
+//   (128 lanes x 512 K = 256 columns, filled once per launch) and stages batch rows [r*64, +64)
+//   of every h_{t-1} chunk (B operand, N = 128 split across the pair): per step 32 pair MMAs
+//   M256 N128 K16 with A from TMEM into a double-buffered accumulator [128 gate rows, 128 batch]
+//   (256 columns).  16 epilogue warps (lane quadrant x 32-column group) transpose gate quads as in
+//   fwd2 (a thread owns one unit x 8 batch columns, c in registers), stage h_t in smem for
+//   coalesced stores; a publisher warp releases the CTA's step flag and counts the step on
+//   P.gate[dir * T + t] (the streamed projection of the next layer waits on those).
+//   16 CTAs per (dir, batch block): chunk k of h (64 units) = pair k.
+namespace fwd3 {
+constexpr int kNB = 128;                 // batch columns per pair (MMA N)
+constexpr int kNH = kNB / 2;             // batch rows staged per CTA
+constexpr int kPairs = kH / 64;          // 8 pairs per (dir, batch block)
+constexpr int kCtas = 2 * kPairs;        // 16
+constexpr int kChunkB = kNH * 128;       // 8 KB: 64 batch rows x 64 units bf16 (SWIZZLE_128B)
+constexpr int kBufB = 8 * kChunkB;       // one step's B operand (64 KB)
+constexpr int kWB = 128 * kH * 2;        // 128 KB W slice, staged once for the TMEM fill (aliases the B buffers)
+constexpr int kHst = kNB * 64;           // h staging: 128 batch rows x 32 units bf16 (8 KB)
+constexpr size_t kSmem = 1024 + 2 * kBufB + kHst + 512;
+constexpr int kEpiWarps = 16;
+constexpr int kEpiT = kEpiWarps * 32;
+constexpr int kThreadsF = 32 * (4 + kEpiWarps);
+constexpr uint32_t kACol = 256;          // A = W slice at TMEM columns 256..511 (two bf16 per column)
+constexpr int kPub = 2;                  // named barriers 2/3: epilogue <-> publisher
+static_assert(kWB <= 2 * kBufB, "W staging must fit in the B buffers");
+}  // namespace fwd3
+
+__global__ void __launch_bounds__(fwd3::kThreadsF, 1) lstm_fwd3_kernel(const __grid_constant__ LstmParams P) {
+  using namespace fwd3;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sm;                       // [2 steps][8 chunks][64 rows x 128 B]; launch: W staging
+  uint8_t* sH = sB + 2 * kBufB;           // [128 rows][32 units] bf16
+  uint64_t* full = reinterpret_cast<uint64_t*>(sH + kHst);  // [2][8], leader only
+  uint64_t* wbar = full + 16;
+  uint64_t* tfull = wbar + 1;    // [2]
+  uint64_t* tempty = tfull + 2;  // [2], leader: every epilogue warp of both CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ uint32_t s_base;
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();  // 0 = leader
+  const bool leader = rank == 0;
+  const int pg = blockIdx.x >> 1;
+  const int pr = pg % kPairs;
+  const int bb = (pg / kPairs) % P.n_btile;  // batch block of 128
+  const int dir = pg / (kPairs * P.n_btile);
+  const int gblk = P.b0 / kNB + bb;  // global 128-row block (its even 64-row flag line, shared with fwd2)
+  uint32_t* flags = P.counters + (size_t)gblk * kFlagWords128 + 2 * kGroupFlagWords + dir * kFlagLine;
+  const int T = P.T, B = P.B;
+  const int b0 = P.b0 + bb * kNB;
+
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < 16; ++i) mbar_init(&full[i], 1);
+    mbar_init(wbar, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // programmatic launch: the W_hh slice (operand snapshot, not written by the predecessor) goes
+  // into tensor memory before waiting for the predecessor grid
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&P.tmA);
+    tma_prefetch_desc(&P.tmW);
+    mbar_arrive_expect_tx(wbar, kWB);
+    const int wrow = dir * 4 * kH + pr * 256 + (int)rank * 128;
+    for (int kb = 0; kb < kH / 64; ++kb) tma_load_2d(sB + kb * 16384, &P.tmW, wbar, kb * 64, wrow);
+  }
+  if (warp >= 4) {  // TMEM lane m = gate row, column c = K (2c, 2c+1); 16-byte chunks unswizzled
+    const uint32_t e = warp - 4, q = e & 3, cq = e >> 2;  // lane quadrant, K quarter (128 K = 2 boxes)
+    const uint32_t m = q * 32 + lane;
+    mbar_wait(wbar, 0);
+#pragma unroll
+    for (int hb = 0; hb < 2; ++hb) {
+      const uint8_t* row = sB + (2 * cq + hb) * 16384 + m * 128;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t rr[16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint4 w = *reinterpret_cast<const uint4*>(row + (((half * 4 + j) ^ (m & 7)) << 4));
+          rr[4 * j] = w.x;
+          rr[4 * j + 1] = w.y;
+          rr[4 * j + 2] = w.z;
+          rr[4 * j + 3] = w.w;
+        }
+        tmem_st16(tmem + ((q * 32) << 16) + kACol + (2 * cq + hb) * 32 + half * 16, rr);
+      }
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // A in the TMEM of both CTAs; the staging area is free for the B operand
+  tc_fence_after();
+  griddep_wait();
+  if (threadIdx.x == 0) s_base = ld_relaxed_gpu(flags + (pr >> 2) * 8 + (pr & 3) * 2 + (int)rank);
+  if (threadIdx.x == 0 && blockIdx.x == 0 && P.seq)  // started: release GEMMs gated on this launch
+    st_release_gpu(P.seq + 2, ld_relaxed_gpu(P.seq) * 16u + (uint32_t)P.tag);
+  __syncthreads();
+  const uint32_t base = s_base;  // flag value at launch start (same for every CTA of the group)
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t full_c = mapa_shared(smem_u32(full), 0);
+      FlagSeg seg[2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) seg[0].v[i] = seg[1].v[i] = 0;
+      for (int s = 0; s < T; ++s) {
+        const int t = dir == 0 ? s : T - 1 - s;
+        const int tprev = dir == 0 ? t - 1 : t + 1;
+        const int arow = (tprev + 1) * B + b0 + (int)rank * kNH;
+        const int buf = s & 1;
+        for (int k = 0; k < kPairs; ++k) {
+          uint64_t* fb = &full[buf * 8 + k];
+          if (leader) mbar_arrive_expect_tx(fb, 2 * kChunkB);
+          if (s > 0) {  // chunk k of h_{t-1} = both CTAs of pair k (flags 2k, 2k+1)
+            wait_seg<2>(seg[k >> 2], flags + (k >> 2) * 8, (k & 3) * 2, base + (uint32_t)s, P.err);
+            fence_proxy_async_global();
+          }
+          tma_load_2d_pair(sB + buf * kBufB + k * kChunkB, &P.tmA, full_c + (uint32_t)(buf * 8 + k) * 8,
+                           dir * kH + k * 64, arow);
+          if (k == 0) trace_mark(P.trace, T, s, 0);
+        }
+        trace_mark(P.trace, T, s, 1);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      const uint32_t idesc = idesc_bf16_f32(256, kNB, 0, 0);
+      const uint32_t bbase = smem_u32(sB);
+      for (int s = 0; s < T; ++s) {
+        const int acc = s & 1, buf = s & 1;
+        mbar_wait_acq_cluster(&tempty[acc], ((s >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem + acc * kNB;
+        for (int k = 0; k < kPairs; ++k) {
+          mbar_wait(&full[buf * 8 + k], (s >> 1) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ts_pair(dacc, tmem + kACol + (uint32_t)(k * 4 + kk) * 8,
+                               smem_desc_sw128(bbase + buf * kBufB + k * kChunkB + kk * 32, 16, 1024), idesc,
+                               (k | kk) != 0);
+            if (k == kPairs - 1) mma_commit_pair_mc(&tfull[acc], 0x3);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // publisher: h_t of this CTA stored -> release the step flag, count the step for the next layer
+    uint32_t* myflag = flags + (pr >> 2) * 8 + (pr & 3) * 2 + (int)rank;
+    for (int s = 0; s < T; ++s) {
+      named_bar_sync(kPub, kEpiT + 32);
+      if (lane == 0) {
+        st_release_gpu(myflag, base + (uint32_t)(s + 1));
+        if (P.gate) red_release_gpu_add(P.gate + dir * T + (dir == 0 ? s : T - 1 - s), 1u);
+        trace_mark(P.trace, T, s, 4);
+      }
+      __syncwarp();
+      asm volatile("bar.arrive %0, %1;" ::"n"(kPub + 1), "n"(kEpiT + 32) : "memory");
+    }
+  } else if (warp >= 4) {
+    const uint32_t e = warp - 4;
+    const uint32_t q = e & 3, hc = e >> 2;      // TMEM lane quadrant, 32-column batch group
+    const uint32_t g = lane & 3;                 // gate of this thread's TMEM row (unit-interleaved rows)
+    const uint32_t b0b = g & 1, b1b = g >> 1;
+    const int uq = (int)(q * 8 + (lane >> 2));   // unit within the CTA's 32
+    const int unit = pr * 64 + (int)rank * 32 + uq;  // unit within the direction
+    const int col0 = (int)(hc * 32 + g * 8);     // after the transpose: batch columns col0 .. +8
+    const uint32_t tcol = tmem + ((q * 32) << 16) + hc * 32;
+    const uint32_t tempty_c = mapa_shared(smem_u32(tempty), 0);
+    const size_t gcol = (size_t)dir * 4 * kH + (size_t)unit * 4;
+    const int nrow = P.nb - bb * kNB;            // valid rows of this block in this launch
+    float c[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = 0.f;
+    for (int s = 0; s < T; ++s) {
+      if (s == T - 1) griddep_launch();  // the next kernel may start its prologue
+      const int t = dir == 0 ? s : T - 1 - s;
+      uint2 gp[8];  // input projection (i,f,g,o of this unit) of my 8 batch rows, fetched before the wait
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = b0 + col0 + i;
+        gp[i] = b < B ? *reinterpret_cast<const uint2*>(P.gates + ((size_t)t * B + b) * (8 * kH) + gcol)
+                      : make_uint2(0u, 0u);
+      }
+      mbar_wait(&tfull[s & 1], (s >> 1) & 1);
+      tc_fence_after();
+      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
+      float v[32];
+      tmem_ld32(tcol + (s & 1) * kNB, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tempty[s & 1]);
+        else
+          mbar_arrive_remote(tempty_c + (s & 1) * 8);
+      }
+      // quad transpose: stage 1 (lane ^ 2) splits the 32 columns in halves,
+      // stage 2 (lane ^ 1) in quarters -> 4 gates x 8 columns per lane
+      float a1[16], a2[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float send = b1b ? v[i] : v[16 + i];
+        a1[i] = b1b ? v[16 + i] : v[i];
+        a2[i] = __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      float k1[8], k2[8], r1[8], r2[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float s1 = b0b ? a1[i] : a1[8 + i];
+        const float s2 = b0b ? a2[i] : a2[8 + i];
+        k1[i] = b0b ? a1[8 + i] : a1[i];
+        k2[i] = b0b ? a2[8 + i] : a2[i];
+        r1[i] = __shfl_xor_sync(0xffffffffu, s1, 1);
+        r2[i] = __shfl_xor_sync(0xffffffffu, s2, 1);
+      }
+      float hv[8];
+#pragma unroll
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float x0 = b0b ? (b1b ? r2[i] : r1[i]) : (b1b ? k2[i] : k1[i]);   // i gate
+        const float x1 = b0b ? (b1b ? k2[i] : k1[i]) : (b1b ? r2[i] : r1[i]);   // f gate
+        const float x2 = b0b ? (b1b ? r1[i] : r2[i]) : (b1b ? k1[i] : k2[i]);   // g gate
+        const float x3 = b0b ? (b1b ? k1[i] : k2[i]) : (b1b ? r1[i] : r2[i]);   // o gate
+        const __nv_bfloat162* gg = reinterpret_cast<const __nv_bfloat162*>(&gp[i]);
+        const float2 g01 = __bfloat1622float2(gg[0]), g23 = __bfloat1622float2(gg[1]);
+        const float ig = sigmoid_fast(x0 + g01.x);
+        const float fg = sigmoid_fast(x1 + g01.y);
+        const float gt = tanh_fast(x2 + g23.x);
+        const float og = sigmoid_fast(x3 + g23.y);
+        c[i] = fmaf(fg, c[i], ig * gt);
+        hv[i] = og * tanh_fast(c[i]);
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(ig, fg), p1 = __floats2bfloat162_rn(gt, og);
+        gp[i].x = *reinterpret_cast<uint32_t*>(&p0);
+        gp[i].y = *reinterpret_cast<uint32_t*>(&p1);
+      }
+      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 5);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<__nv_bfloat16*>(sH)[(col0 + i) * 32 + uq] = __float2bfloat16_rn(hv[i]);
+      named_bar_sync(1, kEpiT);
+      {
+        const int tid = (int)(e * 32 + lane);  // 512 threads = 128 rows x 4 segments of 8 units
+        const int row = tid >> 2, sg = tid & 3;
+        const int b = b0 + row;
+        const uint4 w = reinterpret_cast<const uint4*>(sH)[tid];
+        if (b < B && row < nrow)
+          *reinterpret_cast<uint4*>(P.y + ((size_t)(t + 1) * B + b) * (2 * kH) + dir * kH + pr * 64 + rank * 32 +
+                                    sg * 8) = w;
+      }
+      if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);
+      asm volatile("bar.arrive %0, %1;" ::"n"(kPub), "n"(kEpiT + 32) : "memory");
+      named_bar_sync(kPub + 1, kEpiT + 32);  // the release is out: BPTT state, then reuse sH
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = b0 + col0 + i;
+        if (b < B && col0 + i < nrow) {
+          const size_t n = (size_t)t * B + b;
+          *reinterpret_cast<uint2*>(P.gates + n * (8 * kH) + gcol) = gp[i];
+          P.cstate[n * (2 * kH) + dir * kH + unit] = c[i];
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair(tmem, 512);
+}
+
+// ============================================================================
 // Backward: split-K over a 4-CTA cluster.
 //   cluster = (dir, batch tile, unit group ug of 64 units); CTA rank ks holds
 //   W_hh[gate rows ks*512 .. +512][64 units of ug] (64 KB, read as an
@@ -1245,17 +1535,29 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
   if (warp == kMmaWarp) tmem_dealloc_pair(tmem, 512);
 }
 
-__global__ void wait_started_kernel(const uint32_t* seq, int tag, int* err) {
+__global__ void wait_started_kernel(const uint32_t* seq, int tag, int slot, int* err) {
   const uint32_t target = ld_relaxed_gpu(seq) * 16u + (uint32_t)tag;  // this step's epoch (bumped by its gather)
   SpinGuard g;
-  while (!reached(ld_acquire_gpu(seq + 1), target))
+  while (!reached(ld_acquire_gpu(seq + slot), target))
+    if (spin_expired(g, err)) return;
+}
+
+__global__ void wait_counters_kernel(const uint32_t* a, const uint32_t* b, uint32_t target, int* err) {
+  SpinGuard g;
+  while (ld_acquire_gpu(a) < target || ld_acquire_gpu(b) < target)
     if (spin_expired(g, err)) return;
 }
 
 }  // namespace
 
-int lstm_wait_started(uint32_t* seq, int tag, int* err, cudaStream_t stream) {
-  wait_started_kernel<<<1, 32, 0, stream>>>(seq, tag, err);
+int lstm_wait_counters(const uint32_t* a, const uint32_t* b, uint32_t target, int* err, cudaStream_t stream) {
+  wait_counters_kernel<<<1, 32, 0, stream>>>(a, b, target, err);
+  DS_CUDA_TRY(cudaGetLastError());
+  return DS_OK;
+}
+
+int lstm_wait_started(uint32_t* seq, int tag, int* err, cudaStream_t stream, bool forward) {
+  wait_started_kernel<<<1, 32, 0, stream>>>(seq, tag, forward ? 2 : 1, err);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
@@ -1309,7 +1611,7 @@ static int launch_coop(const void* fn, int grid, const LstmParams& P, cudaStream
 // device), not just by the SM count: cluster placement inside GPCs leaves
 // SMs unusable.  A larger batch runs as several launches.
 struct RecCaps {
-  int fwd_ctas = 0, bwd_ctas = 0, bwd3_ctas = 0;  // co-resident CTAs in recurrent-kernel clusters
+  int fwd_ctas = 0, fwd3_ctas = 0, bwd_ctas = 0, bwd3_ctas = 0;  // co-resident CTAs in recurrent-kernel clusters
   int err = 0;
 };
 // DS_BWD=1 selects the round-1 split-K BPTT (single-CTA MMAs, 4-CTA clusters); default: transposed CTA-pair BPTT
@@ -1318,6 +1620,17 @@ static bool use_bwd3() {
   if (v < 0) {
     const char* e = getenv("DS_BWD");
     v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+// DS_FWD=3 selects the 64-CTA forward (W_hh in tensor memory, 128-row batch blocks: 5.4 us per step
+// against 4.5 for the default 128-CTA forward, whose cell work per SM is half; it would leave 84 SMs
+// to a projection streaming beside it)
+static bool use_fwd3() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_FWD");
+    v = (e && e[0] == '3') ? 1 : 0;
   }
   return v == 1;
 }
@@ -1350,6 +1663,8 @@ static const RecCaps& rec_caps() {
         cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(lstm_bwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd3::kSmem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(lstm_fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd3::kSmem) !=
             cudaSuccess) {
       cudaGetLastError();
       caps.err = 1;
@@ -1357,9 +1672,11 @@ static const RecCaps& rec_caps() {
     }
     const int sm = num_sms() >= 132 ? 128 : num_sms();
     const int f = cluster_cap((const void*)lstm_fwd2_kernel, fwd2::kSmem, 2);
+    const int f3 = cluster_cap((const void*)lstm_fwd3_kernel, fwd3::kSmem, 2, fwd3::kThreadsF);
     const int b = cluster_cap((const void*)lstm_bwd_kernel, bwd::kSmem, 4);
     const int b3 = cluster_cap((const void*)lstm_bwd3_kernel, bwd3::kSmem, 8, bwd3::kThreads3);
     caps.fwd_ctas = f < 0 ? sm : (f < sm ? f : sm);
+    caps.fwd3_ctas = f3 < 0 ? sm : (f3 < sm ? f3 : sm);
     caps.bwd_ctas = b < 0 ? sm : (b < sm ? b : sm);
     caps.bwd3_ctas = b3 < 0 ? sm : (b3 < sm ? b3 : sm);
   }
@@ -1374,7 +1691,7 @@ int lstm_bwd_narrow_ctas(int B) {
   return 32 * (tiles < cap ? tiles : cap);
 }
 int lstm_max_tiles() {
-  const int f = rec_caps().fwd_ctas / 64, b = lstm_bwd_max_tiles();
+  const int f = use_fwd3() ? rec_caps().fwd3_ctas / 32 : rec_caps().fwd_ctas / 64, b = lstm_bwd_max_tiles();
   const int t = b < f ? b : f;
   return t > 0 ? t : 0;
 }
@@ -1383,6 +1700,42 @@ int lstm_counter_words(int B) { return kFlagWords128 * ((B + 127) / 128); }
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   if (rec_caps().err) return fail_arg("recurrent kernels: cannot set the shared-memory attribute");
   const int B = a.B, T = a.T;
+  if (fwd && use_fwd3()) {
+    // 32 CTAs (2 directions x 8 pairs x 2) per 128-row batch block
+    const int max_blocks = rec_caps().fwd3_ctas / (2 * fwd3::kCtas);
+    if (max_blocks < 1) return fail_arg("device too small for the recurrent kernel");
+    LstmParams P;
+    memset(&P, 0, sizeof(P));
+    int rc = make_tmap_2d(&P.tmA, a.y_full, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2 * kH, (uint64_t)(T + 2) * B,
+                          2 * kH * 2, 64, fwd3::kNH);
+    if (rc) return rc;
+    rc = make_tmap_2d(&P.tmW, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kH, 8 * kH, kH * 2, 64, 128);
+    if (rc) return rc;
+    P.gates = a.gates;
+    P.cstate = a.cstate;
+    P.y = a.y_full;
+    P.trace = a.trace;
+    P.err = a.err;
+    P.seq = a.seq;
+    P.tag = a.tag;
+    P.gate = a.gate;
+    P.B = B;
+    P.T = T;
+    const int chunk_rows = max_blocks * fwd3::kNB;
+    for (int b0 = 0; b0 < B; b0 += chunk_rows) {
+      const int nb = (B - b0) < chunk_rows ? (B - b0) : chunk_rows;
+      P.b0 = b0;
+      P.nb = nb;
+      P.n_btile = (nb + fwd3::kNB - 1) / fwd3::kNB;  // 128-row blocks
+      P.counters = a.counters;
+      rc = launch_coop((const void*)lstm_fwd3_kernel, 2 * fwd3::kCtas * P.n_btile, P, stream, fwd3::kSmem, 2,
+                       fwd3::kThreadsF, a.prio);
+      if (rc) return rc;
+      P.trace = nullptr;  // trace only the first chunk
+      P.seq = nullptr;    // the start signal is the first launch's
+    }
+    return DS_OK;
+  }
   if (fwd) {
     // 32 CTAs (2 directions x 8 pairs x 2) per 64-row batch block
     const int max_blocks = rec_caps().fwd_ctas / (2 * fwd2::kCtas);

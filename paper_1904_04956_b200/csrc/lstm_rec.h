@@ -24,9 +24,10 @@ struct LstmParams {
   int variant;  // debug: bit0 skip writer proxy fence, bit1 skip release fence
   float xscale; // BPTT: fp16 scale of the exchanged partial dh (power of two)
   int* err;     // optional: |= 8 when a flag wait times out (a peer CTA never published)
-  uint32_t* seq;  // transposed BPTT: [0] step epoch, [1] last started launch (epoch*16 + tag)
+  uint32_t* seq;  // [0] step epoch, [1] last started BPTT launch, [2] last started forward launch (epoch*16 + tag)
   int tag;        // position of this backward launch in the step (0 = first: bumps the epoch)
-  uint32_t* gate; // transposed BPTT: per-(direction, time step) counters, +1 per CTA once its dG of that step is stored
+  uint32_t* gate; // narrow forward / transposed BPTT: per-(direction, time step) counters, +1 per CTA once its h / dG
+                  // of that step is stored
   const __nv_bfloat16* dy2;  // transposed BPTT: optional second dY input
   const uint32_t* dyready;  // transposed BPTT: per-(time step, direction, input) dY counters of the GEMM producing dY
   uint32_t dyready_target;  //   (0 / null: dY is complete when the launch starts)
@@ -61,7 +62,9 @@ struct LstmLayerArgs {
 int lstm_bwd_gate_target(int B);
 // Block `stream` until the backward launch with `tag` of the current step has started (its grid is
 // placed), so a GEMM issued next on `stream` only takes the SMs the recurrence left free.
-int lstm_wait_started(uint32_t* seq, int tag, int* err, cudaStream_t stream);
+int lstm_wait_started(uint32_t* seq, int tag, int* err, cudaStream_t stream, bool forward = false);
+// Block `stream` until the (per-step zeroed) counters *a and *b both reach `target`.
+int lstm_wait_counters(const uint32_t* a, const uint32_t* b, uint32_t target, int* err, cudaStream_t stream);
 
 int lstm_max_tiles();
 // CTAs of the first backward launch for a batch of B (the SMs a concurrent GEMM must leave free),
