@@ -365,7 +365,44 @@ struct SgdCtx {
   float mu = 0.f;
   int nfork = 0;
   const GroupSync* grp = nullptr;  // SSGD: per-layer group sync instead of the local update
+  bool mirror = false;             // the local updates also write the padded W_ih0 / bias snapshot copies
 };
+// the operand-snapshot extras (op_snapshot_aux) inside the update of the block [off, off + n)
+SgdMirror segment_mirror(const ds_blstm* h, int64_t off, int64_t n) {
+  const ModelLayout& L = h->L;
+  SgdMirror m;
+  auto in = [&](int64_t b, int64_t c) { return b >= off && b + c <= off + n; };
+  if (in(L.off_wih[0], (int64_t)kGates2 * L.input_dim)) {
+    m.wpad = h->wih0pad;
+    m.wbeg = L.off_wih[0] - off;
+    m.wcnt = (int64_t)kGates2 * L.input_dim;
+    m.din = L.input_dim;
+  }
+  int k = 0;
+  auto add = [&](int64_t b, int64_t c, float* dst, float scale) {
+    if (k < 3 && in(b, c)) {
+      m.fdst[k] = dst;
+      m.fbeg[k] = b - off;
+      m.fcnt[k] = c;
+      m.fscale[k] = scale;
+      ++k;
+    }
+  };
+  float* bs = h->bias_snap;
+  for (int l = 0; l < L.layers; ++l) add(L.off_b[l], kGates2, bs + (size_t)l * kGates2, 1.f);
+  float* bo = bs + (size_t)L.layers * kGates2;
+  add(L.off_bb, L.bottleneck, bo, 1.f);
+  add(L.off_bo, L.classes, bo + L.bottleneck, 1.f);
+  add(L.off_bo, L.classes, bo + L.bottleneck + L.classes, 1.4426950408889634f);  // b_o * log2(e) (CE statistics)
+  return m;
+}
+bool mirror_ok(const ds_blstm* h) {  // every mirrored range 4-aligned (float4 update path)
+  const ModelLayout& L = h->L;
+  bool ok = L.input_dim % 4 == 0 && L.off_wih[0] % 4 == 0 && L.off_bb % 4 == 0 && L.off_bo % 4 == 0 &&
+            L.bottleneck % 4 == 0 && L.classes % 4 == 0;
+  for (int l = 0; l < L.layers; ++l) ok = ok && L.off_b[l] % 4 == 0;
+  return ok;
+}
 // SSGD group update of [off, off + n): barrier, sharded reduce + SGD + all-gather, barrier
 int group_segment(ds_blstm* h, SgdCtx& c, int64_t off, int64_t n, cudaStream_t s) {
   int rc = group_barrier(*c.grp, s);
@@ -410,14 +447,16 @@ int sgd_segment(ds_blstm* h, SgdCtx& c, float* grad, int* flag, int64_t off, int
     DS_CUDA_TRY(cudaEventRecord(h->ev_join[k], h->side));
     return DS_OK;
   }
+  const SgdMirror mir = segment_mirror(h, off, n);
   if (!side)
-    return op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, 0, s);
+    return op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, 0, s,
+                     c.mirror ? &mir : nullptr);
   const int k = c.nfork++;
   DS_CUDA_TRY(cudaEventRecord(h->ev_fork[k], s));
   DS_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork[k], 0));
   static const int side_blocks = getenv("DS_SGD_BLOCKS") ? atoi(getenv("DS_SGD_BLOCKS")) : 48;  // 16 left the last layer's update on the critical path
   int rc = op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, side_blocks,
-                     h->side);
+                     h->side, c.mirror ? &mir : nullptr);
   if (rc) return rc;
   if ((rc = tl_mark(h, "sgd" + std::to_string(k), h->side))) return rc;
   DS_CUDA_TRY(cudaEventRecord(h->ev_join[k], h->side));
@@ -931,8 +970,8 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     MARK(PH_OTHER);
     for (int k = 0; k < sg.nfork; ++k) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_join[k], 0));
     TL("sgd-joined", s);
-    TRY(op_snapshot_aux(sg.theta, L, h->wih0pad, h->bias_snap, s));
-    nl += L.layers + 2;
+    if (!sg.mirror) TRY(op_snapshot_aux(sg.theta, L, h->wih0pad, h->bias_snap, s));  // else written by the updates
+    nl += L.layers + (sg.mirror ? 1 : 2);
   }
   TL("end", s);
   MARK(PH_END);
@@ -1210,6 +1249,7 @@ int ds_blstm_train_step(ds_blstm* h, const int64_t* idx, int32_t B, float* theta
       return fail_arg("group step: theta / grad differ from this member's buffers in the group");
     sg.grp = &h->grp;
   }
+  sg.mirror = !sg.grp && mirror_ok(h) && !getenv("DS_NO_SGD_MIRROR");
   return run_step(h, idx, B, grad, loss_sum, nonfinite, s, sg);
 }
 

@@ -104,7 +104,8 @@ __global__ void rowsum_kernel(const float* __restrict__ part, int nrows, int nco
 }
 
 // split-K finish: out(bf16)[m][n] = sum_s part[s][m][n] in split order
-__global__ void splitk_bf16_kernel(const float* __restrict__ part, int S, int64_t n, __nv_bfloat16* __restrict__ out) {
+__global__ void splitk_bf16_kernel(const float* __restrict__ part, int S, int64_t n, __nv_bfloat16* __restrict__ out,
+                                   const float* __restrict__ bias, int ncols) {
   if ((n & 3) == 0) {  // 16-byte loads, all S partials of a vector in flight at once
     const int64_t n4 = n >> 2;
     const float4* p4 = reinterpret_cast<const float4*>(part);
@@ -129,6 +130,13 @@ __global__ void splitk_bf16_kernel(const float* __restrict__ part, int S, int64_
         a.z += b.z;
         a.w += b.w;
       }
+      if (bias) {  // + bias[column] after the split sum (ncols % 4 == 0)
+        const float4 b = __ldg(reinterpret_cast<const float4*>(bias + (i * 4) % ncols));
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+      }
       __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
       uint2 w;
       w.x = *reinterpret_cast<uint32_t*>(&lo);
@@ -140,6 +148,7 @@ __global__ void splitk_bf16_kernel(const float* __restrict__ part, int S, int64_
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float s = part[i];
     for (int k = 1; k < S; ++k) s += part[(int64_t)k * n + i];
+    if (bias) s += bias[i % ncols];
     out[i] = __float2bfloat16_rn(s);
   }
 }
@@ -277,9 +286,24 @@ __global__ void sgd_kernel(float* __restrict__ theta, float* __restrict__ v, con
 // step graph is reused while the schedule changes lr), two float4 per thread
 // per iteration so a small grid (the SMs a recurrence leaves free) still
 // keeps enough bytes in flight.  Same rounding order as sgd_kernel.
-__global__ void sgd_lr_kernel(float* __restrict__ theta, float* __restrict__ v, const float* __restrict__ g,
+__device__ __forceinline__ void sgd_mirror4(const SgdMirror& m, int64_t i, float4 w) {
+  if (m.wpad && i >= m.wbeg && i < m.wbeg + m.wcnt) {  // 4 consecutive columns of one W_ih0 row
+    const int64_t r = (i - m.wbeg) / m.din, c = (i - m.wbeg) % m.din;
+    __nv_bfloat162 a = __floats2bfloat162_rn(w.x, w.y), b = __floats2bfloat162_rn(w.z, w.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&a);
+    pk.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(m.wpad + r * kInPad + c) = pk;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if (m.fdst[k] && i >= m.fbeg[k] && i < m.fbeg[k] + m.fcnt[k])
+      *reinterpret_cast<float4*>(m.fdst[k] + (i - m.fbeg[k])) =
+          make_float4(w.x * m.fscale[k], w.y * m.fscale[k], w.z * m.fscale[k], w.w * m.fscale[k]);
+}
+__global__ void __launch_bounds__(1024) sgd_lr_kernel(float* __restrict__ theta, float* __restrict__ v, const float* __restrict__ g,
                               const float* __restrict__ lr_dev, float mu, int64_t n, __nv_bfloat16* __restrict__ snap,
-                              int* __restrict__ flag) {
+                              int* __restrict__ flag, const SgdMirror mir, int use_mir) {
   const float lr = *lr_dev;
   const int64_t n4 = n / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -315,6 +339,7 @@ __global__ void sgd_lr_kernel(float* __restrict__ theta, float* __restrict__ v, 
         pk.y = *reinterpret_cast<uint32_t*>(&b);
         reinterpret_cast<uint2*>(snap)[idx[u]] = pk;
       }
+      if (use_mir) sgd_mirror4(mir, idx[u] * 4, w[u]);
     }
   }
   for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -518,8 +543,10 @@ int op_splitk_f32(const float* part, int S, int64_t n, float* out, cudaStream_t 
   return DS_OK;
 }
 
-int op_splitk_bf16(const float* part, int S, int64_t n, __nv_bfloat16* out, cudaStream_t s) {
-  splitk_bf16_kernel<<<ew_grid(n), kEW, 0, s>>>(part, S, n, out);
+int op_splitk_bf16(const float* part, int S, int64_t n, __nv_bfloat16* out, cudaStream_t s, const float* bias,
+                   int ncols) {
+  if (bias && (ncols < 4 || ncols % 4 || n % ncols)) return fail_arg("splitk_bf16: bias needs whole rows of 4k columns");
+  splitk_bf16_kernel<<<ew_grid(n), kEW, 0, s>>>(part, S, n, out, bias, ncols);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
@@ -548,14 +575,21 @@ int op_sgd(float* theta, float* v, const float* g, float lr, float mu, int64_t n
 }
 
 int op_sgd_lr(float* theta, float* v, const float* g, const float* lr_dev, float mu, int64_t n, __nv_bfloat16* snap,
-              int* flag, int max_blocks, cudaStream_t s) {
+              int* flag, int max_blocks, cudaStream_t s, const SgdMirror* mir) {
   if (((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(g)) & 15))
     return fail_arg("sgd: buffers must be 16-byte aligned");
+  if (mir) {  // the float4 path covers the mirrored ranges only when they are 4-aligned inside n / 4 * 4
+    bool ok = !mir->wpad || (mir->din % 4 == 0 && mir->wbeg % 4 == 0 && mir->wbeg + mir->wcnt <= n / 4 * 4);
+    for (int k = 0; k < 3; ++k)
+      ok = ok && (!mir->fdst[k] || (mir->fbeg[k] % 4 == 0 && mir->fcnt[k] % 4 == 0 && mir->fbeg[k] + mir->fcnt[k] <= n / 4 * 4));
+    if (!ok) return fail_arg("sgd mirror: ranges must be 4-aligned");
+  }
   const int threads = max_blocks > 0 ? 1024 : kEW;
   int64_t blocks = (n / 8 + threads - 1) / threads;
   const int64_t cap = max_blocks > 0 ? max_blocks : (int64_t)num_sms() * 8;
   blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
-  sgd_lr_kernel<<<(int)blocks, threads, 0, s>>>(theta, v, g, lr_dev, mu, n, snap, flag);
+  sgd_lr_kernel<<<(int)blocks, threads, 0, s>>>(theta, v, g, lr_dev, mu, n, snap, flag, mir ? *mir : SgdMirror(),
+                                                 mir ? 1 : 0);
   DS_CUDA_TRY(cudaGetLastError());
   return DS_OK;
 }
