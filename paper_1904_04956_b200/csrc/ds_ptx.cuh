@@ -142,6 +142,14 @@ DS_DEV uint32_t ld_relaxed_gpu(const uint32_t* p) {
   return v;
 }
 // 16-byte acquire load of four consecutive flags (one L2 round trip)
+DS_DEV uint4 ld_relaxed_gpu_v4(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
 DS_DEV uint4 ld_acquire_gpu_v4(const uint32_t* p) {
   uint4 v;
   asm volatile("ld.acquire.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"

@@ -1437,7 +1437,10 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
         }
         named_bar_sync(3, kEpi * 32);  // own-slice partials in recv; local expect below
         if (kEpiLead) mbar_arrive_expect_tx(&rfull[buf], (kKS - 1) * 2 * kBlock);
-        mbar_wait_acq_cluster(&rfull[buf], (it >> 1) & 1);
+        // the peers' partials arrive by bulk copies completing on rfull (async proxy, complete_tx): the
+        // phase flip makes them visible like a TMA load's, no cluster-scope acquire (an L1 invalidation
+        // per waiting warp) needed
+        mbar_wait(&rfull[buf], (it >> 1) & 1);
         if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 5);
 #pragma unroll
         for (int src = 0; src < kKS; ++src) {
