@@ -884,7 +884,11 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
         nl += 2;
       }
       DS_CUDA_TRY(cudaStreamWaitEvent(h->side3, h->ev_dw[l][0], 0));
-      gb.max_pairs = dw_pairs - dxp;
+      // beside BPTT_0 no dX runs: layer 1's weight gradients take its pairs too (its update then runs
+      // beside BPTT_0 instead of competing with the layer-0 gradients after it); the early layer-0
+      // gradients follow on the pairs it frees
+      static const bool dw1_all = !getenv("DS_DW1_ALL") || getenv("DS_DW1_ALL")[0] != '0';
+      gb.max_pairs = (l == 1 && dw1_all) ? dw_pairs : dw_pairs - dxp;
       gb.prio = h->prio_lo;
       gb.b_early = 0;  // its stream predecessor is the previous layer's dW, not BPTT_l
       // dW_l only once BPTT_{l-1} holds its SMs (dX_l runs alone on the machine first)
