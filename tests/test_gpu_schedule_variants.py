@@ -1,0 +1,81 @@
+"""The alternative schedules and kernels of the fused training step (environment switches read
+once per process, so each runs in a subprocess) against the default schedule on the same inputs:
+a 4-layer model with the paper's hidden sizes at B = 256, T = 21 (so the streamed dX with its
+per-direction halves, the triple-buffered dG, the split layer-0 weight gradients and the
+recurrent kernels' 2-tile launches all run), 3 fused momentum steps.
+
+  DS_DX_STREAM=0     dX after each BPTT on the main stream (one dY input)
+  DS_DW0_EARLY=0     layer-0 weight gradients after BPTT_0 only
+  DS_DW1_ALL=0       layer 1's weight gradients on the pairs dX leaves
+  DS_BWD=1           round 1's split-K BPTT (128 CTAs, no streamed dX)
+  DS_FWD=3           the 64-CTA forward recurrence (W_hh in tensor memory)
+  DS_NO_SGD_MIRROR=1 the operand-snapshot extras as a pass at the end of the step
+
+Bound: the same BF16 arithmetic in a different order (K splits, summation of the dY halves), so
+the trajectories agree to BF16 level: loss rel <= 1e-3, update rel <= 2e-2 over three steps,
+cosine >= 0.999.  Variants that only reorder independent work are bit-identical (checked)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from oracle import blstm_ref as O
+from paper_1904_04956_b200.blstm import BlstmObjective, DeviceDataset, Learner
+obj = BlstmObjective(layers=4, classes=2048, frames=21)
+spec = O.BlstmSpec(layers=4, input_dim=obj.input_dim, hidden=512, bottleneck=obj.bottleneck, classes=2048, frames=21)
+x, y, _, _ = O.make_dataset(spec, 768, seed=11)
+w = O.initial_weights(spec, 11)
+L = Learner(obj, DeviceDataset(x, y), max_batch=256, theta0=w)
+rng = np.random.default_rng(5)
+losses = []
+for lr in (0.05, 0.02, 0.08):
+    L.train_step(rng.permutation(len(x))[:256], lr)
+    L.check_finite()
+    losses.append(L.mean_loss())
+th = L.theta.double().cpu().numpy()
+np.save(sys.argv[1], np.concatenate([np.array(losses), th - w]))
+""" % ROOT
+
+
+def _run(tmp_path, env_extra, name):
+    out = tmp_path / f"{name}.npy"
+    env = dict(os.environ)
+    env.update(env_extra)
+    subprocess.run([sys.executable, "-c", SCRIPT, str(out)], check=True, env=env, timeout=600)
+    return np.load(out)
+
+
+@pytest.fixture(scope="module")
+def default_run(tmp_path_factory):
+    return _run(tmp_path_factory.mktemp("default"), {}, "default")
+
+
+@pytest.mark.parametrize("env,exact", [
+    ({"DS_DX_STREAM": "0"}, False),
+    ({"DS_DW0_EARLY": "0"}, False),
+    ({"DS_DW1_ALL": "0"}, True),
+    ({"DS_BWD": "1"}, False),
+    ({"DS_FWD": "3"}, True),
+    ({"DS_NO_SGD_MIRROR": "1"}, True),
+])
+def test_schedule_variant_matches_default(tmp_path, default_run, env, exact):
+    got = _run(tmp_path, env, "variant")
+    ref = default_run
+    loss_g, loss_r = got[:3], ref[:3]
+    d_g, d_r = got[3:], ref[3:]
+    if exact:
+        assert np.array_equal(got, ref), (env, np.abs(got - ref).max())
+        return
+    assert np.all(np.abs(loss_g - loss_r) <= 1e-3 * np.abs(loss_r)), (env, loss_g, loss_r)
+    rel = np.linalg.norm(d_g - d_r) / np.linalg.norm(d_r)
+    cos = float(d_g @ d_r / (np.linalg.norm(d_g) * np.linalg.norm(d_r)))
+    print(env, "update rel", rel, "cos", cos)
+    assert rel <= 2e-2 and cos >= 0.999, (env, rel, cos)
