@@ -194,12 +194,14 @@ constexpr int kChunkB = kNH * 128;      // 4 KB: 32 batch rows x 64 units bf16
 constexpr int kBufB = 8 * kChunkB;      // one step's B operand (32 KB)
 constexpr int kHst = kNB * 64;          // h staging: 64 batch rows x 32 units bf16 (4 KB)
 constexpr size_t kSmem = 1024 + kWB + 2 * kBufB + kHst + 512;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;             // lane quadrant x 16-column group (4 per SM sub-partition)
 constexpr int kEpiT = kEpiWarps * 32;
+constexpr int kThreadsF2 = 32 * (kEpiWarp0 + kEpiWarps);
+constexpr int kGC = 16;                    // batch columns per epilogue warp (TMEM load width)
 constexpr int kPub = 2;                 // named barriers 2/3: epilogue <-> publisher
 }  // namespace fwd2
 
-__global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_constant__ LstmParams P) {
+__global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __grid_constant__ LstmParams P) {
   using namespace fwd2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -326,25 +328,25 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     const uint32_t e = warp - kEpiWarp0;
-    const uint32_t q = e & 3, hc = e >> 2;      // TMEM lane quadrant, batch-column half
+    const uint32_t q = e & 3, hc = e >> 2;      // TMEM lane quadrant, 16-column batch group
     const uint32_t g = lane & 3;                 // gate of this thread's TMEM row (unit-interleaved rows)
     const uint32_t b0b = g & 1, b1b = g >> 1;
     const int uq = (int)(q * 8 + (lane >> 2));   // unit within the CTA's 32
     const int unit = pr * 64 + (int)rank * 32 + uq;  // unit within the direction
-    const int col0 = (int)(hc * 32 + g * 8);     // after the transpose: batch columns col0 .. +8
-    const uint32_t tcol = tmem + ((q * 32) << 16) + hc * 32;
+    const int col0 = (int)(hc * kGC + g * 4);    // after the transpose: batch columns col0 .. +4
+    const uint32_t tcol = tmem + ((q * 32) << 16) + hc * kGC;
     const uint32_t tempty_c = mapa_shared(smem_u32(tempty), 0);
     const size_t gcol = (size_t)dir * 4 * kH + (size_t)unit * 4;
-    float c[8];
+    float c[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) c[i] = 0.f;
+    for (int i = 0; i < 4; ++i) c[i] = 0.f;
     for (int s = 0; s < T; ++s) {
       if (s == T - 1) griddep_launch();  // the next kernel may start its prologue
       const int t = dir == 0 ? s : T - 1 - s;
-      // prefetch the input projection (i,f,g,o of this unit) for my 8 batch rows
-      uint2 gp[8];
+      // prefetch the input projection (i,f,g,o of this unit) for my 4 batch rows
+      uint2 gp[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 4; ++i) {
         const int b = b0 + col0 + i;
         gp[i] = b < B ? *reinterpret_cast<const uint2*>(P.gates + ((size_t)t * B + b) * (8 * kH) + gcol)
                       : make_uint2(0u, 0u);
@@ -352,8 +354,8 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
       mbar_wait(&tfull[s & 1], (s >> 1) & 1);
       tc_fence_after();
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 2);
-      float v[32];
-      tmem_ld32(tcol + (s & 1) * kNB, v);
+      float v[kGC];
+      tmem_ld16(tcol + (s & 1) * kNB, v);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
@@ -363,28 +365,28 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
         else
           mbar_arrive_remote(tempty_c + (s & 1) * 8);
       }
-      // quad transpose: stage 1 (lane ^ 2) splits the 32 columns in halves,
-      // stage 2 (lane ^ 1) in quarters -> 4 gates x 8 columns per lane
-      float a1[16], a2[16];  // a1: gate g, a2: gate g^2 (columns of my half)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float send = b1b ? v[i] : v[16 + i];
-        a1[i] = b1b ? v[16 + i] : v[i];
-        a2[i] = __shfl_xor_sync(0xffffffffu, send, 2);
-      }
-      float k1[8], k2[8], r1[8], r2[8];  // gates g, g^2 (kept), g^1, g^3 (received)
+      // quad transpose: stage 1 (lane ^ 2) splits the 16 columns in halves,
+      // stage 2 (lane ^ 1) in quarters -> 4 gates x 4 columns per lane
+      float a1[8], a2[8];  // a1: gate g, a2: gate g^2 (columns of my half)
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float s1 = b0b ? a1[i] : a1[8 + i];
-        const float s2 = b0b ? a2[i] : a2[8 + i];
-        k1[i] = b0b ? a1[8 + i] : a1[i];
-        k2[i] = b0b ? a2[8 + i] : a2[i];
+        const float send = b1b ? v[i] : v[8 + i];
+        a1[i] = b1b ? v[8 + i] : v[i];
+        a2[i] = __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      float k1[4], k2[4], r1[4], r2[4];  // gates g, g^2 (kept), g^1, g^3 (received)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float s1 = b0b ? a1[i] : a1[4 + i];
+        const float s2 = b0b ? a2[i] : a2[4 + i];
+        k1[i] = b0b ? a1[4 + i] : a1[i];
+        k2[i] = b0b ? a2[4 + i] : a2[i];
         r1[i] = __shfl_xor_sync(0xffffffffu, s1, 1);
         r2[i] = __shfl_xor_sync(0xffffffffu, s2, 1);
       }
-      float hv[8];
+      float hv[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 4; ++i) {
         // gate x lives in: d = g ^ x -> d0 ? (d1 ? r2 : r1) : (d1 ? k2 : k1)
         const float x0 = b0b ? (b1b ? r2[i] : r1[i]) : (b1b ? k2[i] : k1[i]);   // i gate (x = 0)
         const float x1 = b0b ? (b1b ? k2[i] : k1[i]) : (b1b ? r2[i] : r1[i]);   // f gate (x = 1)
@@ -406,15 +408,15 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 5);
       // h_t -> smem [64 rows][32 units] -> coalesced 16-byte stores
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 4; ++i)
         reinterpret_cast<__nv_bfloat16*>(sH)[(col0 + i) * 32 + uq] = __float2bfloat16_rn(hv[i]);
       named_bar_sync(1, kEpiT);
       {
-        const int tid = (int)(e * 32 + lane);  // 256 threads = 64 rows x 4 segments of 8 units
+        const int tid = (int)(e * 32 + lane);  // threads 0..255 = 64 rows x 4 segments of 8 units
         const int row = tid >> 2, sg = tid & 3;
         const int b = b0 + row;
-        const uint4 w = reinterpret_cast<const uint4*>(sH)[tid];
-        if (b < B && row < P.nb - bb * kNB)
+        const uint4 w = tid < kNB * 4 ? reinterpret_cast<const uint4*>(sH)[tid] : make_uint4(0u, 0u, 0u, 0u);
+        if (tid < kNB * 4 && b < B && row < P.nb - bb * kNB)
           *reinterpret_cast<uint4*>(P.y + ((size_t)(t + 1) * B + b) * (2 * kH) + dir * kH + pr * 64 + rank * 32 +
                                     sg * 8) = w;
       }
@@ -422,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_fwd2_kernel(const __grid_con
       asm volatile("bar.arrive %0, %1;" ::"n"(kPub), "n"(kEpiT + 32) : "memory");
       named_bar_sync(kPub + 1, kEpiT + 32);  // the release is out: BPTT state, then reuse sH
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 4; ++i) {
         const int b = b0 + col0 + i;
         if (b < B && col0 + i < P.nb - bb * kNB) {
           const size_t n = (size_t)t * B + b;
@@ -1674,7 +1676,7 @@ static const RecCaps& rec_caps() {
       return caps;
     }
     const int sm = num_sms() >= 132 ? 128 : num_sms();
-    const int f = cluster_cap((const void*)lstm_fwd2_kernel, fwd2::kSmem, 2);
+    const int f = cluster_cap((const void*)lstm_fwd2_kernel, fwd2::kSmem, 2, fwd2::kThreadsF2);
     const int f3 = cluster_cap((const void*)lstm_fwd3_kernel, fwd3::kSmem, 2, fwd3::kThreadsF);
     const int b = cluster_cap((const void*)lstm_bwd_kernel, bwd::kSmem, 4);
     const int b3 = cluster_cap((const void*)lstm_bwd3_kernel, bwd3::kSmem, 8, bwd3::kThreads3);
@@ -1764,7 +1766,8 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
       P.nb = nb;
       P.n_btile = (nb + fwd2::kNB - 1) / fwd2::kNB;  // 64-row blocks
       P.counters = a.counters;
-      rc = launch_coop((const void*)lstm_fwd2_kernel, 2 * fwd2::kCtas * P.n_btile, P, stream, fwd2::kSmem, 2);
+      rc = launch_coop((const void*)lstm_fwd2_kernel, 2 * fwd2::kCtas * P.n_btile, P, stream, fwd2::kSmem, 2,
+                       fwd2::kThreadsF2);
       if (rc) return rc;
       P.trace = nullptr;  // trace only the first chunk
     }
