@@ -17,7 +17,7 @@ if [ $MODE = ncu ]; then
 else
   for i in 1 2 3; do for v in new old; do
     use $v
-    echo -n "$v "; python bench.py --steps 60 --warmup 5 2>/dev/null | \
+    echo -n "$v "; python bench.py --steps 60 --warmup 5 --no-cpu --no-library 2>/dev/null | \
       python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['e2e']['value'])"
   done; done
 fi
