@@ -169,7 +169,16 @@ class Learner:
         self.grad = torch.zeros(P, dtype=torch.float32, device=dev)
         self.loss_sum = torch.zeros(1, dtype=torch.float32, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.idx = torch.zeros(max_batch, dtype=torch.int64, device=dev)
+        # minibatch indices: the step reads them from one of two device slots (one cached step graph
+        # per slot); a slot is filled on an input stream beside the previous step and the learner stream
+        # only waits for that copy's event, so nothing runs between two step graphs on it
+        self._islot = [torch.zeros(max_batch, dtype=torch.int64, device=dev) for _ in range(2)]
+        self._islot_ready = [torch.cuda.Event() for _ in range(2)]
+        self._islot_done = [torch.cuda.Event() for _ in range(2)]  # the step that read the slot has finished
+        self._islot_used = [False, False]
+        self._islot_i = 0
+        self._in_stream = torch.cuda.Stream(device=dev)
+        self.idx = self._islot[0]
         # ring of pinned staging buffers: a batch upload only waits for the
         # copy that used the same slot several uploads ago
         self._ring = [torch.zeros(max_batch, dtype=torch.int64).pin_memory() for _ in range(4)]
@@ -209,7 +218,24 @@ class Learner:
                    "ds_blstm_cast_snapshot")
 
     # -- hot path -------------------------------------------------------------
-    def _upload_batch(self, batch: np.ndarray) -> int:
+    def _stage(self, fill) -> int:
+        """Fill the next index slot on the input stream (`fill(slot_tensor, stream)`), make the learner
+        stream wait for it; returns the slot.  Call `_consumed(slot)` after queueing the step."""
+        r = self._islot_i
+        self._islot_i ^= 1
+        if self._islot_used[r]:
+            self._in_stream.wait_event(self._islot_done[r])  # the step that read it has run
+        fill(self._islot[r], self._in_stream)
+        self._islot_ready[r].record(self._in_stream)
+        self.stream.wait_event(self._islot_ready[r])
+        return r
+
+    def _consumed(self, r: int) -> None:
+        self._islot_done[r].record(self.stream)
+        self._islot_used[r] = True
+
+    def _upload_batch(self, batch: np.ndarray):
+        """Host indices -> pinned staging ring -> H2D copy into the next device slot.  Returns (B, slot)."""
         B = len(batch)
         if not 1 <= B <= self.max_batch:
             raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
@@ -217,40 +243,59 @@ class Learner:
         self._ring_i = (k + 1) % len(self._ring)
         ev = self._ring_ev[k]
         if self._ring_used[k]:
-            ev.synchronize()  # the slot's previous H2D copy has finished
+            ev.synchronize()  # the pinned slot's previous H2D copy has finished
         arr = np.ascontiguousarray(batch, dtype=np.int64)
         ctypes.memmove(self._ring_ptr[k], arr.ctypes.data, B * 8)  # into pinned memory
-        _lib.check(_lib.load().ds_device_copy(self.idx.data_ptr(), self._ring_ptr[k], B * 8, self.stream.cuda_stream),
-                   "ds_device_copy")
-        ev.record(self.stream)
+
+        def fill(dst, st):
+            _lib.check(_lib.load().ds_device_copy(dst.data_ptr(), self._ring_ptr[k], B * 8, st.cuda_stream),
+                       "ds_device_copy")
+            ev.record(st)
+
+        r = self._stage(fill)
         self._ring_used[k] = True
-        return B
+        return B, r
 
     def gradient(self, batch: np.ndarray) -> None:
         """gradient(objective, snapshot, batch, dataset) into self.grad
         (objectives.py:236-263); asynchronous on self.stream."""
-        B = self._upload_batch(batch)
+        B, r = self._upload_batch(batch)
         self.batch = B
         lib = _lib.load()
-        _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self.idx.data_ptr(), B, self.grad.data_ptr(),
+        _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self._islot[r].data_ptr(), B, self.grad.data_ptr(),
                                         self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
                    "ds_blstm_fwd_bwd")
+        self._consumed(r)
 
-    def gradient_device(self, idx_dev, B: int) -> None:
-        """Same as `gradient` for indices already resident on the device: a
-        device-to-device copy into the bound index buffer keeps the cached
-        CUDA graph and never synchronises the host."""
-        if not 1 <= B <= self.max_batch:
-            raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
+    def _stage_device(self, idx_dev, B: int) -> int:
+        """Device-resident int64 indices -> the next index slot (a device copy on the input stream,
+        after the caller's stream produced them).  Returns the slot."""
         import torch
 
-        with torch.cuda.stream(self.stream):
-            self.idx[:B].copy_(idx_dev[:B], non_blocking=True)
+        if not 1 <= B <= self.max_batch:
+            raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
+        if idx_dev.dtype != torch.int64 or idx_dev.device != self.theta.device or idx_dev.numel() < B:
+            raise ValueError("device indices must be an int64 tensor on the learner's device")
+        cur = torch.cuda.current_stream(self.theta.device)
+
+        def fill(dst, st):
+            st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                dst[:B].copy_(idx_dev.reshape(-1)[:B], non_blocking=True)
+            idx_dev.record_stream(st)
+
+        return self._stage(fill)
+
+    def gradient_device(self, idx_dev, B: int) -> None:
+        """Same as `gradient` for indices already resident on the device (never
+        synchronises the host)."""
+        r = self._stage_device(idx_dev, B)
         self.batch = B
         lib = _lib.load()
-        _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self.idx.data_ptr(), B, self.grad.data_ptr(),
+        _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self._islot[r].data_ptr(), B, self.grad.data_ptr(),
                                         self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
                    "ds_blstm_fwd_bwd")
+        self._consumed(r)
 
     def train_step(self, batch, lr: float, device_idx: bool = False) -> None:
         """gradient(...) then sgd_step(...) in one fused graph (engines/single.py:
@@ -260,21 +305,17 @@ class Learner:
         if lr <= 0:
             raise ValueError(f"learning rate must be > 0, got {lr}")
         if device_idx:
-            import torch
-
             B = int(batch.shape[0])
-            if not 1 <= B <= self.max_batch:
-                raise ValueError(f"batch of {B} sequences outside 1..{self.max_batch}")
-            with torch.cuda.stream(self.stream):
-                self.idx[:B].copy_(batch, non_blocking=True)
+            r = self._stage_device(batch, B)
         else:
-            B = self._upload_batch(batch)
+            B, r = self._upload_batch(batch)
         self.batch = B
         lib = _lib.load()
-        _lib.check(lib.ds_blstm_train_step(self.handle, self.idx.data_ptr(), B, self.theta.data_ptr(),
+        _lib.check(lib.ds_blstm_train_step(self.handle, self._islot[r].data_ptr(), B, self.theta.data_ptr(),
                                            self.vel.data_ptr(), self.grad.data_ptr(), float(lr), self.mu,
                                            self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
                    "ds_blstm_train_step")
+        self._consumed(r)
 
     def set_grad_scale(self, frames_total: float) -> None:
         """CE gradient divisor for the next gradients (0 = this batch's frames)."""
@@ -292,11 +333,12 @@ class Learner:
         return int(_lib.load().ds_blstm_kernel_count(self.handle))
 
     def loss(self, batch: np.ndarray) -> None:
-        B = self._upload_batch(batch)
+        B, r = self._upload_batch(batch)
         self.batch = B
         lib = _lib.load()
-        _lib.check(lib.ds_blstm_loss(self.handle, self.idx.data_ptr(), B, self.loss_sum.data_ptr(),
+        _lib.check(lib.ds_blstm_loss(self.handle, self._islot[r].data_ptr(), B, self.loss_sum.data_ptr(),
                                      self.flag.data_ptr(), self.stream.cuda_stream), "ds_blstm_loss")
+        self._consumed(r)
 
     def heldout_mean(self, idx: np.ndarray) -> float:
         """Mean CE over the sequences `idx` (held-out evaluation,
