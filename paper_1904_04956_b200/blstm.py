@@ -167,7 +167,11 @@ class Learner:
         self.theta = torch.zeros(P, dtype=torch.float32, device=dev)
         self.vel = torch.zeros(P, dtype=torch.float32, device=dev)
         self.grad = torch.zeros(P, dtype=torch.float32, device=dev)
-        self.loss_sum = torch.zeros(1, dtype=torch.float32, device=dev)
+        # the step's loss sum, per index slot (a read-back of one step's loss on the input stream never
+        # races the next step); self.loss_sum is the last launched step's
+        self._lslot = [torch.zeros(1, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.loss_sum = self._lslot[0]
+        self._last_slot = -1
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         # minibatch indices: the step reads them from one of two device slots (one cached step graph
         # per slot); a slot is filled on an input stream beside the previous step and the learner stream
@@ -230,9 +234,13 @@ class Learner:
         self.stream.wait_event(self._islot_ready[r])
         return r
 
+    def _use_slot(self, r: int) -> None:  # the step about to launch writes its loss into slot r
+        self.loss_sum = self._lslot[r]
+
     def _consumed(self, r: int) -> None:
         self._islot_done[r].record(self.stream)
         self._islot_used[r] = True
+        self._last_slot = r
 
     def _upload_batch(self, batch: np.ndarray):
         """Host indices -> pinned staging ring -> H2D copy into the next device slot.  Returns (B, slot)."""
@@ -261,6 +269,7 @@ class Learner:
         (objectives.py:236-263); asynchronous on self.stream."""
         B, r = self._upload_batch(batch)
         self.batch = B
+        self._use_slot(r)
         lib = _lib.load()
         _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self._islot[r].data_ptr(), B, self.grad.data_ptr(),
                                         self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
@@ -291,6 +300,7 @@ class Learner:
         synchronises the host)."""
         r = self._stage_device(idx_dev, B)
         self.batch = B
+        self._use_slot(r)
         lib = _lib.load()
         _lib.check(lib.ds_blstm_fwd_bwd(self.handle, self._islot[r].data_ptr(), B, self.grad.data_ptr(),
                                         self.loss_sum.data_ptr(), self.flag.data_ptr(), self.stream.cuda_stream),
@@ -310,6 +320,7 @@ class Learner:
         else:
             B, r = self._upload_batch(batch)
         self.batch = B
+        self._use_slot(r)
         lib = _lib.load()
         _lib.check(lib.ds_blstm_train_step(self.handle, self._islot[r].data_ptr(), B, self.theta.data_ptr(),
                                            self.vel.data_ptr(), self.grad.data_ptr(), float(lr), self.mu,
@@ -335,6 +346,7 @@ class Learner:
     def loss(self, batch: np.ndarray) -> None:
         B, r = self._upload_batch(batch)
         self.batch = B
+        self._use_slot(r)
         lib = _lib.load()
         _lib.check(lib.ds_blstm_loss(self.handle, self._islot[r].data_ptr(), B, self.loss_sum.data_ptr(),
                                      self.flag.data_ptr(), self.stream.cuda_stream), "ds_blstm_loss")
@@ -388,19 +400,24 @@ class Learner:
             raise _lib.DsError("recurrent kernel flag wait timed out (CTAs not co-resident?)")
 
     def loss_async(self):
-        """Queue the read-back of the last step's loss on the learner stream and
-        return a callable that waits for that copy and gives the mean CE: the
-        host can issue the next step before the loss arrives (pinned 4-slot ring;
-        call each callable before issuing four more)."""
+        """Queue the read-back of the last step's loss and return a callable that
+        waits for that copy and gives the mean CE: the host can issue the next
+        step before the loss arrives (pinned 4-slot ring; call each callable
+        before issuing four more).  The copy runs on the input stream once the
+        step has finished (its loss slot is not reused before the next-but-one
+        step), so nothing is queued between two steps on the learner stream."""
         k = self._loss_i
         self._loss_i = (k + 1) % len(self._loss_ev)
         ev = self._loss_ev[k]
         if self._loss_used[k]:
             ev.synchronize()  # the slot's previous copy was consumed
         ptr = self._loss_ptr + 4 * k
-        _lib.check(_lib.load().ds_device_copy(ptr, self.loss_sum.data_ptr(), 4, self.stream.cuda_stream),
-                   "ds_device_copy")
-        ev.record(self.stream)
+        st = self.stream
+        if self._last_slot >= 0:
+            st = self._in_stream
+            st.wait_event(self._islot_done[self._last_slot])
+        _lib.check(_lib.load().ds_device_copy(ptr, self.loss_sum.data_ptr(), 4, st.cuda_stream), "ds_device_copy")
+        ev.record(st)
         self._loss_used[k] = True
         slots, denom = self._loss_slots, float(self.batch * self.obj.frames)
 
