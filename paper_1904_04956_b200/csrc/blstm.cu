@@ -299,7 +299,8 @@ int carve(ds_blstm* h, char* base, size_t* total) {
   }
   {  // split-K fp32 partials: dZ (K = classes) and dW_b (K = frames)
     const int64_t s1 = (int64_t)kDzPartMax * N * L.bottleneck, s2 = (int64_t)kWbSplit * L.bottleneck * kLayerOut;
-    h->splitk = a.take<float>(base, s1 > s2 ? s1 : s2);
+    const int64_t s3 = L.off_b[0] - L.off_wih[0];  // the late layer-0 weight gradients of the fused step
+    h->splitk = a.take<float>(base, std::max(std::max(s1, s2), s3));
   }
   h->counters = a.take<uint32_t>(base, counter_words_total(h));
   h->d_lr = a.take<float>(base, 4);
@@ -360,6 +361,8 @@ int mark(ds_blstm* h, int kind, cudaStream_t s) {
 // gradient is final.  side: on the handle's side stream (<= 16 SMs, the ones
 // a recurrence leaves free), forked from / joined back into `s`.
 struct SgdCtx {
+  const float* add0 = nullptr;     // layer 0: late weight-gradient part to sum into the gradient in its update
+  int64_t add0_n = 0;
   float* theta = nullptr;
   float* vel = nullptr;
   float mu = 0.f;
@@ -447,7 +450,11 @@ int sgd_segment(ds_blstm* h, SgdCtx& c, float* grad, int* flag, int64_t off, int
     DS_CUDA_TRY(cudaEventRecord(h->ev_join[k], h->side));
     return DS_OK;
   }
-  const SgdMirror mir = segment_mirror(h, off, n);
+  SgdMirror mir = segment_mirror(h, off, n);
+  if (c.add0 && off == h->L.off_wih[0]) {
+    mir.add = c.add0;
+    mir.add_n = c.add0_n;
+  }
   if (!side)
     return op_sgd_lr(c.theta + off, c.vel + off, grad + off, h->d_lr, c.mu, n, h->snap + off, flag, 0, s,
                      c.mirror ? &mir : nullptr);
@@ -922,6 +929,10 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       GemmBatch ge, gl;
       memset(&ge, 0, sizeof(ge));
       memset(&gl, 0, sizeof(gl));
+      // fused step: the late part goes to scratch (plain stores) and the layer-0 update sums it in
+      // (a streaming pass), instead of an accumulate epilogue re-reading the early part row by row
+      const bool late_scratch = sg.theta && !sg.grp && sg.mirror;
+      const int64_t w0 = L.off_b[0] - L.off_wih[0];  // W_ih0 + W_hh0
       for (int part = 0; part < 2; ++part) {
         GemmBatch& g = part ? gl : ge;
         for (int d = 0; d < 2; ++d) {
@@ -936,6 +947,10 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
           pi.epi = EPI_F32;
           pi.out = grad + L.off_wih[0] + (size_t)d * kGates * L.input_dim;
           pi.accumulate = part;
+          if (part && late_scratch) {
+            pi.out = h->splitk + (size_t)d * kGates * L.input_dim;
+            pi.accumulate = 0;
+          }
           GemmProblem& ph = g.p[g.nprob++];  // dW_hh0[d] = dG[:, dir d]^T H_prev[d]
           const __nv_bfloat16* hp = d == 0 ? h->yfull[0] : h->yfull[0] + (size_t)2 * B * kLayerOut + kHidden;
           TRY(gemm_problem(&ph, dgl + (size_t)r0 * kGates2 + (size_t)d * kGates, kGates2, 1, hp + (size_t)r0 * kLayerOut,
@@ -944,6 +959,10 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
           ph.out = grad + L.off_whh[0] + (size_t)d * kGates * kHidden;
           ph.ldo = kHidden;
           ph.accumulate = part;
+          if (part && late_scratch) {
+            ph.out = h->splitk + (L.off_whh[0] - L.off_wih[0]) + (size_t)d * kGates * kHidden;
+            ph.accumulate = 0;
+          }
         }
       }
       const uint32_t* g0 = gate_words(h, 0);
@@ -953,8 +972,16 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
       TRY(gemm_launch(&ge, h->side4));
       TL("dW0-early", h->side4);
       DS_CUDA_TRY(cudaEventRecord(h->ev_x[0], h->side4));
-      DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_x[0], 0));
+      // into scratch the late part does not depend on the early one: only the update joins them
+      if (!late_scratch) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_x[0], 0));
+      gl.trace = gemm_layer_trace(0);  // tools/dx_trace.py 0 traces this late part
+      gl.trace_keep = gl.trace != nullptr;
       TRY(gemm_launch(&gl, s));
+      if (late_scratch) {
+        DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_x[0], 0));
+        sg.add0 = h->splitk;
+        sg.add0_n = w0;
+      }
       nl += 3;
     } else {
       TRY(gemm_launch(&gb, s));

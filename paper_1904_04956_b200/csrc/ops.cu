@@ -317,6 +317,14 @@ __global__ void __launch_bounds__(1024) sgd_lr_kernel(float* __restrict__ theta,
         w[u] = reinterpret_cast<float4*>(theta)[idx[u]];
         vv[u] = reinterpret_cast<float4*>(v)[idx[u]];
         gg[u] = reinterpret_cast<const float4*>(g)[idx[u]];
+        if (use_mir && mir.add && idx[u] * 4 < mir.add_n) {  // second gradient part, sum stored back
+          const float4 a = reinterpret_cast<const float4*>(mir.add)[idx[u]];
+          gg[u].x += a.x;
+          gg[u].y += a.y;
+          gg[u].z += a.z;
+          gg[u].w += a.w;
+          reinterpret_cast<float4*>(const_cast<float*>(g))[idx[u]] = gg[u];
+        }
       }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -580,6 +588,8 @@ int op_sgd_lr(float* theta, float* v, const float* g, const float* lr_dev, float
     return fail_arg("sgd: buffers must be 16-byte aligned");
   if (mir) {  // the float4 path covers the mirrored ranges only when they are 4-aligned inside n / 4 * 4
     bool ok = !mir->wpad || (mir->din % 4 == 0 && mir->wbeg % 4 == 0 && mir->wbeg + mir->wcnt <= n / 4 * 4);
+    ok = ok && (!mir->add || (mir->add_n % 4 == 0 && mir->add_n <= n / 4 * 4 &&
+                              (reinterpret_cast<uintptr_t>(mir->add) & 15) == 0));
     for (int k = 0; k < 3; ++k)
       ok = ok && (!mir->fdst[k] || (mir->fbeg[k] % 4 == 0 && mir->fcnt[k] % 4 == 0 && mir->fbeg[k] + mir->fcnt[k] <= n / 4 * 4));
     if (!ok) return fail_arg("sgd mirror: ranges must be 4-aligned");

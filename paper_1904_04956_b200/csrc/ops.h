@@ -32,6 +32,10 @@ struct SgdMirror {
   float* fdst[3] = {};
   int64_t fbeg[3] = {}, fcnt[3] = {};
   float fscale[3] = {1.f, 1.f, 1.f};
+  // a second gradient part summed in first (g[i] += add[i] for i < add_n, the sum stored back into g):
+  // the layer-0 weight gradients computed after BPTT_0, added to the part computed beside it
+  const float* add = nullptr;
+  int64_t add_n = 0;
 };
 // lr from device memory; max_blocks > 0: at most that many 1024-thread blocks
 int op_sgd_lr(float* theta, float* v, const float* g, const float* lr_dev, float mu, int64_t n, __nv_bfloat16* snap,

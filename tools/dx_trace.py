@@ -3,7 +3,7 @@ config-2 training step (B=256): per CTA pair, every unit's tile index, when
 its producer started waiting for the BPTT gate and when the gate passed, when
 the MMA issuer started / finished it and when its epilogue ended, in us from
 the step start, next to the step timeline (DS_TIMELINE marks).
-Usage (GPU box):  python tools/dx_trace.py [layer=3]"""
+Usage (GPU box):  python tools/dx_trace.py [layer=3]   (layer 0: the late layer-0 weight gradients)"""
 import ctypes
 import os
 import sys
@@ -39,7 +39,8 @@ for line in tl.value.decode().splitlines():
     n, v = line.split()
     marks[n] = float(v)
 base = marks.pop("base_ns")
-for n in (f"pre-bptt{layer}", f"bptt{layer}", f"dX{layer}", f"pre-bptt{layer - 1}", f"bptt{layer - 1}"):
+for n in (f"pre-bptt{layer}", f"bptt{layer}", f"dX{layer}", f"pre-bptt{layer - 1}", f"bptt{layer - 1}", "dW0-early",
+          "grp0", "sgd-main", "end"):
     if n in marks:
         print(f"{n:>12s} {marks[n] * 1e3:8.1f} us")
 t = buf.cpu().numpy().reshape(160, TILES, FIELDS).astype(np.float64)
