@@ -173,7 +173,7 @@ int dw0_early() {  // frames per direction of layer 0's weight gradients compute
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DS_DW0_EARLY");
-    v = e ? atoi(e) : 10;
+    v = e ? atoi(e) : 8;
     if (v < 0) v = 0;
   }
   return v;
