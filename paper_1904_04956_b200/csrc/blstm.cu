@@ -593,7 +593,9 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   if (dw_pairs < 1) dw_pairs = 1;
   // dX_l streamed behind BPTT_l (side4, direction-split units finished in the kernel) and consumed by
   // BPTT_{l-1} frame by frame: its per-step counters are zeroed on side2 beside the output layer
-  const bool xstream = ovl && use_dx_stream() && B % 32 == 0;
+  // (not with an SSGD group attached: with two learners time-sliced on one device, --same-device, the
+  // group barriers timed out against the spin-gated streams; the group step keeps stream-ordered dX)
+  const bool xstream = ovl && use_dx_stream() && B % 32 == 0 && !sg.grp;
   const int dxp = xstream ? std::min(dx_pairs(), dw_pairs - 1) : 0;
   if (xstream) {
     DS_CUDA_TRY(cudaEventRecord(h->ev_gz[0], s));
