@@ -199,7 +199,7 @@ size_t counter_words_total(const ds_blstm* h) { return lstm_counter_words(h->Bma
 // up first under a simple cost model (a BPTT step ~ 14 k-blocks of a pair tile).
 int dx_schedule(GemmBatch& g, int pairs, int B, int T) {
   struct Unit {
-    int avail, tile;
+    int avail, need, tile;
     double dur;
   };
   std::vector<Unit> us;
@@ -207,17 +207,26 @@ int dx_schedule(GemmBatch& g, int pairs, int B, int T) {
   for (int d = 0; d < g.nprob; ++d) {
     const GemmProblem& P = g.p[d];
     const int n = P.tiles_m * P.tiles_n;
-    for (int local = 0; local < n; ++local) {  // the kernel's mapping: row tile fastest
-      const int tm = local % P.tiles_m;
+    for (int local = 0; local < n; ++local) {  // the kernel's mapping: row tile fastest, then column tile
+      const int tm = local % P.tiles_m, tn = local / P.tiles_m;
       const int r0 = tm * 2 * kGemmBM, r1 = std::min(r0 + 2 * kGemmBM, P.M) - 1;
-      int avail = 0;
-      for (int t = r0 / B; t <= r1 / B; ++t) avail = std::max(avail, d == 0 ? T - 1 - t : t);
-      us.push_back({avail, begin + local, (P.K + kGemmBK - 1) / kGemmBK + 3.0});
+      // the dY columns of the tile belong to the next BPTT's direction u (units u*512 ..), which reads
+      // frame t at its step T-1-t (u = 0) or t (u = 1): among units released at the same step, the
+      // ones that BPTT needs first go first
+      const int u = (tn * kGemmBN) / kHidden;
+      int avail = 0, need = T;
+      for (int t = r0 / B; t <= r1 / B; ++t) {
+        avail = std::max(avail, d == 0 ? T - 1 - t : t);
+        need = std::min(need, u == 0 ? T - 1 - t : t);
+      }
+      us.push_back({avail, need, begin + local, (P.K + kGemmBK - 1) / kGemmBK + 3.0});
     }
     begin += n;
   }
   if ((int)us.size() > kMaxSched || pairs > kMaxPairs) return fail_arg("streamed dX: too many units");
-  std::stable_sort(us.begin(), us.end(), [](const Unit& a, const Unit& b) { return a.avail < b.avail; });
+  std::stable_sort(us.begin(), us.end(), [](const Unit& a, const Unit& b) {
+    return a.avail != b.avail ? a.avail < b.avail : a.need < b.need;
+  });
   std::vector<double> fr(pairs, 0.0);
   std::vector<std::vector<int>> lists(pairs);
   for (const Unit& u : us) {
