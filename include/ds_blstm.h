@@ -160,6 +160,10 @@ int ds_debug_gemm_bf16(const void* A, int64_t lda, int32_t a_mn, const void* B, 
  * aid for tools/gemm_trace.py and tools/cedz_trace.py; never used on the
  * product path. */
 int ds_debug_gemm_trace(void* buf, int32_t launch);
+/* debug: marks (globaltimer ns) of the BPTT of `layer` inside the step graph, layout of
+ * tools/bwd_step_trace.py ([CTA][step][6] + per-chunk slots; null: off); takes effect at the next
+ * graph capture */
+int ds_debug_bptt_trace(void* buf, int32_t layer);
 
 /* ---------------------------------------------------------------------------
  * Multi-process data parallelism (one process per GPU, NVLink P2P).

@@ -46,6 +46,7 @@ SIGNATURES = {
     "ds_blstm_kernel_count": (_I32, [_VP]),
     "ds_blstm_profile_list": (_I32, [_VP, _VP, _VP, _I32, _VP]),
     "ds_debug_gemm_trace": (_I32, [_VP, _I32]),
+    "ds_debug_bptt_trace": (_I32, [_VP, _I32]),
     "ds_debug_gemm_bf16": (_I32, [_VP, _I64, _I32, _VP, _I64, _I32, _VP, _I64, _I32, _I32, _I32, _VP]),
     "ds_debug_lstm_fwd": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ds_debug_lstm_bwd": (_I32, [_I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),

@@ -246,6 +246,9 @@ int dx_schedule(GemmBatch& g, int pairs, int B, int T) {
   g.presched = pairs;
   return DS_OK;
 }
+// debug (tools/bptt_insitu.py): per-(CTA, step) marks of one layer's BPTT inside the step graph
+uint64_t* g_bptt_trace = nullptr;
+int g_bptt_layer = -1;
 int fused_dz_splits(const ds_blstm* h, int N) {
   // h->splitk holds kDzPartMax x N x bottleneck floats
   return ce_grad_dz_splits(N, h->L.classes, kDzPartMax);
@@ -796,7 +799,8 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
     if (xstream && l == Lh - 1) DS_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_gz[1], 0));  // counters zeroed
     const bool dy_streamed = xstream && l + 1 < Lh;  // dY = the two halves of dX_{l+1}
     LstmLayerArgs la{B, T, h->gates[l], h->cstate[l], h->yfull[l], h->snap + L.off_whh[l],
-                     dy_streamed ? h->dyx[(l + 1) & 1][0] : h->dy, dgl, h->counters, nullptr, bpl};
+                     dy_streamed ? h->dyx[(l + 1) & 1][0] : h->dy, dgl, h->counters,
+                     l == g_bptt_layer ? g_bptt_trace : nullptr, bpl};
     la.err = flag;
     if (ovl) {
       la.prio = h->prio_hi;
@@ -1412,6 +1416,12 @@ int ds_debug_timeline(ds_blstm* h, char* buf, int32_t len) {
   for (int i = 0; i < h->tl_n; ++i) out += h->tl_name[i] + " " + std::to_string((double)(t[i] - t[0]) * 1e-6) + "\n";
   if (h->tl_n > 0) out += "base_ns " + std::to_string(t[0]) + "\n";  // absolute globaltimer of "start"
   snprintf(buf, (size_t)len, "%s", out.c_str());
+  return DS_OK;
+}
+
+int ds_debug_bptt_trace(void* buf, int32_t layer) {
+  g_bptt_trace = static_cast<uint64_t*>(buf);
+  g_bptt_layer = buf ? layer : -1;
   return DS_OK;
 }
 

@@ -1194,6 +1194,7 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
       P.counters + (size_t)(P.b0 / 128 + btile) * kFlagWords128 + dir * kGroupFlagWords + kFlagLine0 * kFlagLine;
   uint32_t* myflag = flags + (uh * 2 + r) * kFlagLine + ks;
 
+  if (threadIdx.x == 0) trace_mark(P.trace, T, 0, 0);  // (slot 0 of step 0 is unused below: launch start)
   if (warp == kProdWarp && lane == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
@@ -1255,6 +1256,7 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
     st_release_gpu(P.seq + 1, ld_relaxed_gpu(P.seq) * 16u + (uint32_t)P.tag);  // epoch: bumped by the step's gather
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_mark(P.trace, T, 0, 1);  // prologue done (W^T in TMEM, predecessor waited)
   const uint32_t base = s_base;  // flag value at launch start (same for every flag of the group)
 
   if (warp == kProdWarp) {
