@@ -511,7 +511,24 @@ int issue_step(ds_blstm* h, const int64_t* idx, int B, float* grad, float* loss,
   auto Y = [&](int l) { return h->yfull[l] + (size_t)B * kLayerOut; };
 
   // ---- forward ----
+  // layer 0's input projection (K = 272) inside its recurrence (DS_FWD_XFUSE=0: a GEMM before it)
+  static const bool xfuse = (!getenv("DS_FWD_XFUSE") || getenv("DS_FWD_XFUSE")[0] != '0') &&
+                            !(getenv("DS_FWD") && getenv("DS_FWD")[0] == '3');
   for (int l = 0; l < Lh; ++l) {
+    if (l == 0 && xfuse) {
+      LstmLayerArgs la{B, T, h->gates[0], h->cstate[0], h->yfull[0], h->snap + L.off_whh[0], nullptr, nullptr,
+                       h->counters};
+      la.err = flag;
+      la.xin = h->x0;
+      la.wih = h->wih0pad;
+      la.xbias = bias_l;
+      MARK(PH_LSTM_FWD);
+      TRY(lstm_forward(la, s));
+      TL("proj0", s);
+      TL("fwd0", s);
+      nl += 1 + (B - 1) / (128 * lstm_max_tiles());
+      continue;
+    }
     GemmBatch gb;
     memset(&gb, 0, sizeof(gb));
     gb.nprob = 1;

@@ -26,6 +26,7 @@
 
 #include "ds_internal.h"
 #include "ds_ptx.cuh"
+#include "layout.h"
 #include "lstm_rec.h"
 
 #include <cstdlib>
@@ -193,7 +194,11 @@ constexpr int kWB = 128 * kH * 2;       // 128 KB resident W slice
 constexpr int kChunkB = kNH * 128;      // 4 KB: 32 batch rows x 64 units bf16
 constexpr int kBufB = 8 * kChunkB;      // one step's B operand (32 KB)
 constexpr int kHst = kNB * 64;          // h staging: 64 batch rows x 32 units bf16 (4 KB)
-constexpr size_t kSmem = 1024 + kWB + 2 * kBufB + kHst + 512;
+constexpr int kXKb = 5;                   // fused input projection: K = 272 padded to 5 blocks of 64
+constexpr int kXB = kXKb * kChunkB;        // one step's x tile per CTA (32 rows x 320 K, 20 KB)
+constexpr uint32_t kXCol = 128;           // W_ih slice in TMEM columns 128 .. 287 (two bf16 per column)
+constexpr size_t kSmem = 1024 + kWB + 2 * kBufB + kHst + 1024;  // + kXB for the fused input projection
+constexpr size_t kSmemX = kSmem + kXB;
 constexpr int kEpiWarps = 16;             // lane quadrant x 16-column group (4 per SM sub-partition)
 constexpr int kEpiT = kEpiWarps * 32;
 constexpr int kThreadsF2 = 32 * (kEpiWarp0 + kEpiWarps);
@@ -201,6 +206,9 @@ constexpr int kGC = 16;                    // batch columns per epilogue warp (T
 constexpr int kPub = 2;                 // named barriers 2/3: epilogue <-> publisher
 }  // namespace fwd2
 
+// kX: layer 0's input projection fused in (a separate instantiation: the hot loops of the plain one
+// carry none of its code)
+template <bool kX>
 __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __grid_constant__ LstmParams P) {
   using namespace fwd2;
   extern __shared__ uint8_t smem_raw[];
@@ -212,7 +220,12 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
   uint64_t* wbar = full + 16;
   uint64_t* tfull = wbar + 1;   // [2]
   uint64_t* tempty = tfull + 2;  // [2], leader: every epilogue warp of both CTAs
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xfull = tempty + 2;  // leader: both CTAs' x tile of the step
+  uint64_t* xempty = xfull + 1;  // every CTA: the pair's x MMAs read the tile
+  uint64_t* wibar = xempty + 1;  // launch: W_ih boxes staged
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wibar + 1);
+  uint8_t* sX = sH + kHst + 1024;         // fused input projection only: [5 K blocks][32 rows x 128 B]
+  constexpr bool xin = kX;
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();  // 0 = leader
@@ -235,9 +248,12 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * kEpiWarps);
     }
+    mbar_init(xfull, 1);
+    mbar_init(xempty, 1);
+    mbar_init(wibar, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc_pair(tmem_slot, 128);
+  if (warp == 2) tmem_alloc_pair(tmem_slot, xin ? 512 : 128);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -251,6 +267,46 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
     mbar_arrive_expect_tx(wbar, kWB);
     const int wrow = dir * 4 * kH + pr * 256 + (int)rank * 128;
     for (int kb = 0; kb < kH / 64; ++kb) tma_load_2d(sW + kb * 16384, &P.tmW, wbar, kb * 64, wrow);
+  }
+  if (xin) {
+    // W_ih rows of this CTA (128 gate rows x 320 K) into TMEM, staged through the B buffers (64 KB) in
+    // two rounds: K blocks 0-3, then 4; lane = gate row, column c = K (2c, 2c+1), SW128 chunks
+    const int wrow = dir * 4 * kH + pr * 256 + (int)rank * 128;
+    for (int round = 0; round < 2; ++round) {
+      const int kb0 = round * 4, nkb = round ? kXKb - 4 : 4;
+      if (threadIdx.x == 0) {
+        if (round == 0) tma_prefetch_desc(&P.tmWi);
+        mbar_arrive_expect_tx(wibar, nkb * 16384);
+        for (int j = 0; j < nkb; ++j) tma_load_2d(sB + j * 16384, &P.tmWi, wibar, (kb0 + j) * 64, wrow);
+      }
+      if (warp >= kEpiWarp0) {
+        const uint32_t e = warp - kEpiWarp0, q = e & 3, grp = e >> 2;  // 4 groups split the staged blocks
+        const uint32_t m = q * 32 + lane;
+        mbar_wait(wibar, (uint32_t)round);
+        for (int j = (int)grp; j < nkb; j += 4) {
+          const uint8_t* row = sB + j * 16384 + m * 128;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t rr[16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint4 w = *reinterpret_cast<const uint4*>(row + (((half * 4 + c) ^ (m & 7)) << 4));
+              rr[4 * c] = w.x;
+              rr[4 * c + 1] = w.y;
+              rr[4 * c + 2] = w.z;
+              rr[4 * c + 3] = w.w;
+            }
+            tmem_st16(tmem + ((q * 32) << 16) + kXCol + (uint32_t)(kb0 + j) * 32 + half * 16, rr);
+          }
+        }
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncthreads();  // the staging area is read (round 0) / free for the B operand (round 1)
+      tc_fence_after();
+    }
+    cluster_sync_all();  // the partner's W_ih in its TMEM before the first pair MMA
+    tc_fence_after();
   }
   griddep_wait();
   if (threadIdx.x == 0) s_base = ld_relaxed_gpu(flags + (pr >> 2) * 8 + (pr & 3) * 2 + (int)rank);
@@ -268,6 +324,13 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
         const int tprev = dir == 0 ? t - 1 : t + 1;
         const int arow = (tprev + 1) * B + b0 + (int)rank * kNH;
         const int buf = s & 1;
+        if (xin) {  // x_t of my 32 batch rows, once the pair's x MMAs of the previous step read the tile
+          if (s > 0) mbar_wait(xempty, (uint32_t)(s - 1) & 1);
+          if (leader) mbar_arrive_expect_tx(xfull, 2 * kXB);
+          const uint32_t xfull_c = mapa_shared(smem_u32(xfull), 0);
+          for (int j = 0; j < kXKb; ++j)
+            tma_load_2d_pair(sX + j * kChunkB, &P.tmX, xfull_c, j * 64, t * B + b0 + (int)rank * kNH);
+        }
         for (int k = 0; k < kPairs; ++k) {
           uint64_t* fb = &full[buf * 8 + k];
           if (leader) mbar_arrive_expect_tx(fb, 2 * kChunkB);
@@ -294,6 +357,21 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
         mbar_wait_acq_cluster(&tempty[acc], ((s >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t dacc = tmem + acc * kNB;
+        if (xin) {  // x_t W_ih^T first: its operands do not wait for the previous step
+          mbar_wait(xfull, (uint32_t)s & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t xb = smem_u32(sX);
+#pragma unroll 1
+            for (int j = 0; j < kXKb; ++j)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16_ts_pair(dacc, tmem + kXCol + (uint32_t)(j * 4 + kk) * 8,
+                                 smem_desc_sw128(xb + j * kChunkB + kk * 32, 16, 1024), idesc, (j | kk) != 0);
+            mma_commit_pair_mc(xempty, 0x3);
+          }
+          __syncwarp();
+        }
         for (int k = 0; k < kPairs; ++k) {
           mbar_wait(&full[buf * 8 + k], (s >> 1) & 1);
           tc_fence_after();
@@ -304,7 +382,7 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
             for (int kk = 0; kk < 4; ++kk) {
               uint64_t ad = smem_desc_sw128(wbase + k * 16384 + kk * 32, 16, 1024);
               uint64_t bd = smem_desc_sw128(bbase + buf * kBufB + k * kChunkB + kk * 32, 16, 1024);
-              mma_bf16_ss_pair(dacc, ad, bd, idesc, (k | kk) != 0);
+              mma_bf16_ss_pair(dacc, ad, bd, idesc, xin || (k | kk) != 0);
             }
             if (k == kPairs - 1) mma_commit_pair_mc(&tfull[acc], 0x3);
           }
@@ -340,6 +418,7 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
     float c[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) c[i] = 0.f;
+    const float4 xb4 = xin ? *reinterpret_cast<const float4*>(P.xbias + gcol) : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < T; ++s) {
       if (s == T - 1) griddep_launch();  // the next kernel may start its prologue
       const int t = dir == 0 ? s : T - 1 - s;
@@ -348,8 +427,8 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int b = b0 + col0 + i;
-        gp[i] = b < B ? *reinterpret_cast<const uint2*>(P.gates + ((size_t)t * B + b) * (8 * kH) + gcol)
-                      : make_uint2(0u, 0u);
+        gp[i] = b < B && !xin ? *reinterpret_cast<const uint2*>(P.gates + ((size_t)t * B + b) * (8 * kH) + gcol)
+                              : make_uint2(0u, 0u);
       }
       mbar_wait(&tfull[s & 1], (s >> 1) & 1);
       tc_fence_after();
@@ -393,7 +472,11 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
         const float x2 = b0b ? (b1b ? r1[i] : r2[i]) : (b1b ? k1[i] : k2[i]);   // g gate (x = 2)
         const float x3 = b0b ? (b1b ? k1[i] : k2[i]) : (b1b ? r1[i] : r2[i]);   // o gate (x = 3)
         const __nv_bfloat162* gg = reinterpret_cast<const __nv_bfloat162*>(&gp[i]);
-        const float2 g01 = __bfloat1622float2(gg[0]), g23 = __bfloat1622float2(gg[1]);
+        float2 g01 = __bfloat1622float2(gg[0]), g23 = __bfloat1622float2(gg[1]);
+        if (xin) {  // the accumulator holds x_t W_ih^T + h W_hh^T: add the bias
+          g01 = make_float2(xb4.x, xb4.y);
+          g23 = make_float2(xb4.z, xb4.w);
+        }
         const float ig = sigmoid_fast(x0 + g01.x);
         const float fg = sigmoid_fast(x1 + g01.y);
         const float gt = tanh_fast(x2 + g23.x);
@@ -439,7 +522,7 @@ __global__ void __launch_bounds__(fwd2::kThreadsF2, 1) lstm_fwd2_kernel(const __
   __syncthreads();
   cluster_sync_all();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc_pair(tmem, 128);
+  if (warp == 2) tmem_dealloc_pair(tmem, xin ? 512 : 128);
 }
 
 // ============================================================================
@@ -1665,20 +1748,22 @@ static const RecCaps& rec_caps() {
   static bool done = false;
   if (!done) {
     done = true;
-    if (cudaFuncSetAttribute(lstm_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd2::kSmem) !=
+    if (cudaFuncSetAttribute(lstm_fwd2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd2::kSmem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(lstm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(lstm_bwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd3::kSmem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(lstm_fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd3::kSmem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(lstm_fwd2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd2::kSmemX) !=
             cudaSuccess) {
       cudaGetLastError();
       caps.err = 1;
       return caps;
     }
     const int sm = num_sms() >= 132 ? 128 : num_sms();
-    const int f = cluster_cap((const void*)lstm_fwd2_kernel, fwd2::kSmem, 2, fwd2::kThreadsF2);
+    const int f = cluster_cap((const void*)lstm_fwd2_kernel<false>, fwd2::kSmem, 2, fwd2::kThreadsF2);
     const int f3 = cluster_cap((const void*)lstm_fwd3_kernel, fwd3::kSmem, 2, fwd3::kThreadsF);
     const int b = cluster_cap((const void*)lstm_bwd_kernel, bwd::kSmem, 4);
     const int b3 = cluster_cap((const void*)lstm_bwd3_kernel, bwd3::kSmem, 8, bwd3::kThreads3);
@@ -1707,6 +1792,7 @@ int lstm_counter_words(int B) { return kFlagWords128 * ((B + 127) / 128); }
 static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
   if (rec_caps().err) return fail_arg("recurrent kernels: cannot set the shared-memory attribute");
   const int B = a.B, T = a.T;
+  if (fwd && use_fwd3() && a.xin) return fail_arg("the fused input projection runs in the 128-CTA forward");
   if (fwd && use_fwd3()) {
     // 32 CTAs (2 directions x 8 pairs x 2) per 128-row batch block
     const int max_blocks = rec_caps().fwd3_ctas / (2 * fwd3::kCtas);
@@ -1761,6 +1847,15 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
     P.err = a.err;
     P.B = B;
     P.T = T;
+    if (a.xin) {  // fused input projection: x rows (box 64 K x 32 rows) and W_ih rows (64 K x 128 rows)
+      if (!a.wih || !a.xbias) return fail_arg("fused input projection needs W_ih and the bias");
+      rc = make_tmap_2d(&P.tmX, a.xin, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kInPad, (uint64_t)T * B, kInPad * 2, 64,
+                        fwd2::kNH);
+      if (!rc)
+        rc = make_tmap_2d(&P.tmWi, a.wih, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kInPad, 8 * kH, kInPad * 2, 64, 128);
+      if (rc) return rc;
+      P.xbias = a.xbias;
+    }
     const int chunk_rows = max_blocks * fwd2::kNB;
     for (int b0 = 0; b0 < B; b0 += chunk_rows) {
       const int nb = (B - b0) < chunk_rows ? (B - b0) : chunk_rows;
@@ -1768,7 +1863,8 @@ static int lstm_run(bool fwd, const LstmLayerArgs& a, cudaStream_t stream) {
       P.nb = nb;
       P.n_btile = (nb + fwd2::kNB - 1) / fwd2::kNB;  // 64-row blocks
       P.counters = a.counters;
-      rc = launch_coop((const void*)lstm_fwd2_kernel, 2 * fwd2::kCtas * P.n_btile, P, stream, fwd2::kSmem, 2,
+      rc = launch_coop(P.xbias ? (const void*)lstm_fwd2_kernel<true> : (const void*)lstm_fwd2_kernel<false>,
+                       2 * fwd2::kCtas * P.n_btile, P, stream, P.xbias ? fwd2::kSmemX : fwd2::kSmem, 2,
                        fwd2::kThreadsF2);
       if (rc) return rc;
       P.trace = nullptr;  // trace only the first chunk

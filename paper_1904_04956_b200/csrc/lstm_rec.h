@@ -12,12 +12,14 @@ struct LstmParams {
   CUtensorMap tmW;  // W_hh [4096, 512] bf16 (forward: K-major B; backward: MN-major B)
   CUtensorMap tmG, tmC, tmDY;  // transposed BPTT: per-step cell inputs (gates, c_{t-1}, dY) staged by TMA
   CUtensorMap tmDY2;           //   second dY input (dY = dy + dy2), when dy2 != null
+  CUtensorMap tmX, tmWi;       // forward, fused input projection: X [N, 272] rows, W_ih [4096, 272]
   __nv_bfloat16* gates;
   float* cstate;
   __nv_bfloat16* y;
   const __nv_bfloat16* dy;
   __nv_bfloat16* dg;
   uint32_t* counters;
+  const float* xbias;  // forward, fused input projection (x_t W_ih^T + b in the recurrent MMA): b [4096]
   uint64_t* trace;  // optional per-(CTA, step) globaltimer marks (debug)
   float* dbpart;    // backward: optional [(B/128)*4][4096] bias-gradient partials
   int B, T, b0, nb, n_btile;
@@ -51,6 +53,12 @@ struct LstmLayerArgs {
   uint32_t* gate = nullptr;  // [2][T] per-(direction, time step) completion counters (lstm_bwd_gate_target)
   // backward: dY = dy + dy2 (the two per-direction halves of dX_{l+1}) when dy2 != null
   const __nv_bfloat16* dy2 = nullptr;
+  // forward: the input projection inside the recurrence (layer 0, K = 272): pre-activation =
+  // x_t W_ih^T (W_ih slice in tensor memory, x tiles staged a step ahead) + bias + h W_hh^T; `gates`
+  // then only receives the activations
+  const __nv_bfloat16* xin = nullptr;  // [T*B, 272] time-major
+  const __nv_bfloat16* wih = nullptr;  // [4096, 272] (zero-padded columns)
+  const float* xbias = nullptr;        // [4096]
   // dY streamed in by a GEMM still running: frame t of direction d's units of input i is complete once
   // dyready[(2t + d) * 2 + i] >= dyready_target (GemmProblem::ready with ready_rows = B, ready_cols = 512,
   // ready_stride = 2)

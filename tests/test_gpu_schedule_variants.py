@@ -10,6 +10,8 @@ recurrent kernels' 2-tile launches all run), 3 fused momentum steps.
   DS_BWD=1           round 1's split-K BPTT (128 CTAs, no streamed dX)
   DS_FWD=3           the 64-CTA forward recurrence (W_hh in tensor memory)
   DS_NO_SGD_MIRROR=1 the operand-snapshot extras as a pass at the end of the step
+  DS_FWD_XFUSE=0     layer 0's input projection as a GEMM before its recurrence (bf16 pre-activations
+                     instead of the fp32 accumulator)
 
 Bound: the same BF16 arithmetic in a different order (K splits, summation of the dY halves), so
 the trajectories agree to BF16 level: loss rel <= 1e-3, update rel <= 2e-2 over three steps,
@@ -63,8 +65,9 @@ def default_run(tmp_path_factory):
     ({"DS_DW0_EARLY": "0"}, False),
     ({"DS_DW1_ALL": "0"}, True),
     ({"DS_BWD": "1"}, False),
-    ({"DS_FWD": "3"}, True),
+    ({"DS_FWD": "3"}, False),  # (its layer 0 runs the input projection as a GEMM)
     ({"DS_NO_SGD_MIRROR": "1"}, True),
+    ({"DS_FWD_XFUSE": "0"}, False),
 ])
 def test_schedule_variant_matches_default(tmp_path, default_run, env, exact):
     got = _run(tmp_path, env, "variant")
