@@ -1536,13 +1536,12 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float2 a = __half22float2(h0[i]);
-            dh[2 * i] += a.x;
-            dh[2 * i + 1] += a.y;
+            fadd2(dh[2 * i], dh[2 * i + 1], dh[2 * i], dh[2 * i + 1], a.x, a.y);
           }
         }
         const float inv = 1.f / P.xscale;
 #pragma unroll
-        for (int i = 0; i < kCellRows; ++i) dh[i] *= inv;
+        for (int i = 0; i < kCellRows; i += 2) fmul2(dh[i], dh[i + 1], dh[i], dh[i + 1], inv, inv);
         named_bar_sync(3, kEpi * 32);  // every finaliser thread has read recv[buf]
         if (kEpiLead) {
           for (int f = 0; f < kKS; ++f)
@@ -1556,33 +1555,64 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
       if (P.trace && blockIdx.x == 0 && threadIdx.x == 0)
         P.trace[(size_t)gridDim.x * T * kTraceSlots + (size_t)T * 18 + 2 * s + 1] = globaltimer();
       uint2* dgp = reinterpret_cast<uint2*>(P.dg + ((size_t)t * B + brow0 + row0) * (8 * kH) + col_g);
+      // two rows per iteration on the packed fp32 pipe (FFMA2 / FMUL2 / FADD2): the same per-element
+      // operations in the same order as the scalar form (fma where it contracted), about half the
+      // float instructions of this issue-bound loop
 #pragma unroll
-      for (int i = 0; i < kCellRows; ++i) {
-        const bool ok = (okmask >> i) & 1u;
-        const uint2 actw = ld_shared_v2(cg_in + i * 256);
-        const float ig = __uint_as_float(actw.x << 16), fg = __uint_as_float(actw.x & 0xffff0000u);
-        const float gg = __uint_as_float(actw.y << 16), og = __uint_as_float(actw.y & 0xffff0000u);
-        float dyv = __uint_as_float(ld_shared_u16(cdy_in + i * 64) << 16);
-        if (P.dy2) dyv += __uint_as_float(ld_shared_u16(cdy_in + kInDY + i * 64) << 16);
-        const float cpv = has_cprev ? ld_shared_f32(cc_in + i * 128) : 0.f;
-        const float dht = dh[i] + dyv;
-        const float tcn = tanh_fast(cc[i]);
-        const float dct = fmaf(dht * og, 1.f - tcn * tcn, dcc[i]);
-        float dgv[4];
-        dgv[0] = dct * gg * ig * (1.f - ig);
-        dgv[1] = dct * cpv * fg * (1.f - fg);
-        dgv[2] = dct * ig * (1.f - gg * gg);
-        dgv[3] = dht * tcn * og * (1.f - og);
-        dcc[i] = dct * fg;
-        cc[i] = cpv;
-        if (ok) {
-          __nv_bfloat162 p0 = __floats2bfloat162_rn(dgv[0], dgv[1]), p1 = __floats2bfloat162_rn(dgv[2], dgv[3]);
-          uint2 w;
-          w.x = *reinterpret_cast<uint32_t*>(&p0);
-          w.y = *reinterpret_cast<uint32_t*>(&p1);
-          dgp[(size_t)i * (8 * kH / 4)] = w;
+      for (int i = 0; i < kCellRows; i += 2) {
+        const uint2 aw0 = ld_shared_v2(cg_in + i * 256), aw1 = ld_shared_v2(cg_in + (i + 1) * 256);
+        const float ig0 = __uint_as_float(aw0.x << 16), fg0 = __uint_as_float(aw0.x & 0xffff0000u);
+        const float gg0 = __uint_as_float(aw0.y << 16), og0 = __uint_as_float(aw0.y & 0xffff0000u);
+        const float ig1 = __uint_as_float(aw1.x << 16), fg1 = __uint_as_float(aw1.x & 0xffff0000u);
+        const float gg1 = __uint_as_float(aw1.y << 16), og1 = __uint_as_float(aw1.y & 0xffff0000u);
+        float dy0 = __uint_as_float(ld_shared_u16(cdy_in + i * 64) << 16);
+        float dy1 = __uint_as_float(ld_shared_u16(cdy_in + (i + 1) * 64) << 16);
+        if (P.dy2)
+          fadd2(dy0, dy1, dy0, dy1, __uint_as_float(ld_shared_u16(cdy_in + kInDY + i * 64) << 16),
+                __uint_as_float(ld_shared_u16(cdy_in + kInDY + (i + 1) * 64) << 16));
+        const float cp0 = has_cprev ? ld_shared_f32(cc_in + i * 128) : 0.f;
+        const float cp1 = has_cprev ? ld_shared_f32(cc_in + (i + 1) * 128) : 0.f;
+        float dht0, dht1, om0, om1, a0, a1, dct0, dct1;
+        fadd2(dht0, dht1, dh[i], dh[i + 1], dy0, dy1);
+        const float tc0 = tanh_fast(cc[i]), tc1 = tanh_fast(cc[i + 1]);
+        ffma2(om0, om1, -tc0, -tc1, tc0, tc1, 1.f, 1.f);  // 1 - tanh^2
+        fmul2(a0, a1, dht0, dht1, og0, og1);
+        ffma2(dct0, dct1, a0, a1, om0, om1, dcc[i], dcc[i + 1]);
+        float x0, x1, y0, y1, d0[4], d1[4];
+        // dg_i = dct gg ig (1 - ig)
+        fmul2(x0, x1, dct0, dct1, gg0, gg1);
+        fmul2(x0, x1, x0, x1, ig0, ig1);
+        fadd2(y0, y1, 1.f, 1.f, -ig0, -ig1);
+        fmul2(d0[0], d1[0], x0, x1, y0, y1);
+        // dg_f = dct c_{t-1} fg (1 - fg)
+        fmul2(x0, x1, dct0, dct1, cp0, cp1);
+        fmul2(x0, x1, x0, x1, fg0, fg1);
+        fadd2(y0, y1, 1.f, 1.f, -fg0, -fg1);
+        fmul2(d0[1], d1[1], x0, x1, y0, y1);
+        // dg_g = dct ig (1 - gg^2)
+        fmul2(x0, x1, dct0, dct1, ig0, ig1);
+        ffma2(y0, y1, -gg0, -gg1, gg0, gg1, 1.f, 1.f);
+        fmul2(d0[2], d1[2], x0, x1, y0, y1);
+        // dg_o = dh tanh(c) og (1 - og)
+        fmul2(x0, x1, dht0, dht1, tc0, tc1);
+        fmul2(x0, x1, x0, x1, og0, og1);
+        fadd2(y0, y1, 1.f, 1.f, -og0, -og1);
+        fmul2(d0[3], d1[3], x0, x1, y0, y1);
+        fmul2(dcc[i], dcc[i + 1], dct0, dct1, fg0, fg1);
+        cc[i] = cp0;
+        cc[i + 1] = cp1;
 #pragma unroll
-          for (int g = 0; g < 4; ++g) db[g] += dgv[g];
+        for (int h = 0; h < 2; ++h) {
+          const float* dg = h ? d1 : d0;
+          if ((okmask >> (i + h)) & 1u) {
+            __nv_bfloat162 p0 = __floats2bfloat162_rn(dg[0], dg[1]), p1 = __floats2bfloat162_rn(dg[2], dg[3]);
+            uint2 w;
+            w.x = *reinterpret_cast<uint32_t*>(&p0);
+            w.y = *reinterpret_cast<uint32_t*>(&p1);
+            dgp[(size_t)(i + h) * (8 * kH / 4)] = w;
+            fadd2(db[0], db[1], db[0], db[1], dg[0], dg[1]);
+            fadd2(db[2], db[3], db[2], db[3], dg[2], dg[3]);
+          }
         }
       }
       if (e == 0 && lane == 0) trace_mark(P.trace, T, s, 3);

@@ -6,7 +6,9 @@ import ctypes
 import os
 import sys
 
-os.environ["DS_TIMELINE"] = "1"
+TL = "--no-timeline" not in sys.argv
+if TL:
+    os.environ["DS_TIMELINE"] = "1"
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -36,18 +38,28 @@ def direct(k, ptr=None):  # the C ABI call alone
 
 
 for name, fn in (("train_step(device_idx)", lambda k: L.train_step(dev[k % 8], 0.01, device_idx=True)),
+                 ("  ..current stream default", None),
                  ("train_step(same tensor)", lambda k: L.train_step(dev[0], 0.01, device_idx=True)),
                  ("ABI, one index buffer", direct),
                  ("ABI, 8 index buffers", lambda k: direct(k, dev[k % 8].data_ptr()))):
     n = 40
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
-    with torch.cuda.stream(L.stream):
+    if fn is None:  # the bench's call: indices produced before the loop, caller on the default stream
         for k in range(n):
             ev[k].record(L.stream)
-            fn(k)
+            L.train_step(dev[k % 8], 0.01, device_idx=True)
         ev[n].record(L.stream)
+    else:
+        with torch.cuda.stream(L.stream):  # the caller's stream is the learner's: the index copy waits for
+            for k in range(n):             # the previous step (wait_stream), serialising it behind it
+                ev[k].record(L.stream)
+                fn(k)
+            ev[n].record(L.stream)
     torch.cuda.synchronize()
     per = [ev[k].elapsed_time(ev[k + 1]) * 1e3 for k in range(n)]
+    if not TL:
+        print(f"{name:26s}: period median {np.median(per[5:]):8.1f} us")
+        continue
     buf = ctypes.create_string_buffer(1 << 16)
     _lib.check(lib.ds_debug_timeline(L.handle, buf, len(buf)), "timeline")
     marks = {}
