@@ -1205,6 +1205,7 @@ constexpr int kInDY = kRows * kFin * 2;     // 8 KB per dY input (dY, or the two
 constexpr size_t kSmem = 1024 + kRingBytes + 2 * kRecvBuf + kSendBytes + kInG + kInC + 2 * kInDY + 256;
 static_assert(kWBytes <= kRingBytes + 2 * kRecvBuf + kSendBytes, "W staging must fit in the ring + recv + send region");
 static_assert(kSmem <= 232448, "shared memory");
+static_assert(kChunks == kStages + 1, "producer lanes: chunk 7 reuses the stage of the same step's chunk 0");
 constexpr uint32_t kACol = 256;            // A = W^T slice at TMEM columns 256..511 (two bf16 per column)
 constexpr int kEpi = 16;                   // epilogue warps 0..15 (warp % 4 = TMEM lane quadrant)
 constexpr int kProdWarp = 16, kMmaWarp = 17;  // TMA producer, MMA issuer (+ TMEM allocation)
@@ -1343,43 +1344,43 @@ __global__ void __launch_bounds__(bwd3::kThreads3, 1) lstm_bwd3_kernel(const __g
   const uint32_t base = s_base;  // flag value at launch start (same for every flag of the group)
 
   if (warp == kProdWarp) {
-    if (elect_one()) {
+    // lane j stages chunk j of every step: the chunks' stage waits, byte counts, flag polls and TMA
+    // issues run side by side (one issuing thread spent ~260 cycles per chunk on them in sequence,
+    // ~1.1 us per step before the last chunk was in flight).  Parity waits on the 7-stage ring stay
+    // sound as long as a stage's previous use was issued before its next wait: chunks 0..6 of a step
+    // reuse stages of the previous step's chunks 1..7 (issued before the step's first __syncwarp), and
+    // chunk 7 reuses the stage of the same step's chunk 0, so it waits after the lanes 0..6 issued.
+    const int j = (int)lane;
+    if (j < kChunks) {
       const uint32_t full_c = mapa_shared(smem_u32(full), pair0);
-      const uint32_t* seg = flags + ks * kFlagLine;  // the 4 producers of slice ks (2 chunks each)
-      int stage = 0;
-      uint32_t phase = 0;
+      const uint32_t* word = flags + ks * kFlagLine + (j >> 1);  // producer of my chunk (2 chunks each)
       for (int s = 1; s < T; ++s) {
         const int t = dir == 0 ? T - 1 - s : s;
         const int tprev = dir == 0 ? t + 1 : t - 1;
         const int arow = tprev * B + brow0 + r * kHalfRows;
-        uint4 fv = make_uint4(0u, 0u, 0u, 0u);
-        bool fresh = false;  // the segment is re-read at least once per step (wrap-safe compare)
-        for (int j = 0; j < kChunks; ++j) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kChunk);
-          const uint32_t target = base + (uint32_t)s;
-          const int w = j >> 1;
-          if (!fresh || !reached(w == 0 ? fv.x : w == 1 ? fv.y : w == 2 ? fv.z : fv.w, target)) {
-            SpinGuard g;
-            while (true) {
-              fv = ld_acquire_gpu_v4(seg);
-              fresh = true;
-              if (reached(w == 0 ? fv.x : w == 1 ? fv.y : w == 2 ? fv.z : fv.w, target) || spin_expired(g, P.err))
-                break;
+        const int g = (s - 1) * kChunks + j;  // running chunk count: ring stage and phase
+        const int stage = g % kStages;
+#pragma unroll 1
+        for (int round = 0; round < 2; ++round) {
+          if ((j == kChunks - 1) == (round == 1)) {
+            mbar_wait(&empty[stage], ((uint32_t)(g / kStages) & 1u) ^ 1u);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kChunk);
+            const uint32_t target = base + (uint32_t)s;
+            if (!reached(ld_acquire_gpu(word), target)) {
+              SpinGuard sg;
+              while (!reached(ld_acquire_gpu(word), target))
+                if (spin_expired(sg, P.err)) break;
             }
+            fence_proxy_async_global();
+            if (j == 0) trace_mark(P.trace, T, s, 0);
+            tma_load_2d_pair(ring + stage * kChunk, &P.tmA, full_c + (uint32_t)stage * 8,
+                             dir * 4 * kH + ks * kSlice + j * 64, arow);
+            if (P.trace && blockIdx.x == 0)
+              P.trace[(size_t)gridDim.x * T * kTraceSlots + ((size_t)s * 8 + j) * 2] = globaltimer();
+            if (j == kChunks - 1) trace_mark(P.trace, T, s, 1);
           }
-          fence_proxy_async_global();
-          if (j == 0) trace_mark(P.trace, T, s, 0);
-          tma_load_2d_pair(ring + stage * kChunk, &P.tmA, full_c + (uint32_t)stage * 8,
-                           dir * 4 * kH + ks * kSlice + j * 64, arow);
-          if (P.trace && blockIdx.x == 0)
-            P.trace[(size_t)gridDim.x * T * kTraceSlots + ((size_t)s * 8 + j) * 2] = globaltimer();
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+          __syncwarp(0xffu);
         }
-        trace_mark(P.trace, T, s, 1);
       }
     }
   } else if (warp == kMmaWarp) {
