@@ -547,14 +547,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                             "soft-max/dZ kernels)",
                   "achieved": round(gemm_tfs, 1), "peak": burst, "unit": "TFLOP/s", "frac": round(gemm_tfs / burst, 4),
                   "traffic": traffic, "algorithmic_flop_per_step": gemm_flops}
-    # the dominant kernel of the launch list (profiles/r2f_launches.csv: 34.6 %): the BPTT
+    # the dominant kernel of the launch list (profiles/r2h_launches.csv: 34.9 %): the BPTT
     # (lstm_bwd3_kernel, the transposed CTA-pair recurrence, one launch per layer)
     bwd_flop = 2.0 * N * (8 * 512) * 512  # dh = dG W_hh, both directions
     bwd_ms = ph["lstm_bwd"] / obj.layers if ph["lstm_bwd"] > 0 else 0.0
     bwd_tfs = bwd_flop / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else 0.0
     bwd_traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r2f_kernel_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2h_kernel_traffic.json")) as f:
             kt = json.load(f)
         if B == 256 and obj.layers == 6 and "lstm_bwd3_kernel" in kt:
             bwd_traffic = kt["lstm_bwd3_kernel"]["dram_bytes_per_launch"]

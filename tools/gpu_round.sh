@@ -12,8 +12,10 @@ tests)  timeout 1200 python -m pytest tests -m gpu -x -q > $O/${TAG}_pytest_gpu.
 smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" ;;
 bench)  timeout 600 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err; echo "bench rc=$?"; cat $O/${TAG}_bench.json ;;
 ref)    timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/${TAG}_bench_ref.json 2>&1; echo "ref rc=$?"; cat $O/${TAG}_bench_ref.json ;;
-launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
-          --log-file $O/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --n-seq 4096 \
+launches) # ncu serialises launches: the bench's gated side streams would wait on kernels that cannot run
+          # beside them, so the launch list comes from the profiling-mode step (same kernels, GEMMs in order)
+          timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+          --log-file $O/${TAG}_launches.csv python tools/phase_profile.py \
           > $O/${TAG}_launches_bench.log 2>&1; echo "launches rc=$?" ;;
 full)   for k in lstm_bwd lstm_fwd gemm_kernel sgd_kernel; do
           timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 2 \

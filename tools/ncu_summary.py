@@ -34,8 +34,11 @@ def launches(path):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h, data = rows[hi], rows[hi + 1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     seq = []
     for r in data:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":  # a multi-metric capture (e.g. + DRAM bytes)
+            continue
         v = float(r[vi].replace(",", ""))
         u = r[ui]
         v = v / 1000 if u in ("nsecond", "ns") else v * 1000 if u == "msecond" else v
